@@ -1,0 +1,456 @@
+/*
+ * sf_oracle.c -- plain, slow, single-threaded CPU oracle of the structure-flow
+ * filter's per-frame predictor-update loop (Adarve & Mahony, arXiv 2406.18031).
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs may load this library.  It shares no code,
+ * header, table or constant with the CUDA library under paper_2406_18031_b200/;
+ * the only thing both sides consume in common is the seeded input data produced
+ * by sfgen/ (grid geometry, brightness, depth, run parameters).
+ *
+ * Compiled twice (see oracle/build.py):
+ *   liboracle_f32.so  -DOR_F32   every value and every decision in IEEE float32;
+ *                                this is the parity oracle, because the paper fixes
+ *                                no precision and the discontinuous decisions
+ *                                (dominant flow, upwind side, rho one-sided
+ *                                difference) must be taken in the kernel's precision.
+ *   liboracle_f64.so  (default)  the same algorithm in float64; pins the float32
+ *                                build's rounding drift.
+ * Build flags: -O2 -ffp-contract=off (no implicit FMA); every fused multiply-add
+ * is an explicit fma() call, written where the formula is "a*b + c".
+ *
+ * Notation follows the paper; line numbers cite /root/reference/PAPER.md.
+ * Readings of ambiguous passages are numbered as in DESIGN.md section 3
+ * ("Readings"); the arithmetic order below IS the definition the CUDA path
+ * reproduces.
+ *
+ * Parity status: every function below is pinned by tests/test_oracle_*.py except
+ * the full multi-frame trajectory on scenes with occlusions and an active flow
+ * clamp, which is pinned only by invariants (C1-C7) and f32-vs-f64 agreement
+ * (DESIGN.md "Parity unpinned").
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#ifdef OR_F32
+typedef float real;
+#define FMA fmaf
+#define FABS fabsf
+#define FMIN fminf
+#define FMAX fmaxf
+#else
+typedef double real;
+#define FMA fma
+#define FABS fabs
+#define FMIN fmin
+#define FMAX fmax
+#endif
+#define R(x) ((real)(x))
+
+#define OR_FLAG_CLAMPED 1u   /* |u_hat| exceeded max_flow and was clamped (reading 12) */
+#define OR_FLAG_NONFINITE 2u /* a non-finite value appeared in the inputs Y or the state */
+#define OR_FLAG_CFL 4u       /* clamp disabled and dt*|u_hat| > 1 (eq:numerical_stability) */
+
+#define OR_DOM_LARGEST 0
+#define OR_DOM_PRINTED 1
+
+/* Run parameters, a fixed C layout independent of `real`. */
+typedef struct {
+    int32_t H, W;
+    int32_t N;                      /* substeps, N = ceil(max_flow) (L684-689)           */
+    int32_t smooth_iters;           /* S, 5x5 box passes after the solve (L590, L796)    */
+    int32_t dominant_rule;          /* OR_DOM_LARGEST (reading 1) or OR_DOM_PRINTED       */
+    int32_t clamp_advection;        /* 1: clamp u_hat to +-max_flow (reading 12)          */
+    int32_t input_is_inverse_depth; /* 0: depth lambda in metres (L463); 1: rho given     */
+    int32_t pad;
+    double max_flow;
+    double sigma;    /* source-term weight per pass (reading 2; 0.5)                     */
+    double gamma[5]; /* gamma1..gamma5 (L556-559, L613-616)                               */
+} or_params;
+
+static inline int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
+
+/* <a, x> accumulated x, then y, then z: fma(a.z, x.z, fma(a.y, x.y, a.x * x.x)). */
+static inline real dot3(const real* a, const real* x) { return FMA(a[2], x[2], FMA(a[1], x[1], a[0] * x[0])); }
+
+/* ------------------------------------------------------------------ geometry
+ * Per-grid working geometry geo[p][10] = (s, e1, e2, d2) from the Spherepix input
+ * (s, b1, b2, ds) (L406-437):  e_k = b_k / ds  (so that Phi = (1/ds) B^T w = (e1.w, e2.w),
+ * eq:oflow_numeric L639-642, reading 5), d2 = ds * ds.
+ */
+void or_geometry(int H, int W, const float* g10, real* geo)
+{
+    for (long p = 0; p < (long)H * W; ++p) {
+        const float* g = g10 + 10 * p;
+        real* o = geo + 10 * p;
+        real ds = R(g[9]);
+        for (int a = 0; a < 3; ++a) {
+            o[a] = R(g[a]);
+            o[3 + a] = R(g[3 + a]) / ds;
+            o[6 + a] = R(g[6 + a]) / ds;
+        }
+        o[9] = ds * ds;
+    }
+}
+
+/* ------------------------------------------------------------------ predict (P1-P5)
+ * One transport pass along one axis for all pixels (Jacobi: every read is a pre-pass value).
+ *   axis 0 = column pass (beta_1, neighbours (i, j+-1), e = e1), L663-673;
+ *   axis 1 = row pass    (beta_2, neighbours (i+-1, j), e = e2), L674-683 (reading 3).
+ * For each pixel p:
+ *   u_p  = <e_p, w_p>                                    optical flow in px, eq:oflow_numeric
+ *   u_hat = dominant(u_{p-}, u_{p+})                      L643-650 (reading 1)
+ *   u_hat = clamp(u_hat, -U, U)                           reading 12
+ *   D(f) = f_p - f_{p-} if u_hat > 0 else f_{p+} - f_p    upwind operator, L652-658, table
+ *   f*_p = f_p - dt [ u_hat D(f) + f_p sigma <s_p, w_p> ] for f in (w.x, w.y, w.z, rho), L665-669
+ * with replicate (clamp-to-edge) neighbours at the border (reading 10).
+ * Arithmetic: t = fma(u_hat, D, f * (sigma*sw)); f* = fma(-dt, t, f).
+ */
+static unsigned pass(const or_params* P, const real* geo, int axis, const real* w, const real* rho, real* wo,
+                     real* rhoo, real* u)
+{
+    const int H = P->H, W = P->W;
+    const real U = R(P->max_flow), sigma = R(P->sigma), dt = R(1) / R(P->N);
+    unsigned flags = 0;
+    for (long p = 0; p < (long)H * W; ++p) u[p] = dot3(geo + 10 * p + 3 + 3 * axis, w + 3 * p);
+    for (int i = 0; i < H; ++i) {
+        for (int j = 0; j < W; ++j) {
+            const long p = (long)i * W + j;
+            long pm, pp;
+            if (axis == 0) {
+                pm = (long)i * W + clampi(j - 1, 0, W - 1);
+                pp = (long)i * W + clampi(j + 1, 0, W - 1);
+            } else {
+                pm = (long)clampi(i - 1, 0, H - 1) * W + j;
+                pp = (long)clampi(i + 1, 0, H - 1) * W + j;
+            }
+            const real um = u[pm], up = u[pp];
+            real uh;
+            if (P->dominant_rule == OR_DOM_PRINTED)
+                uh = (FABS(up) - FABS(um) > R(0)) ? um : up; /* as printed: delta^c |u| > 0 -> u_{j-1} */
+            else
+                uh = (FABS(um) > FABS(up)) ? um : up; /* largest magnitude, ties -> u_{j+1} */
+            if (P->clamp_advection) {
+                if (FABS(uh) > U) flags |= OR_FLAG_CLAMPED;
+                uh = FMIN(FMAX(uh, -U), U);
+            } else if (dt * FABS(uh) > R(1)) {
+                flags |= OR_FLAG_CFL;
+            }
+            const real sw = dot3(geo + 10 * p, w + 3 * p); /* <s, w^n> at p */
+            const real q = sigma * sw;
+            real f[4] = {w[3 * p], w[3 * p + 1], w[3 * p + 2], rho[p]};
+            real fm[4] = {w[3 * pm], w[3 * pm + 1], w[3 * pm + 2], rho[pm]};
+            real fp[4] = {w[3 * pp], w[3 * pp + 1], w[3 * pp + 2], rho[pp]};
+            real out[4];
+            for (int c = 0; c < 4; ++c) {
+                const real D = (uh > R(0)) ? (f[c] - fm[c]) : (fp[c] - f[c]);
+                out[c] = FMA(-dt, FMA(uh, D, f[c] * q), f[c]);
+            }
+            wo[3 * p] = out[0];
+            wo[3 * p + 1] = out[1];
+            wo[3 * p + 2] = out[2];
+            rhoo[p] = out[3];
+        }
+    }
+    return flags;
+}
+
+/* Prediction k -> k+ (L501-523, numerical scheme L662-683): exactly N substeps
+ * (reading 4), each a column pass then a row pass.  In place on (w, rho). */
+unsigned or_predict(const or_params* P, const real* geo, real* w, real* rho)
+{
+    const long n = (long)P->H * P->W;
+    real* w2 = malloc(sizeof(real) * 3 * n);
+    real* r2 = malloc(sizeof(real) * n);
+    real* u = malloc(sizeof(real) * n);
+    unsigned flags = 0;
+    for (int s = 0; s < P->N; ++s) {
+        flags |= pass(P, geo, 0, w, rho, w2, r2, u);
+        flags |= pass(P, geo, 1, w2, r2, w, rho, u);
+    }
+    free(w2);
+    free(r2);
+    free(u);
+    return flags;
+}
+
+/* ------------------------------------------------------------------ update models (U1, U2)
+ * Brightness model (L442-457, eq:img_model, eq:img_gradient).  The 5x5 Gaussian-weighted
+ * LS fit of Y_q ~ Yhat_p + beta . (q - p) (reading 7: offset q - p) has, because
+ * sum g = 1, sum g k = 0, sum g k^2 = 1 for g = [1,4,6,4,1]/16, the closed form
+ *   Yhat = (g x g) * Y,  beta1 = (g along i) x (h along j) * Y,  beta2 = (h along i) x (g along j) * Y
+ * with h_k = k g_k = [-1,-2,0,2,1]/8, taps in offset order k = -2..2, as separable 1-D
+ * convolutions (L452).  Horizontal pass first, then vertical; replicate border.
+ * Each 1-D tap sum: acc = k_{-2} x_{-2}; acc = fma(k_t, x_t, acc) for t = -1..2.
+ * Lift (eq:img_gradient, reading 5): ghat = ds B beta = d2 (e1 beta1 + e2 beta2),
+ * per component  ghat_a = d2 * fma(e2_a, beta2, e1_a * beta1).
+ */
+static const double G5[5] = {0.0625, 0.25, 0.375, 0.25, 0.0625};
+static const double H5[5] = {-0.125, -0.25, 0.0, 0.25, 0.125};
+
+static void conv_h(int H, int W, const real* k5, const real* x, real* out)
+{
+    for (int i = 0; i < H; ++i)
+        for (int j = 0; j < W; ++j) {
+            const real* row = x + (long)i * W;
+            real acc = k5[0] * row[clampi(j - 2, 0, W - 1)];
+            for (int t = 1; t < 5; ++t) acc = FMA(k5[t], row[clampi(j + t - 2, 0, W - 1)], acc);
+            out[(long)i * W + j] = acc;
+        }
+}
+
+static void conv_v(int H, int W, const real* k5, const real* x, real* out)
+{
+    for (int i = 0; i < H; ++i)
+        for (int j = 0; j < W; ++j) {
+            real acc = k5[0] * x[(long)clampi(i - 2, 0, H - 1) * W + j];
+            for (int t = 1; t < 5; ++t) acc = FMA(k5[t], x[(long)clampi(i + t - 2, 0, H - 1) * W + j], acc);
+            out[(long)i * W + j] = acc;
+        }
+}
+
+void or_brightness_model(int H, int W, const float* Y, const real* geo, real* yhat, real* beta1, real* beta2,
+                         real* ghat)
+{
+    const long n = (long)H * W;
+    real g[5], h[5];
+    for (int t = 0; t < 5; ++t) {
+        g[t] = R(G5[t]);
+        h[t] = R(H5[t]);
+    }
+    real* y = malloc(sizeof(real) * n);
+    real* hg = malloc(sizeof(real) * n);
+    real* hh = malloc(sizeof(real) * n);
+    for (long p = 0; p < n; ++p) y[p] = R(Y[p]);
+    conv_h(H, W, g, y, hg);
+    conv_h(H, W, h, y, hh);
+    conv_v(H, W, g, hg, yhat);
+    conv_v(H, W, g, hh, beta1);
+    conv_v(H, W, h, hg, beta2);
+    for (long p = 0; p < n; ++p) {
+        const real* e1 = geo + 10 * p + 3;
+        const real* e2 = geo + 10 * p + 6;
+        const real d2 = geo[10 * p + 9];
+        for (int a = 0; a < 3; ++a) ghat[3 * p + a] = d2 * FMA(e2[a], beta2[p], e1[a] * beta1[p]);
+    }
+    free(y);
+    free(hg);
+    free(hh);
+}
+
+/* Inverse-depth model (L460-499, eq:dominant_b1/b2, table:diff_operators, eq:inv_depth_gradient).
+ *   valid = isfinite(lambda) && lambda > 0;  rhohat = 1 / lambda  (eq:inv_depth, lambda_ref = 1 m, L173)
+ *   per axis: d+ = rho_{p+} - rho_p, d- = rho_p - rho_{p-};  beta_rho = d+ if |d+| <= |d-| else d-
+ *   (reading 14: an invalid neighbour's difference drops out; both invalid -> 0; invalid p -> 0)
+ *   drho = d2 * fma(e2, beta_rho2, e1 * beta_rho1)   (lift as for ghat, reading 5)
+ */
+static real pick_side(const real* rh, const unsigned char* v, long p, long pm, long pp)
+{
+    if (!v[p]) return R(0);
+    const int hp = v[pp], hm = v[pm];
+    const real dp = rh[pp] - rh[p];
+    const real dm = rh[p] - rh[pm];
+    if (hp && hm) return (FABS(dp) <= FABS(dm)) ? dp : dm;
+    if (hp) return dp;
+    if (hm) return dm;
+    return R(0);
+}
+
+void or_invdepth_model(int H, int W, const float* depth, int is_inverse, const real* geo, real* rhohat,
+                       unsigned char* valid, real* beta_r1, real* beta_r2, real* drho)
+{
+    const long n = (long)H * W;
+    for (long p = 0; p < n; ++p) {
+        const real x = R(depth[p]);
+        const int ok = is_inverse ? (isfinite(x) && x >= R(0)) : (isfinite(x) && x > R(0));
+        valid[p] = (unsigned char)ok;
+        rhohat[p] = ok ? (is_inverse ? x : R(1) / x) : R(0);
+    }
+    for (int i = 0; i < H; ++i)
+        for (int j = 0; j < W; ++j) {
+            const long p = (long)i * W + j;
+            const real b1 =
+                pick_side(rhohat, valid, p, (long)i * W + clampi(j - 1, 0, W - 1), (long)i * W + clampi(j + 1, 0, W - 1));
+            const real b2 =
+                pick_side(rhohat, valid, p, (long)clampi(i - 1, 0, H - 1) * W + j, (long)clampi(i + 1, 0, H - 1) * W + j);
+            beta_r1[p] = b1;
+            beta_r2[p] = b2;
+            const real* e1 = geo + 10 * p + 3;
+            const real* e2 = geo + 10 * p + 6;
+            const real d2 = geo[10 * p + 9];
+            for (int a = 0; a < 3; ++a) drho[3 * p + a] = d2 * FMA(e2[a], b2, e1[a] * b1);
+        }
+}
+
+/* ------------------------------------------------------------------ update solve (U3)
+ * Per-pixel regularised LS (L552-588, eq:cost_top, eq:img_cost_top, eq:invdepth_cost_top,
+ * eq:LS_update), with E_t = w - w^{k+} (reading 8) and P(s) dropped (reading 16):
+ *   E_Y = ghat . w + cY,  E_rho = m . w + crho,  E_t = w - wp
+ *   A = g3 I + g1 ghat ghat^T + g2 m m^T,   b = g3 wp - g1 cY ghat - g2 crho m
+ * A is SPD (lambda_min >= g3 > 0); solved by LDL^T without pivoting (reading 17):
+ *   entries  A_ab = fma(g2 m_a, m_b, (g1 g_a) g_b),  A_aa += g3
+ *            b_a  = fma(-(g2 m_a), crho, fma(-(g1 g_a), cY, g3 wp_a))
+ *   factor   r0 = 1/A00; l10 = A10 r0; l20 = A20 r0; d1 = fma(-l10, A10, A11); r1 = 1/d1;
+ *            t = fma(-l20, A10, A21); l21 = t r1; d2 = fma(-l21, t, fma(-l20, A20, A22)); r2 = 1/d2
+ *   forward  y1 = fma(-l10, b0, b1); y2 = fma(-l21, y1, fma(-l20, b0, b2))
+ *   back     x2 = y2 r2; x1 = fma(-l21, x2, y1 r1); x0 = fma(-l20, x2, fma(-l10, x1, b0 r0))
+ */
+static void ls_solve(const real* g, const real* m, real cY, real cr, const real* wp, real g1, real g2, real g3,
+                     real* x)
+{
+    real g1g[3], g2m[3], A[3][3], b[3];
+    for (int a = 0; a < 3; ++a) {
+        g1g[a] = g1 * g[a];
+        g2m[a] = g2 * m[a];
+    }
+    for (int a = 0; a < 3; ++a)
+        for (int c = 0; c <= a; ++c) A[a][c] = FMA(g2m[a], m[c], g1g[a] * g[c]);
+    for (int a = 0; a < 3; ++a) {
+        A[a][a] = A[a][a] + g3;
+        b[a] = FMA(-g2m[a], cr, FMA(-g1g[a], cY, g3 * wp[a]));
+    }
+    const real r0 = R(1) / A[0][0];
+    const real l10 = A[1][0] * r0, l20 = A[2][0] * r0;
+    const real d1 = FMA(-l10, A[1][0], A[1][1]);
+    const real r1 = R(1) / d1;
+    const real t = FMA(-l20, A[1][0], A[2][1]);
+    const real l21 = t * r1;
+    const real d2 = FMA(-l21, t, FMA(-l20, A[2][0], A[2][2]));
+    const real r2 = R(1) / d2;
+    const real y1 = FMA(-l10, b[0], b[1]);
+    const real y2 = FMA(-l21, y1, FMA(-l20, b[0], b[2]));
+    x[2] = y2 * r2;
+    x[1] = FMA(-l21, x[2], y1 * r1);
+    x[0] = FMA(-l20, x[2], FMA(-l10, x[1], b[0] * r0));
+}
+
+/* Batch entry point for the L1 pin: n independent pixel systems; gam = (g1, g2, g3). */
+void or_ls_solve_batch(long n, const real* g, const real* m, const real* cY, const real* cr, const real* wp,
+                       const double* gam, real* out)
+{
+    for (long p = 0; p < n; ++p)
+        ls_solve(g + 3 * p, m + 3 * p, cY[p], cr[p], wp + 3 * p, R(gam[0]), R(gam[1]), R(gam[2]), out + 3 * p);
+}
+
+/* ------------------------------------------------------------------ smoothing (U4)
+ * "average smoothing filter of size 5x5" applied S times to w after the solve (L590, L796,
+ * reading 13): each iteration a horizontal 5-sum (left to right, replicate border), then a
+ * vertical 5-sum (top to bottom), then division by 25.
+ */
+void or_smooth(int H, int W, int S, real* w)
+{
+    const long n = (long)H * W;
+    real* t = malloc(sizeof(real) * 3 * n);
+    for (int it = 0; it < S; ++it) {
+        for (int i = 0; i < H; ++i)
+            for (int j = 0; j < W; ++j)
+                for (int a = 0; a < 3; ++a) {
+                    real acc = w[3 * ((long)i * W + clampi(j - 2, 0, W - 1)) + a];
+                    for (int k = -1; k <= 2; ++k) acc = acc + w[3 * ((long)i * W + clampi(j + k, 0, W - 1)) + a];
+                    t[3 * ((long)i * W + j) + a] = acc;
+                }
+        for (int i = 0; i < H; ++i)
+            for (int j = 0; j < W; ++j)
+                for (int a = 0; a < 3; ++a) {
+                    real acc = t[3 * ((long)clampi(i - 2, 0, H - 1) * W + j) + a];
+                    for (int k = -1; k <= 2; ++k) acc = acc + t[3 * ((long)clampi(i + k, 0, H - 1) * W + j) + a];
+                    w[3 * ((long)i * W + j) + a] = acc / R(25);
+                }
+    }
+    free(t);
+}
+
+/* ------------------------------------------------------------------ update (U1-U6)
+ * k+ -> k+1 (L546-621).  State (w, rho, yhat) holds frame k on entry and k+1 on exit;
+ * (wp, rhop) is the prediction k+.  Temporal references are yhat^k (L564) and rho^k (L572),
+ * reading 9.  init != 0: first frame (L750): w = 0, rho = rhohat (0 where invalid), yhat = Yhat.
+ * Fusion (L609-621): rho = rho^{k+} + kappa (rhohat - rho^{k+}), kappa = g4/(g4+g5), 0 where invalid,
+ * computed as fma(kappa, rhohat - rhop, rhop).
+ */
+unsigned or_update(const or_params* P, const real* geo, const float* Y, const float* depth, const real* wp,
+                   const real* rhop, real* w, real* rho, real* yhat, int init)
+{
+    const int H = P->H, W = P->W;
+    const long n = (long)H * W;
+    unsigned flags = 0;
+    real* yh1 = malloc(sizeof(real) * n);
+    real* b1 = malloc(sizeof(real) * n);
+    real* b2 = malloc(sizeof(real) * n);
+    real* ghat = malloc(sizeof(real) * 3 * n);
+    real* rh = malloc(sizeof(real) * n);
+    real* br1 = malloc(sizeof(real) * n);
+    real* br2 = malloc(sizeof(real) * n);
+    real* drho = malloc(sizeof(real) * 3 * n);
+    unsigned char* valid = malloc(n);
+    for (long p = 0; p < n; ++p)
+        if (!isfinite(Y[p])) flags |= OR_FLAG_NONFINITE;
+    or_brightness_model(H, W, Y, geo, yh1, b1, b2, ghat);
+    or_invdepth_model(H, W, depth, P->input_is_inverse_depth, geo, rh, valid, br1, br2, drho);
+    if (init) {
+        for (long p = 0; p < n; ++p) {
+            w[3 * p] = w[3 * p + 1] = w[3 * p + 2] = R(0);
+            rho[p] = rh[p];
+            yhat[p] = yh1[p];
+        }
+    } else {
+        const real g1 = R(P->gamma[0]), g2v = R(P->gamma[1]), g3 = R(P->gamma[2]);
+        const real kap = R(P->gamma[3]) / (R(P->gamma[3]) + R(P->gamma[4]));
+        real* wls = malloc(sizeof(real) * 3 * n);
+        for (long p = 0; p < n; ++p) {
+            const real* s = geo + 10 * p;
+            const real d2 = geo[10 * p + 9];
+            const real d2r = d2 * rh[p];
+            real m[3];
+            for (int a = 0; a < 3; ++a) m[a] = FMA(d2r, s[a], drho[3 * p + a]);
+            const real cY = d2 * (yh1[p] - yhat[p]);
+            const real cr = d2 * (rh[p] - rho[p]);
+            ls_solve(ghat + 3 * p, m, cY, cr, wp + 3 * p, g1, valid[p] ? g2v : R(0), g3, wls + 3 * p);
+        }
+        or_smooth(H, W, P->smooth_iters, wls);
+        for (long p = 0; p < n; ++p) {
+            for (int a = 0; a < 3; ++a) w[3 * p + a] = wls[3 * p + a];
+            const real kappa = valid[p] ? kap : R(0);
+            rho[p] = FMA(kappa, rh[p] - rhop[p], rhop[p]);
+            yhat[p] = yh1[p];
+        }
+        free(wls);
+    }
+    for (long p = 0; p < n; ++p)
+        if (!isfinite(w[3 * p]) || !isfinite(w[3 * p + 1]) || !isfinite(w[3 * p + 2]) || !isfinite(rho[p]))
+            flags |= OR_FLAG_NONFINITE;
+    free(yh1);
+    free(b1);
+    free(b2);
+    free(ghat);
+    free(rh);
+    free(br1);
+    free(br2);
+    free(drho);
+    free(valid);
+    return flags;
+}
+
+/* One frame k -> k+1: predict (P1-P5) then update (U1-U6), Fig. 3a (L385, L397-401).
+ * init != 0 runs only the first-frame initialisation.  If wp_out/rhop_out are non-NULL the
+ * prediction (w^{k+}, rho^{k+}) is copied there. */
+unsigned or_step(const or_params* P, const real* geo, const float* Y, const float* depth, real* w, real* rho,
+                 real* yhat, int init, real* wp_out, real* rhop_out)
+{
+    const long n = (long)P->H * P->W;
+    if (init) return or_update(P, geo, Y, depth, NULL, NULL, w, rho, yhat, 1);
+    real* wp = malloc(sizeof(real) * 3 * n);
+    real* rp = malloc(sizeof(real) * n);
+    memcpy(wp, w, sizeof(real) * 3 * n);
+    memcpy(rp, rho, sizeof(real) * n);
+    unsigned flags = or_predict(P, geo, wp, rp);
+    if (wp_out) memcpy(wp_out, wp, sizeof(real) * 3 * n);
+    if (rhop_out) memcpy(rhop_out, rp, sizeof(real) * n);
+    flags |= or_update(P, geo, Y, depth, wp, rp, w, rho, yhat, 0);
+    free(wp);
+    free(rp);
+    return flags;
+}
+
+int or_real_bytes(void) { return (int)sizeof(real); }
