@@ -1,0 +1,310 @@
+#!/usr/bin/env python3
+"""Benchmark: structure-flow predictor-update frames/s on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl sf|reference] [--config 2|3|4]
+
+One step = one frame k -> k+1 of the whole hot path (predict N substeps + update) for
+every sequence in the batch.  N = 1: configs[1] (512 x 512, max flow 8 px, S = 2, batch 1).
+N > 1 (torchrun, one process per GPU): each rank runs its own independent sequence, no
+data-path collective ("weak" scaling; value = frames of all ranks / max-over-ranks time).
+
+Inputs: a ring of R distinct frames resident in HBM (R x 2 MiB > the 126 MB L2), so each
+step reads cold brightness/depth; steps are replayed from per-frame CUDA graphs captured on
+the context stream.  Timing: CUDA events on that stream, barrier + synchronize on both
+sides, max over ranks.  --impl reference times the float32 CPU oracle (the only other
+place this file runs oracle/), see DESIGN.md section 9.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "predictor-update Hz at 512x512, 8-px max flow; achieved HBM GB/s vs peak"
+CONFIG_NAMES = {2: "512x512 spherepix (gnomonic 90 deg), max flow 8 px (N=8), S=2, H=1 level",
+                3: "1024x1024 spherepix (gnomonic 90 deg), max flow 16 px (N=16), S=2, H=1 level",
+                4: "64 x 512x512 sequences per job, max flow 8 px (N=8), S=2, H=1 level"}
+ALGO_BYTES_PER_PX = 48  # read w 12 + rho 4 + Yhat 4 + Y 4 + lambda 4, write 12 + 4 + 4
+
+
+def env_rank():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return None
+
+
+def start_clock_sampler(device: int):
+    fd, path = tempfile.mkstemp(prefix="clocks_", suffix=".csv")
+    os.close(fd)
+    q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+    try:
+        p = subprocess.Popen(["nvidia-smi", f"--id={device}", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                              "-lms", "50"], stdout=open(path, "w"), stderr=subprocess.DEVNULL)
+    except Exception:
+        return None, path
+    return p, path
+
+
+def stop_clock_sampler(p, path):
+    if p is None:
+        return None
+    p.terminate()
+    try:
+        p.wait(timeout=5)
+    except Exception:
+        p.kill()
+    sm, mx, reasons = [], [], set()
+    names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+    for line in open(path):
+        parts = [x.strip() for x in line.split(",")]
+        if len(parts) < 9:
+            continue
+        try:
+            sm.append(float(parts[1]))
+            mx.append(float(parts[2]))
+        except ValueError:
+            continue
+        for n, v in zip(names, parts[5:9]):
+            if v.lower() == "active":
+                reasons.add(n)
+    os.unlink(path)
+    if not sm:
+        return None
+    load = [x for x in sm if x > 0.5 * max(sm)] or sm
+    return {"sm_mhz": statistics.median(load), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+            "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- CPU oracle arms
+def oracle_frames(seq, frames, rows=None):
+    """Run the float32 oracle over `frames` frames (optionally on the first `rows` rows of
+    the grid, a bounded sample); return seconds per frame (excluding the init frame)."""
+    import oracle
+
+    g = seq.geom if rows is None else np.ascontiguousarray(seq.geom[:rows])
+    o = oracle.Oracle(g, seq.params, "f32")
+    sl = (slice(None),) if rows is None else (slice(None), slice(0, rows))
+    Y = np.ascontiguousarray(seq.Y[sl])
+    D = np.ascontiguousarray(seq.depth[sl])
+    o.step(Y[0], D[0])
+    t0 = time.perf_counter()
+    for k in range(1, frames + 1):
+        o.step(Y[k % len(Y)], D[k % len(D)])
+    return (time.perf_counter() - t0) / frames
+
+
+def cpu_baseline(seq, budget_s=15.0):
+    """Oracle on host cores, single thread, bounded sample: full 512x512 frames until ~budget."""
+    t1 = oracle_frames(seq, 1)
+    frames = max(2, min(60, int(budget_s / max(t1, 1e-6))))
+    t = oracle_frames(seq, frames)
+    H, W = seq.geom.shape[:2]
+    return {"value": 1.0 / t, "unit": "Hz", "cores": 1, "kind": "oracle",
+            "sample": f"{frames} full {H}x{W} frames (N={seq.params.N}, S={seq.params.smooth_iters}) of the "
+                      f"bench workload, float32 oracle, 1 thread, {os.cpu_count()} host cores present"}
+
+
+def run_reference(args):
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return 0
+    import sfgen
+
+    cid = args.config
+    seq = sfgen.config_sequence(cid if cid != 4 else 2, frames=8)
+    H, W = seq.geom.shape[:2]
+    t1 = oracle_frames(seq, 1)
+    total = args.steps + args.warmup
+    budget = 150.0
+    rows = H if t1 * total <= budget else max(8, int(H * budget / (t1 * total)))
+    per_frame = oracle_frames(seq, args.warmup, rows) if args.warmup else 0.0  # warm-up (untimed)
+    per_frame = oracle_frames(seq, args.steps, rows)
+    frac = rows / H
+    value = frac / per_frame  # full frames per second equivalent
+    sample = f"each step: one frame of the first {rows} of {H} rows ({frac:.3f} of a frame), f32 oracle, 1 thread"
+    out = {"impl": "reference", "metric": METRIC, "value": value, "unit": "Hz", "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_frame * 1e3 / frac,
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+           "config": {"workload": CONFIG_NAMES[cid], "batch": 1},
+           "cpu_baseline": {"value": value, "unit": "Hz", "cores": 1, "kind": "oracle", "sample": sample},
+           "e2e": {"value": value, "unit": "Hz", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out))
+    return 0
+
+
+# ----------------------------------------------------------------------------- GPU arm
+def run_sf(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2406_18031_b200 as sf
+    import sfgen
+
+    rank, world, local = env_rank()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    cid = args.config
+    B = 1 if cid != 4 else max(1, 64 // world)
+    base = sfgen.CONFIGS[2 if cid == 4 else cid]
+    H, W = base["H"], base["W"]
+    ring = args.ring
+    # independent sequence(s) per rank (seeds differ); frames of the sequence fill the ring
+    seqs = [sfgen.config_sequence(2 if cid == 4 else cid, frames=ring if B == 1 else 8,
+                                  seed=(base["seed"] + 1000 * rank + b)) for b in range(B)]
+    geom, params = seqs[0].geom, seqs[0].params
+    if B == 1:
+        Yh, Dh = seqs[0].Y, seqs[0].depth
+    else:  # batch: 8 rendered frames per sequence, cycled through the ring
+        Yh = np.stack([np.stack([s.Y[k % 8] for s in seqs]) for k in range(ring)])
+        Dh = np.stack([np.stack([s.depth[k % 8] for s in seqs]) for k in range(ring)])
+    Yd = torch.from_numpy(np.ascontiguousarray(Yh.reshape(ring, B, H, W))).to(dev)
+    Dd = torch.from_numpy(np.ascontiguousarray(Dh.reshape(ring, B, H, W))).to(dev)
+    frame_bytes = B * H * W * 4
+
+    s = torch.cuda.Stream(device=dev)
+    kern = {"auto": sf.SF_KERNEL_AUTO, "fused": sf.SF_KERNEL_FUSED, "passes": sf.SF_KERNEL_PASSES}[args.kernel]
+    m = sf.StructureFlow(geom, params, batch=B, device=local, stream=s, kernel=kern)
+    with torch.cuda.stream(s):
+        m.step(Yd[0], Dd[0])  # frame 0: initialisation (not a timed step)
+        for k in range(1, ring):  # one real pass over the ring before capture (untimed)
+            m.step(Yd[k], Dd[k])
+    s.synchronize()
+    # one CUDA graph per ring slot (R even keeps the double-buffer parity)
+    graphs = []
+    for k in range(ring):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            m.step(Yd[k], Dd[k])
+        graphs.append(g)
+    launches = m.launches_per_step
+
+    def replay(i):
+        graphs[i % ring].replay()
+
+    with torch.cuda.stream(s):
+        for i in range(args.warmup):
+            replay(i)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    clk, clk_path = (None, None)
+    if rank == 0:
+        clk, clk_path = start_clock_sampler(local)
+        time.sleep(0.3)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    with torch.cuda.stream(s):
+        ev[0].record(s)
+        for i in range(args.steps):
+            replay(args.warmup + i)
+            ev[i + 1].record(s)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    clocks = stop_clock_sampler(clk, clk_path) if rank == 0 else None
+    total_ms = ev[0].elapsed_time(ev[-1])
+    step_ms = [ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps)]
+    t = torch.tensor([total_ms], device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    st, flags = sf.sf_status_flags(m.ctx)
+
+    # ---- end to end through the host-buffer C-ABI call (pinned host memory), same metric
+    e2e_steps = max(3, min(args.steps, 200))
+    Yp = torch.empty((ring, B, H, W), dtype=torch.float32, pin_memory=True)
+    Dp = torch.empty_like(Yp).pin_memory()
+    Yp.copy_(Yd.cpu())
+    Dp.copy_(Dd.cpu())
+    w_out = torch.empty((B, H, W, 3), dtype=torch.float32, pin_memory=True)
+    r_out = torch.empty((B, H, W), dtype=torch.float32, pin_memory=True)
+    for i in range(3):
+        sf.sf_step_host(m.ctx, Yp[i].data_ptr(), Dp[i].data_ptr(), w_out.data_ptr(), r_out.data_ptr())
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for i in range(e2e_steps):
+        sf.sf_step_host(m.ctx, Yp[i % ring].data_ptr(), Dp[i % ring].data_ptr(), w_out.data_ptr(), r_out.data_ptr())
+    e2e_s = torch.tensor([time.perf_counter() - t0], device=dev)
+    if world > 1:
+        dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
+    e2e_value = world * B * e2e_steps / float(e2e_s.item())
+
+    if rank == 0:
+        value = world * B * args.steps / (total_ms / 1e3)
+        pk = peaks() or {}
+        hbm_peak = pk.get("hbm_gbs", 6650.0)
+        # dominant (only) kernel per step: CUDA-event step durations on the launching stream
+        med_ms = statistics.median(step_ms)
+        mean_ms = total_ms / args.steps
+        algo_bytes = ALGO_BYTES_PER_PX * B * H * W
+        achieved = algo_bytes / (mean_ms / 1e3) / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
+                "traffic": None, "kernel": "step" if launches > 1 else "sf_fused_step",
+                "launches_per_step": launches, "algo_bytes_per_launch": algo_bytes / max(1, launches),
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in pk else "fallback 6.65 TB/s"}
+        out = {"metric": METRIC, "value": value, "unit": "Hz", "n_gpus": world, "steps": args.steps,
+               "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+               "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+               "config": {"workload": CONFIG_NAMES[cid], "batch_per_gpu": B, "H": H, "W": W, "N": params.N,
+                          "S": params.smooth_iters, "parallelism": f"independent sequences x{world}",
+                          "inputs": f"ring of {ring} frames ({ring * 2 * frame_bytes / 2**20:.0f} MiB) > L2, "
+                                    "cold reads each step; per-frame CUDA graphs",
+                          "kernel": {sf.SF_KERNEL_FUSED: "fused", sf.SF_KERNEL_PASSES: "passes"}.get(m.kernel)},
+               "roofline": roof, "gpu_launches": launches * args.steps, "step_ms_median": med_ms,
+               "e2e": {"value": e2e_value, "unit": "Hz", "h2d_bytes_per_step": 2 * frame_bytes,
+                       "d2h_bytes_per_step": 4 * frame_bytes,
+                       "note": "sf_step_host: pinned Y,lambda H2D + step + w,rho D2H + stream sync per frame"},
+               "device_flags": flags, "clocks": clocks}
+        if world == 1 and not args.no_cpu_baseline:
+            out["cpu_baseline"] = cpu_baseline(seqs[0])
+        print(json.dumps(out))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--warmup", type=int, default=100)
+    ap.add_argument("--impl", choices=["sf", "reference"], default="sf")
+    ap.add_argument("--config", type=int, choices=[2, 3, 4], default=2)
+    ap.add_argument("--kernel", choices=["auto", "fused", "passes"], default="auto")
+    ap.add_argument("--ring", type=int, default=96)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.ring % 2:
+        args.ring += 1
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_sf(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,152 @@
+/*
+ * sf.h -- C-ABI of libsf, the B200 (sm_100a) structure-flow predictor-update loop.
+ *
+ * Method: Adarve & Mahony, "Real-time Structure Flow", arXiv 2406.18031.  Line numbers
+ * below cite /root/reference/PAPER.md ("P:L"); readings of ambiguous passages are the
+ * numbered rows of DESIGN.md section 3.
+ *
+ * The filter estimates, per Spherepix pixel, the structure flow w (3-vector, rad/frame;
+ * eq:homogeneous_flow P:L194-198) and the inverse depth rho (eq:inv_depth P:L167-173)
+ * recursively from brightness Y and depth lambda frames (problem statement P:L360,
+ * Fig. 3a).  One context holds B independent sequences on one grid.
+ *
+ * Conventions (all calls):
+ *  - Every call returns sf_status; SF_OK = 0.  Validation failures return synchronously
+ *    and leave the context unchanged.
+ *  - Field pointers are DEVICE pointers unless the name ends in _host.  Layout is C
+ *    row-major float32: scalar planes [B][H][W], 3-vectors [B][H][W][3].  The caller owns
+ *    every buffer it passes; libsf reads/writes them asynchronously on the context stream
+ *    and the caller keeps them alive until that stream has passed the call.
+ *  - Device anomalies never fail a call: they set sticky flags (SF_FLAG_*) read by
+ *    sf_status_flags, the only call that synchronises the stream.
+ *  - One context is single-writer; distinct contexts are independent.
+ *  - Arithmetic is IEEE float32 in the fixed order of DESIGN.md section 4 (no FTZ, no
+ *    implicit contraction), so results are bitwise reproducible and equal to the CPU
+ *    oracle's float32 build.
+ */
+#ifndef SF_H
+#define SF_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SF_ABI_VERSION 1
+
+typedef enum {
+    SF_OK = 0,
+    SF_E_DATA = 2,        /* NULL or misaligned pointer argument                        */
+    SF_E_STABILITY = 3,   /* sf_status_flags: CFL violated with clamp_advection = 0     */
+    SF_E_CONFIG = 4,      /* invalid sf_config field                                    */
+    SF_E_STATE = 5,       /* call not valid in the context's current state              */
+    SF_E_CUDA = 6,        /* a CUDA runtime call failed                                 */
+    SF_E_NCCL = 7,        /* halo exchange failed (banded mode)                         */
+    SF_E_UNSUPPORTED = 8  /* valid request this build does not implement (levels > 1)   */
+} sf_status;
+
+/* Dominant-flow rule (DESIGN reading 1). */
+enum { SF_DOM_LARGEST = 0, SF_DOM_PRINTED = 1 };
+/* Which fields sf_get_fields returns. */
+enum { SF_FIELDS_STATE = 0, SF_FIELDS_PREDICTED = 1 };
+/* Sticky device flags. */
+enum {
+    SF_FLAG_CLAMPED = 1u,   /* |u_hat| or |v_hat| exceeded max_flow and was clamped (reading 12) */
+    SF_FLAG_NONFINITE = 2u, /* non-finite brightness input, or a non-finite solved field       */
+    SF_FLAG_CFL = 4u        /* clamp_advection = 0 and dt*|u_hat| > 1 (eq:numerical_stability)  */
+};
+/* Kernel strategy. */
+enum {
+    SF_KERNEL_AUTO = 0,   /* fused when available for the configuration, else passes     */
+    SF_KERNEL_FUSED = 1,  /* one on-chip kernel per frame (predict + update)             */
+    SF_KERNEL_PASSES = 2  /* one kernel per pass (2N + 3 + 2S launches per frame)        */
+};
+
+typedef struct sf_ctx sf_ctx; /* opaque; owns all device state */
+
+typedef struct {
+    int32_t abi_version;            /* == SF_ABI_VERSION                                              */
+    int32_t height, width;          /* grid H x W, each >= 2                                          */
+    int32_t batch;                  /* B >= 1 independent sequences sharing the grid                  */
+    int32_t levels;                 /* pyramid levels H; this build accepts 1 only       */
+    float max_flow_px;              /* > 0. N = ceil(max_flow_px) substeps, dt = 1/N;
+                                       also the clamp bound on u_hat, v_hat (reading 12)              */
+    float gamma[5];                 /* gamma1..gamma5 exactly as in eq:cost_top and
+                                       eq:cost_invdepth; all >= 0, gamma3 > 0, g4+g5 > 0    */
+    int32_t smooth_iters;           /* S >= 0 box passes after the solve (paper H=1: 2)       */
+    int32_t dominant_rule;          /* SF_DOM_LARGEST (default) or SF_DOM_PRINTED                     */
+    float source_weight;            /* sigma, weight of -f<s,w> per pass (reading 2): 0.5 default     */
+    int32_t clamp_advection;        /* 1 (default): clamp u_hat to +-max_flow; 0: literal + CFL flag  */
+    int32_t input_is_inverse_depth; /* 0: depth lambda in metres; 1: rho given directly      */
+    int32_t device;                 /* CUDA device ordinal                                            */
+    void* stream;                   /* cudaStream_t for all work (cudaStreamLegacy allowed); NULL: the
+                                       context creates its own non-blocking stream                     */
+    int32_t kernel;                 /* SF_KERNEL_*                                                    */
+    int32_t reserved[7];            /* zero                                                           */
+} sf_config;
+
+/* Fill *cfg with defaults for an H x W grid (batch 1, max flow 1 px, S = 2, sigma = 0.5,
+ * LARGEST, clamp on, gamma = {1,1,1,1,1}, device 0, own stream, AUTO kernel). */
+void sf_config_default(sf_config* cfg, int32_t height, int32_t width);
+
+/* Create a context.  geometry: the Spherepix grid as [H][W][10] float32 =
+ * (s.xyz, b1.xyz, b2.xyz, ds): unit direction s, basis columns b1 (towards (i,j+1)) and
+ * b2 (towards (i+1,j)), pixel separation ds = ||P(s_ij) s_{i,j+1}||.  Host or
+ * device pointer (detected); copied, so the caller may free it after the call returns.
+ * The state is "fresh": the first sf_update / sf_step initialises it.
+ * Errors: SF_E_CONFIG (bad field), SF_E_DATA (NULL), SF_E_CUDA (allocation). */
+sf_status sf_create(const sf_config* cfg, const float* geometry, sf_ctx** out);
+
+/* Release all device memory (synchronises the context stream).  NULL is a no-op. */
+void sf_destroy(sf_ctx* ctx);
+
+/* Prediction k -> k+ (section "State prediction" P:L501-523, numerical scheme
+ * P:L623-690): N substeps of a column pass then a row pass of the upwind transport of
+ * (w, rho) with source -f<s,w>.  Keeps the state (w^k, rho^k) and stores the prediction.
+ * Errors: SF_E_STATE on a fresh context or when a prediction is already pending. */
+sf_status sf_predict(sf_ctx* ctx);
+
+/* Update k+ -> k+1 (section "State update" P:L546-621) from brightness Y and depth
+ * (device [B][H][W]): brightness model, inverse-depth model,
+ * per-pixel 3x3 LS (eq:LS_update P:L583-588), S box smoothings, rho fusion
+ * (P:L617-621).  On a fresh context it initialises the state instead: w = 0, rho = 1/lambda
+ * (0 where invalid), Yhat = brightness model of Y.
+ * Errors: SF_E_DATA (NULL), SF_E_STATE (initialised context without a pending prediction). */
+sf_status sf_update(sf_ctx* ctx, const float* Y, const float* depth);
+
+/* One frame: sf_predict then sf_update (bitwise identical results), using the fused
+ * kernel when selected.  On a fresh context: initialisation only.  Errors: as above. */
+sf_status sf_step(sf_ctx* ctx, const float* Y, const float* depth);
+
+/* End-to-end variant with HOST buffers: copies Y_host, depth_host ([B][H][W]) to the
+ * device, runs sf_step, copies the new state to w_host ([B][H][W][3]) and rho_host
+ * ([B][H][W]) (either may be NULL), and synchronises the stream before returning. */
+sf_status sf_step_host(sf_ctx* ctx, const float* Y_host, const float* depth_host, float* w_host, float* rho_host);
+
+/* Copy fields out (asynchronously, canonical layout): which = SF_FIELDS_STATE (w^k, rho^k,
+ * Yhat^k) or SF_FIELDS_PREDICTED (w^{k+}, rho^{k+}; needs a pending prediction).  Any
+ * output pointer may be NULL.  Errors: SF_E_STATE (fresh, or no prediction). */
+sf_status sf_get_fields(sf_ctx* ctx, int32_t which, float* w, float* rho, float* yhat);
+
+/* Overwrite the state (checkpoint / test hook); marks the context initialised and drops a
+ * pending prediction.  yhat may be NULL (zeros).  Errors: SF_E_DATA. */
+sf_status sf_set_fields(sf_ctx* ctx, const float* w, const float* rho, const float* yhat);
+
+/* Read (and optionally clear) the sticky device flags; synchronises the stream.  Returns
+ * SF_E_STABILITY if SF_FLAG_CFL is set, else SF_OK. */
+sf_status sf_status_flags(sf_ctx* ctx, uint32_t* flags, int32_t clear);
+
+/* Kernel strategy actually used by sf_step (SF_KERNEL_FUSED or SF_KERNEL_PASSES). */
+int32_t sf_kernel_in_use(const sf_ctx* ctx);
+
+/* Number of kernel launches one sf_step issues (for the bench's gpu_launches count). */
+int32_t sf_launches_per_step(const sf_ctx* ctx);
+
+/* Static description of a status code. */
+const char* sf_error_string(sf_status s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SF_H */

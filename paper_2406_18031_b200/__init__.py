@@ -1,0 +1,231 @@
+"""paper_2406_18031_b200 -- B200-native structure-flow predictor-update loop.
+
+Thin ctypes binding over libsf.so (include/sf.h): the same entry points, argument
+marshalling only.  Every step of the filter runs in the CUDA kernels of libsf; there
+is no CPU or PyTorch fallback -- importing this package without a built libsf.so raises.
+PyTorch is used only for device memory, streams and process groups.
+
+Method: Adarve & Mahony, "Real-time Structure Flow", arXiv 2406.18031.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libsf.so")
+
+SF_OK, SF_E_DATA, SF_E_STABILITY, SF_E_CONFIG, SF_E_STATE, SF_E_CUDA, SF_E_NCCL, SF_E_UNSUPPORTED = 0, 2, 3, 4, 5, 6, 7, 8
+SF_DOM_LARGEST, SF_DOM_PRINTED = 0, 1
+SF_FIELDS_STATE, SF_FIELDS_PREDICTED = 0, 1
+SF_FLAG_CLAMPED, SF_FLAG_NONFINITE, SF_FLAG_CFL = 1, 2, 4
+SF_KERNEL_AUTO, SF_KERNEL_FUSED, SF_KERNEL_PASSES = 0, 1, 2
+SF_ABI_VERSION = 1
+
+EXPORTS = ("sf_config_default", "sf_create", "sf_destroy", "sf_predict", "sf_update", "sf_step", "sf_step_host",
+           "sf_get_fields", "sf_set_fields", "sf_status_flags", "sf_kernel_in_use", "sf_launches_per_step",
+           "sf_error_string")
+
+
+class sf_config(C.Structure):
+    _fields_ = [("abi_version", C.c_int32), ("height", C.c_int32), ("width", C.c_int32), ("batch", C.c_int32),
+                ("levels", C.c_int32), ("max_flow_px", C.c_float), ("gamma", C.c_float * 5),
+                ("smooth_iters", C.c_int32), ("dominant_rule", C.c_int32), ("source_weight", C.c_float),
+                ("clamp_advection", C.c_int32), ("input_is_inverse_depth", C.c_int32), ("device", C.c_int32),
+                ("stream", C.c_void_p), ("kernel", C.c_int32), ("reserved", C.c_int32 * 7)]
+
+
+class SFError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        super().__init__(f"{where}: {sf_error_string(status)} (status {status})")
+        self.status = status
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"libsf.so not built at {LIB_PATH}: run `python paper_2406_18031_b200/build.py` "
+                          "(there is no fallback path)")
+    lib = C.CDLL(LIB_PATH)
+    P = C.c_void_p
+    lib.sf_config_default.argtypes = [C.POINTER(sf_config), C.c_int32, C.c_int32]
+    lib.sf_config_default.restype = None
+    lib.sf_create.argtypes = [C.POINTER(sf_config), P, C.POINTER(P)]
+    lib.sf_destroy.argtypes = [P]
+    lib.sf_destroy.restype = None
+    lib.sf_predict.argtypes = [P]
+    lib.sf_update.argtypes = [P, P, P]
+    lib.sf_step.argtypes = [P, P, P]
+    lib.sf_step_host.argtypes = [P, P, P, P, P]
+    lib.sf_get_fields.argtypes = [P, C.c_int32, P, P, P]
+    lib.sf_set_fields.argtypes = [P, P, P, P]
+    lib.sf_status_flags.argtypes = [P, C.POINTER(C.c_uint32), C.c_int32]
+    lib.sf_kernel_in_use.argtypes = [P]
+    lib.sf_launches_per_step.argtypes = [P]
+    lib.sf_error_string.argtypes = [C.c_int]
+    lib.sf_error_string.restype = C.c_char_p
+    for name in ("sf_create", "sf_predict", "sf_update", "sf_step", "sf_step_host", "sf_get_fields",
+                 "sf_set_fields", "sf_status_flags", "sf_kernel_in_use", "sf_launches_per_step"):
+        getattr(lib, name).restype = C.c_int
+    return lib
+
+
+_lib = _load()
+
+
+# ----------------------------------------------------------------------------- C-ABI names
+def sf_error_string(status: int) -> str:
+    return _lib.sf_error_string(int(status)).decode()
+
+
+def _check(st: int, where: str) -> None:
+    if st != SF_OK:
+        raise SFError(st, where)
+
+
+def sf_config_default(height: int, width: int) -> sf_config:
+    cfg = sf_config()
+    _lib.sf_config_default(C.byref(cfg), height, width)
+    return cfg
+
+
+def sf_create(cfg: sf_config, geometry_ptr: int) -> int:
+    h = C.c_void_p()
+    _check(_lib.sf_create(C.byref(cfg), C.c_void_p(geometry_ptr), C.byref(h)), "sf_create")
+    return h.value
+
+
+def sf_destroy(ctx: int) -> None:
+    _lib.sf_destroy(C.c_void_p(ctx))
+
+
+def sf_predict(ctx: int) -> None:
+    _check(_lib.sf_predict(C.c_void_p(ctx)), "sf_predict")
+
+
+def sf_update(ctx: int, Y_ptr: int, depth_ptr: int) -> None:
+    _check(_lib.sf_update(C.c_void_p(ctx), C.c_void_p(Y_ptr), C.c_void_p(depth_ptr)), "sf_update")
+
+
+def sf_step(ctx: int, Y_ptr: int, depth_ptr: int) -> None:
+    _check(_lib.sf_step(C.c_void_p(ctx), C.c_void_p(Y_ptr), C.c_void_p(depth_ptr)), "sf_step")
+
+
+def sf_step_host(ctx: int, Y_ptr: int, depth_ptr: int, w_ptr: int | None, rho_ptr: int | None) -> None:
+    _check(_lib.sf_step_host(C.c_void_p(ctx), C.c_void_p(Y_ptr), C.c_void_p(depth_ptr), C.c_void_p(w_ptr),
+                             C.c_void_p(rho_ptr)), "sf_step_host")
+
+
+def sf_get_fields(ctx: int, which: int, w_ptr: int | None, rho_ptr: int | None, yhat_ptr: int | None) -> None:
+    _check(_lib.sf_get_fields(C.c_void_p(ctx), which, C.c_void_p(w_ptr), C.c_void_p(rho_ptr), C.c_void_p(yhat_ptr)),
+           "sf_get_fields")
+
+
+def sf_set_fields(ctx: int, w_ptr: int, rho_ptr: int, yhat_ptr: int | None) -> None:
+    _check(_lib.sf_set_fields(C.c_void_p(ctx), C.c_void_p(w_ptr), C.c_void_p(rho_ptr), C.c_void_p(yhat_ptr)),
+           "sf_set_fields")
+
+
+def sf_status_flags(ctx: int, clear: bool = False) -> tuple[int, int]:
+    """Returns (status, flags); status is SF_E_STABILITY when SF_FLAG_CFL is set."""
+    f = C.c_uint32()
+    st = _lib.sf_status_flags(C.c_void_p(ctx), C.byref(f), int(clear))
+    if st not in (SF_OK, SF_E_STABILITY):
+        raise SFError(st, "sf_status_flags")
+    return st, f.value
+
+
+def sf_kernel_in_use(ctx: int) -> int:
+    return _lib.sf_kernel_in_use(C.c_void_p(ctx))
+
+
+def sf_launches_per_step(ctx: int) -> int:
+    return _lib.sf_launches_per_step(C.c_void_p(ctx))
+
+
+# ----------------------------------------------------------------------------- torch convenience
+class StructureFlow:
+    """One libsf context over torch CUDA tensors (marshalling only).
+
+    geometry: [H][W][10] float32 (s, b1, b2, ds), host numpy or torch tensor.
+    params: any object with max_flow, gamma, smooth_iters, sigma, dominant_rule,
+    clamp_advection, input_is_inverse_depth (e.g. sfgen.Params).
+    """
+
+    def __init__(self, geometry, params, batch: int = 1, device: int = 0, stream=None, kernel: int = SF_KERNEL_AUTO):
+        import numpy as np
+        import torch
+
+        self.torch = torch
+        g = geometry if isinstance(geometry, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(geometry))
+        g = g.to(dtype=torch.float32, device=f"cuda:{device}").contiguous()
+        H, W, ch = g.shape
+        assert ch == 10
+        self.H, self.W, self.B, self.device = H, W, batch, torch.device(f"cuda:{device}")
+        cfg = sf_config_default(H, W)
+        cfg.batch = batch
+        cfg.max_flow_px = float(params.max_flow)
+        for k in range(5):
+            cfg.gamma[k] = float(params.gamma[k])
+        cfg.smooth_iters = int(params.smooth_iters)
+        cfg.dominant_rule = int(params.dominant_rule)
+        cfg.source_weight = float(params.sigma)
+        cfg.clamp_advection = int(params.clamp_advection)
+        cfg.input_is_inverse_depth = int(params.input_is_inverse_depth)
+        cfg.device = device
+        self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
+        # torch's default stream has handle 0, which sf_create reads as "make your own";
+        # pass cudaStreamLegacy (0x1) so libsf orders with torch's work on that stream.
+        cfg.stream = self.stream.cuda_stream or 1
+        cfg.kernel = kernel
+        self.cfg = cfg
+        torch.cuda.synchronize(self.device)
+        self.ctx = sf_create(cfg, g.data_ptr())
+
+    def __del__(self):
+        ctx = getattr(self, "ctx", None)
+        if ctx:
+            sf_destroy(ctx)
+            self.ctx = None
+
+    def _in(self, x):
+        t = self.torch
+        assert isinstance(x, t.Tensor) and x.is_cuda and x.dtype == t.float32 and x.is_contiguous()
+        assert x.numel() == self.B * self.H * self.W
+        return x.data_ptr()
+
+    def step(self, Y, depth):
+        sf_step(self.ctx, self._in(Y), self._in(depth))
+
+    def predict(self):
+        sf_predict(self.ctx)
+
+    def update(self, Y, depth):
+        sf_update(self.ctx, self._in(Y), self._in(depth))
+
+    def get_fields(self, which: int = SF_FIELDS_STATE):
+        t = self.torch
+        w = t.empty((self.B, self.H, self.W, 3), dtype=t.float32, device=self.device)
+        rho = t.empty((self.B, self.H, self.W), dtype=t.float32, device=self.device)
+        yhat = t.empty((self.B, self.H, self.W), dtype=t.float32, device=self.device) if which == SF_FIELDS_STATE else None
+        sf_get_fields(self.ctx, which, w.data_ptr(), rho.data_ptr(), yhat.data_ptr() if yhat is not None else None)
+        return w, rho, yhat
+
+    def set_fields(self, w, rho, yhat=None):
+        sf_set_fields(self.ctx, self._in3(w), self._in(rho), self._in(yhat) if yhat is not None else None)
+
+    def _in3(self, x):
+        t = self.torch
+        assert isinstance(x, t.Tensor) and x.is_cuda and x.dtype == t.float32 and x.is_contiguous()
+        assert x.numel() == 3 * self.B * self.H * self.W
+        return x.data_ptr()
+
+    def flags(self, clear: bool = False) -> int:
+        return sf_status_flags(self.ctx, clear)[1]
+
+    @property
+    def kernel(self) -> int:
+        return sf_kernel_in_use(self.ctx)
+
+    @property
+    def launches_per_step(self) -> int:
+        return sf_launches_per_step(self.ctx)

@@ -1,0 +1,269 @@
+// sf_api.cu -- host side of the libsf C-ABI (include/sf.h): validation, device memory,
+// state machine (fresh -> initialised -> prediction pending), dispatch to the kernels.
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include "sf_internal.cuh"
+
+#define SF_TRY(x)                                  \
+    do {                                           \
+        cudaError_t e_ = (x);                      \
+        if (e_ != cudaSuccess) return SF_E_CUDA;   \
+    } while (0)
+
+extern "C" void sf_config_default(sf_config* cfg, int32_t height, int32_t width) {
+    memset(cfg, 0, sizeof(*cfg));
+    cfg->abi_version = SF_ABI_VERSION;
+    cfg->height = height;
+    cfg->width = width;
+    cfg->batch = 1;
+    cfg->levels = 1;
+    cfg->max_flow_px = 1.0f;
+    for (int k = 0; k < 5; ++k) cfg->gamma[k] = 1.0f;
+    cfg->smooth_iters = 2;
+    cfg->dominant_rule = SF_DOM_LARGEST;
+    cfg->source_weight = 0.5f;
+    cfg->clamp_advection = 1;
+    cfg->kernel = SF_KERNEL_AUTO;
+}
+
+static sf_status validate(const sf_config* c) {
+    if (c->abi_version != SF_ABI_VERSION) return SF_E_CONFIG;
+    if (c->height < 2 || c->width < 2 || c->batch < 1) return SF_E_CONFIG;
+    if ((long long)c->height * c->width * c->batch > (1LL << 31)) return SF_E_CONFIG;
+    if (!(c->max_flow_px > 0.0f) || !isfinite(c->max_flow_px) || c->max_flow_px > 4096.0f) return SF_E_CONFIG;
+    for (int k = 0; k < 5; ++k)
+        if (!(c->gamma[k] >= 0.0f) || !isfinite(c->gamma[k])) return SF_E_CONFIG;
+    if (!(c->gamma[2] > 0.0f) || !(c->gamma[3] + c->gamma[4] > 0.0f)) return SF_E_CONFIG;
+    if (c->smooth_iters < 0 || c->smooth_iters > 64) return SF_E_CONFIG;
+    if (c->dominant_rule != SF_DOM_LARGEST && c->dominant_rule != SF_DOM_PRINTED) return SF_E_CONFIG;
+    if (!(c->source_weight >= 0.0f) || !isfinite(c->source_weight)) return SF_E_CONFIG;
+    if (c->kernel < SF_KERNEL_AUTO || c->kernel > SF_KERNEL_PASSES) return SF_E_CONFIG;
+    if (c->levels != 1) return SF_E_UNSUPPORTED;
+    return SF_OK;
+}
+
+static void free_ctx(sf_ctx* c) {
+    if (!c) return;
+    void* ptrs[] = {c->G0, c->G1, c->G2, c->state[0], c->state[1], c->pred, c->tmp, c->tmp2,
+                    c->yhat, c->HG, c->HH, c->flags, c->hY, c->hD, c->hw, c->hr};
+    for (void* p : ptrs)
+        if (p) cudaFree(p);
+    if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+    free(c);
+}
+
+extern "C" sf_status sf_create(const sf_config* cfg, const float* geometry, sf_ctx** out) {
+    if (!cfg || !out) return SF_E_DATA;
+    *out = nullptr;
+    sf_status st = validate(cfg);
+    if (st != SF_OK) return st;
+    if (!geometry) return SF_E_DATA;
+    if (cudaSetDevice(cfg->device) != cudaSuccess) return SF_E_CUDA;
+    sf_ctx* c = (sf_ctx*)calloc(1, sizeof(sf_ctx));
+    if (!c) return SF_E_CUDA;
+    c->cfg = *cfg;
+    FrameParams& f = c->fp;
+    f.H = cfg->height;
+    f.W = cfg->width;
+    f.B = cfg->batch;
+    f.N = (int)ceilf(cfg->max_flow_px);
+    if (f.N < 1) f.N = 1;
+    f.S = cfg->smooth_iters;
+    f.rule = cfg->dominant_rule;
+    f.clamp = cfg->clamp_advection ? 1 : 0;
+    f.is_inv = cfg->input_is_inverse_depth ? 1 : 0;
+    f.U = cfg->max_flow_px;
+    f.dt = 1.0f / (float)f.N;
+    f.sigma = cfg->source_weight;
+    f.g1 = cfg->gamma[0];
+    f.g2 = cfg->gamma[1];
+    f.g3 = cfg->gamma[2];
+    {
+        volatile float g45 = cfg->gamma[3] + cfg->gamma[4];  // float32 sum, then IEEE division
+        f.kappa = cfg->gamma[3] / g45;
+    }
+    if (cfg->stream) {
+        c->stream = (cudaStream_t)cfg->stream;
+    } else {
+        if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
+            free_ctx(c);
+            return SF_E_CUDA;
+        }
+        c->own_stream = true;
+    }
+    const size_t npix = (size_t)f.H * f.W, nall = npix * f.B;
+    bool ok = cudaMalloc(&c->G0, npix * sizeof(float4)) == cudaSuccess &&
+              cudaMalloc(&c->G1, npix * sizeof(float4)) == cudaSuccess &&
+              cudaMalloc(&c->G2, npix * sizeof(float4)) == cudaSuccess &&
+              cudaMalloc(&c->state[0], nall * sizeof(float4)) == cudaSuccess &&
+              cudaMalloc(&c->state[1], nall * sizeof(float4)) == cudaSuccess &&
+              cudaMalloc(&c->pred, nall * sizeof(float4)) == cudaSuccess &&
+              cudaMalloc(&c->tmp, nall * sizeof(float4)) == cudaSuccess &&
+              cudaMalloc(&c->tmp2, nall * sizeof(float4)) == cudaSuccess &&
+              cudaMalloc(&c->yhat, nall * sizeof(float)) == cudaSuccess &&
+              cudaMalloc(&c->HG, nall * sizeof(float)) == cudaSuccess &&
+              cudaMalloc(&c->HH, nall * sizeof(float)) == cudaSuccess &&
+              cudaMalloc(&c->flags, sizeof(unsigned)) == cudaSuccess;
+    if (!ok) {
+        free_ctx(c);
+        return SF_E_CUDA;
+    }
+    // geometry: host or device pointer
+    cudaPointerAttributes attr;
+    const float* gsrc = geometry;
+    float* gtmp = nullptr;
+    if (cudaPointerGetAttributes(&attr, geometry) != cudaSuccess || attr.type != cudaMemoryTypeDevice) {
+        cudaGetLastError();
+        if (cudaMalloc(&gtmp, npix * 10 * sizeof(float)) != cudaSuccess ||
+            cudaMemcpy(gtmp, geometry, npix * 10 * sizeof(float), cudaMemcpyHostToDevice) != cudaSuccess) {
+            if (gtmp) cudaFree(gtmp);
+            free_ctx(c);
+            return SF_E_CUDA;
+        }
+        gsrc = gtmp;
+    }
+    ok = cudaMemsetAsync(c->flags, 0, sizeof(unsigned), c->stream) == cudaSuccess &&
+         cudaMemsetAsync(c->state[0], 0, nall * sizeof(float4), c->stream) == cudaSuccess &&
+         cudaMemsetAsync(c->yhat, 0, nall * sizeof(float), c->stream) == cudaSuccess &&
+         sf_launch_geometry(c, gsrc) == cudaSuccess && cudaStreamSynchronize(c->stream) == cudaSuccess;
+    if (gtmp) cudaFree(gtmp);
+    if (!ok) {
+        free_ctx(c);
+        return SF_E_CUDA;
+    }
+    c->kernel = (cfg->kernel != SF_KERNEL_PASSES && sf_fused_supported(c)) ? SF_KERNEL_FUSED : SF_KERNEL_PASSES;
+    if (cfg->kernel == SF_KERNEL_FUSED && c->kernel != SF_KERNEL_FUSED) {
+        free_ctx(c);
+        return SF_E_UNSUPPORTED;
+    }
+    *out = c;
+    return SF_OK;
+}
+
+extern "C" void sf_destroy(sf_ctx* c) {
+    if (!c) return;
+    cudaStreamSynchronize(c->stream);
+    free_ctx(c);
+}
+
+extern "C" sf_status sf_predict(sf_ctx* c) {
+    if (!c) return SF_E_DATA;
+    if (!c->initialized || c->pending) return SF_E_STATE;
+    SF_TRY(sf_launch_predict_passes(c));
+    c->pending = true;
+    return SF_OK;
+}
+
+extern "C" sf_status sf_update(sf_ctx* c, const float* Y, const float* D) {
+    if (!c || !Y || !D) return SF_E_DATA;
+    if (!c->initialized) {
+        SF_TRY(sf_launch_update_passes(c, Y, D, true));
+        c->initialized = true;
+        return SF_OK;
+    }
+    if (!c->pending) return SF_E_STATE;
+    SF_TRY(sf_launch_update_passes(c, Y, D, false));
+    c->cur = 1 - c->cur;
+    c->pending = false;
+    return SF_OK;
+}
+
+extern "C" sf_status sf_step(sf_ctx* c, const float* Y, const float* D) {
+    if (!c || !Y || !D) return SF_E_DATA;
+    if (!c->initialized) return sf_update(c, Y, D);
+    if (c->pending) return SF_E_STATE;
+    if (c->kernel == SF_KERNEL_FUSED) {
+        SF_TRY(sf_launch_fused_step(c, Y, D));
+        c->cur = 1 - c->cur;
+        return SF_OK;
+    }
+    sf_status st = sf_predict(c);
+    if (st != SF_OK) return st;
+    return sf_update(c, Y, D);
+}
+
+extern "C" sf_status sf_step_host(sf_ctx* c, const float* Yh, const float* Dh, float* wh, float* rh) {
+    if (!c || !Yh || !Dh) return SF_E_DATA;
+    const size_t n = (size_t)c->fp.B * c->fp.H * c->fp.W;
+    if (!c->hY) {
+        if (cudaMalloc(&c->hY, n * sizeof(float)) != cudaSuccess || cudaMalloc(&c->hD, n * sizeof(float)) != cudaSuccess ||
+            cudaMalloc(&c->hw, 3 * n * sizeof(float)) != cudaSuccess || cudaMalloc(&c->hr, n * sizeof(float)) != cudaSuccess)
+            return SF_E_CUDA;
+    }
+    SF_TRY(cudaMemcpyAsync(c->hY, Yh, n * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+    SF_TRY(cudaMemcpyAsync(c->hD, Dh, n * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+    sf_status st = sf_step(c, c->hY, c->hD);
+    if (st != SF_OK) return st;
+    if (wh || rh) {
+        SF_TRY(sf_launch_unpack(c, c->state[c->cur], wh ? c->hw : nullptr, rh ? c->hr : nullptr));
+        if (wh) SF_TRY(cudaMemcpyAsync(wh, c->hw, 3 * n * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
+        if (rh) SF_TRY(cudaMemcpyAsync(rh, c->hr, n * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
+    }
+    SF_TRY(cudaStreamSynchronize(c->stream));
+    return SF_OK;
+}
+
+extern "C" sf_status sf_get_fields(sf_ctx* c, int32_t which, float* w, float* rho, float* yhat) {
+    if (!c) return SF_E_DATA;
+    if (!c->initialized) return SF_E_STATE;
+    const size_t n = (size_t)c->fp.B * c->fp.H * c->fp.W;
+    const float4* src;
+    if (which == SF_FIELDS_STATE) {
+        src = c->state[c->cur];
+    } else if (which == SF_FIELDS_PREDICTED) {
+        if (!c->pending) return SF_E_STATE;
+        src = c->pred;
+    } else {
+        return SF_E_CONFIG;
+    }
+    if (w || rho) SF_TRY(sf_launch_unpack(c, src, w, rho));
+    if (yhat) SF_TRY(cudaMemcpyAsync(yhat, c->yhat, n * sizeof(float), cudaMemcpyDeviceToDevice, c->stream));
+    return SF_OK;
+}
+
+extern "C" sf_status sf_set_fields(sf_ctx* c, const float* w, const float* rho, const float* yhat) {
+    if (!c || !w || !rho) return SF_E_DATA;
+    const size_t n = (size_t)c->fp.B * c->fp.H * c->fp.W;
+    SF_TRY(sf_launch_pack(c, w, rho, c->state[c->cur]));
+    if (yhat)
+        SF_TRY(cudaMemcpyAsync(c->yhat, yhat, n * sizeof(float), cudaMemcpyDeviceToDevice, c->stream));
+    else
+        SF_TRY(cudaMemsetAsync(c->yhat, 0, n * sizeof(float), c->stream));
+    c->initialized = true;
+    c->pending = false;
+    return SF_OK;
+}
+
+extern "C" sf_status sf_status_flags(sf_ctx* c, uint32_t* flags, int32_t clear) {
+    if (!c || !flags) return SF_E_DATA;
+    unsigned h = 0;
+    SF_TRY(cudaMemcpyAsync(&h, c->flags, sizeof(unsigned), cudaMemcpyDeviceToHost, c->stream));
+    SF_TRY(cudaStreamSynchronize(c->stream));
+    if (clear) SF_TRY(cudaMemsetAsync(c->flags, 0, sizeof(unsigned), c->stream));
+    *flags = h;
+    return (h & SF_FLAG_CFL) ? SF_E_STABILITY : SF_OK;
+}
+
+extern "C" int32_t sf_kernel_in_use(const sf_ctx* c) { return c ? c->kernel : 0; }
+
+extern "C" int32_t sf_launches_per_step(const sf_ctx* c) {
+    if (!c) return 0;
+    if (c->kernel == SF_KERNEL_FUSED) return sf_fused_launches(c);
+    return 2 * c->fp.N + 2 + 2 * c->fp.S;
+}
+
+extern "C" const char* sf_error_string(sf_status s) {
+    switch (s) {
+        case SF_OK: return "ok";
+        case SF_E_DATA: return "invalid pointer argument";
+        case SF_E_STABILITY: return "CFL stability condition violated (clamp_advection = 0)";
+        case SF_E_CONFIG: return "invalid configuration";
+        case SF_E_STATE: return "call not valid in the current context state";
+        case SF_E_CUDA: return "CUDA runtime error";
+        case SF_E_NCCL: return "halo exchange error";
+        case SF_E_UNSUPPORTED: return "unsupported configuration";
+    }
+    return "unknown status";
+}

@@ -1,0 +1,280 @@
+// sf_passes.cu -- the per-pass kernels of the structure-flow filter (one launch per
+// transport pass / update stage).  This is the simple reference GPU path and the one
+// the banded multi-GPU mode uses between halo exchanges; sf_fused.cu computes the same
+// bits in one launch per frame.  Arithmetic order: DESIGN.md section 4.
+#include "sf_internal.cuh"
+
+namespace {
+
+constexpr int BX = 32, BY = 8;
+
+inline dim3 grid_for(const FrameParams& f) { return dim3((f.W + BX - 1) / BX, (f.H + BY - 1) / BY, f.B); }
+
+// ------------------------------------------------------------------ geometry
+// e_k = b_k / ds (IEEE division), d2 = ds * ds (reading 5).
+__global__ void k_geometry(const float* __restrict__ g10, float4* G0, float4* G1, float4* G2, int n) {
+    int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    const float* g = g10 + 10 * (size_t)p;
+    const float ds = g[9];
+    G0[p] = make_float4(g[0], g[1], g[2], xmul(ds, ds));
+    G1[p] = make_float4(__fdiv_rn(g[3], ds), __fdiv_rn(g[4], ds), __fdiv_rn(g[5], ds), 0.0f);
+    G2[p] = make_float4(__fdiv_rn(g[6], ds), __fdiv_rn(g[7], ds), __fdiv_rn(g[8], ds), 0.0f);
+}
+
+// ------------------------------------------------------------------ transport pass (P1-P4)
+// AXIS 0: column pass (beta_1, neighbours (i, j+-1), e1).
+// AXIS 1: row pass    (beta_2, neighbours (i+-1, j), e2), P:L674-683 (reading 3).
+template <int AXIS>
+__global__ void __launch_bounds__(BX* BY) k_pass(const float4* __restrict__ in, float4* __restrict__ out,
+                                                const float4* __restrict__ G0, const float4* __restrict__ Ge,
+                                                FrameParams f, unsigned* flags) {
+    const int j = blockIdx.x * BX + threadIdx.x, i = blockIdx.y * BY + threadIdx.y, b = blockIdx.z;
+    const bool live = (i < f.H) && (j < f.W);
+    const int ii = live ? i : 0, jj = live ? j : 0;
+    int im = ii, ip = ii, jm = jj, jp = jj;
+    if (AXIS == 0) {
+        jm = max(jj - 1, 0);
+        jp = min(jj + 1, f.W - 1);
+    } else {
+        im = max(ii - 1, 0);
+        ip = min(ii + 1, f.H - 1);
+    }
+    const size_t base = (size_t)b * f.H * f.W;
+    const int g = ii * f.W + jj, gm = im * f.W + jm, gp = ip * f.W + jp;
+    const float4 c = in[base + g], cm = in[base + gm], cp = in[base + gp];
+    const float um = xdot3(Ge[gm], cm), up = xdot3(Ge[gp], cp);  // u at p-, p+ (eq:oflow_numeric)
+    float uh = dominant(um, up, f.rule);
+    bool clamped = false, cfl = false;
+    if (f.clamp) {
+        clamped = fabsf(uh) > f.U;
+        uh = fminf(fmaxf(uh, -f.U), f.U);
+    } else {
+        cfl = xmul(f.dt, fabsf(uh)) > 1.0f;
+    }
+    const float q = xmul(f.sigma, xdot3(G0[g], c));  // sigma <s, w> at p
+    const bool fwd = uh > 0.0f;
+    float4 o;
+    // f* = fma(-dt, fma(u_hat, D, f q), f), D = upwind difference
+    o.x = xfma(-f.dt, xfma(uh, fwd ? xsub(c.x, cm.x) : xsub(cp.x, c.x), xmul(c.x, q)), c.x);
+    o.y = xfma(-f.dt, xfma(uh, fwd ? xsub(c.y, cm.y) : xsub(cp.y, c.y), xmul(c.y, q)), c.y);
+    o.z = xfma(-f.dt, xfma(uh, fwd ? xsub(c.z, cm.z) : xsub(cp.z, c.z), xmul(c.z, q)), c.z);
+    o.w = xfma(-f.dt, xfma(uh, fwd ? xsub(c.w, cm.w) : xsub(cp.w, c.w), xmul(c.w, q)), c.w);
+    raise_flag(flags, live && clamped, SF_FLAG_CLAMPED);
+    raise_flag(flags, live && cfl, SF_FLAG_CFL);
+    if (live) out[base + g] = o;
+}
+
+// ------------------------------------------------------------------ update kernels (U1-U6)
+// Horizontal taps of the brightness model: HG = hz(g, Y), HH = hz(h, Y).
+__global__ void __launch_bounds__(BX* BY) k_hconv(const float* __restrict__ Y, float* HG, float* HH, FrameParams f,
+                                                 unsigned* flags) {
+    const int j = blockIdx.x * BX + threadIdx.x, i = blockIdx.y * BY + threadIdx.y, b = blockIdx.z;
+    const bool live = (i < f.H) && (j < f.W);
+    bool bad = false;
+    if (live) {
+        const float* row = Y + ((size_t)b * f.H + i) * f.W;
+        const float x0 = row[max(j - 2, 0)], x1 = row[max(j - 1, 0)], x2 = row[j], x3 = row[min(j + 1, f.W - 1)],
+                    x4 = row[min(j + 2, f.W - 1)];
+        const size_t p = ((size_t)b * f.H + i) * f.W + j;
+        HG[p] = tap_g(x0, x1, x2, x3, x4);
+        HH[p] = tap_h(x0, x1, x2, x3, x4);
+        bad = !isfinite(x2);
+    }
+    raise_flag(flags, bad, SF_FLAG_NONFINITE);
+}
+
+struct Models {
+    float yh, b1, b2;     // Yhat^{k+1}, beta_hat
+    float rh, br1, br2;   // rhohat, beta_rho
+    bool valid;
+};
+
+__device__ __forceinline__ Models eval_models(const float* __restrict__ HG, const float* __restrict__ HH,
+                                              const float* __restrict__ D, int b, int i, int j, const FrameParams& f) {
+    Models M;
+    const size_t pl = (size_t)b * f.H * f.W;
+    float g[5], h[5];
+#pragma unroll
+    for (int t = 0; t < 5; ++t) {
+        const size_t r = pl + (size_t)iclamp(i + t - 2, 0, f.H - 1) * f.W + j;
+        g[t] = HG[r];
+        h[t] = HH[r];
+    }
+    M.yh = tap_g(g[0], g[1], g[2], g[3], g[4]);
+    M.b1 = tap_g(h[0], h[1], h[2], h[3], h[4]);
+    M.b2 = tap_h(g[0], g[1], g[2], g[3], g[4]);
+    const float* Dp = D + pl;
+    const float dc = Dp[(size_t)i * f.W + j];
+    const float dl = Dp[(size_t)i * f.W + max(j - 1, 0)], dr = Dp[(size_t)i * f.W + min(j + 1, f.W - 1)];
+    const float du = Dp[(size_t)max(i - 1, 0) * f.W + j], dd = Dp[(size_t)min(i + 1, f.H - 1) * f.W + j];
+    const bool vc = depth_valid(dc, f.is_inv), vl = depth_valid(dl, f.is_inv), vr = depth_valid(dr, f.is_inv),
+               vu = depth_valid(du, f.is_inv), vd = depth_valid(dd, f.is_inv);
+    M.rh = rho_hat(dc, f.is_inv);
+    M.br1 = pick_side(M.rh, vc, rho_hat(dl, f.is_inv), vl, rho_hat(dr, f.is_inv), vr);
+    M.br2 = pick_side(M.rh, vc, rho_hat(du, f.is_inv), vu, rho_hat(dd, f.is_inv), vd);
+    M.valid = vc;
+    return M;
+}
+
+// First frame: w = 0, rho = rhohat, Yhat = brightness model.
+__global__ void __launch_bounds__(BX* BY) k_init(const float* __restrict__ HG, const float* __restrict__ HH,
+                                                const float* __restrict__ D, float4* state, float* yhat, FrameParams f) {
+    const int j = blockIdx.x * BX + threadIdx.x, i = blockIdx.y * BY + threadIdx.y, b = blockIdx.z;
+    if (i >= f.H || j >= f.W) return;
+    const Models M = eval_models(HG, HH, D, b, i, j, f);
+    const size_t p = ((size_t)b * f.H + i) * f.W + j;
+    state[p] = make_float4(0.0f, 0.0f, 0.0f, M.rh);
+    yhat[p] = M.yh;
+}
+
+// Models + per-pixel LS + fusion (U1-U3, U5).  Reads w^{k+}, rho^{k+} (pred), rho^k (st),
+// Yhat^k (yhat, in place); writes (w_LS, rho^{k+1}) to out and Yhat^{k+1} to yhat.
+__global__ void __launch_bounds__(BX* BY) k_solve(const float* __restrict__ HG, const float* __restrict__ HH,
+                                                 const float* __restrict__ D, const float4* __restrict__ pred,
+                                                 const float4* __restrict__ st, float* yhat, float4* out,
+                                                 const float4* __restrict__ G0, const float4* __restrict__ G1,
+                                                 const float4* __restrict__ G2, FrameParams f, unsigned* flags) {
+    const int j = blockIdx.x * BX + threadIdx.x, i = blockIdx.y * BY + threadIdx.y, b = blockIdx.z;
+    const bool live = (i < f.H) && (j < f.W);
+    bool bad = false;
+    if (live) {
+        const Models M = eval_models(HG, HH, D, b, i, j, f);
+        const int gi = i * f.W + j;
+        const size_t p = (size_t)b * f.H * f.W + gi;
+        const float4 s = G0[gi], e1 = G1[gi], e2 = G2[gi];
+        const float d2 = s.w;
+        const float e1a[3] = {e1.x, e1.y, e1.z}, e2a[3] = {e2.x, e2.y, e2.z}, sa[3] = {s.x, s.y, s.z};
+        float gh[3], m[3];
+        const float d2r = xmul(d2, M.rh);
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            gh[a] = xmul(d2, xfma(e2a[a], M.b2, xmul(e1a[a], M.b1)));          // ghat (eq:img_gradient)
+            const float dr = xmul(d2, xfma(e2a[a], M.br2, xmul(e1a[a], M.br1)));  // drho (eq:inv_depth_gradient)
+            m[a] = xfma(d2r, sa[a], dr);
+        }
+        const float4 wp = pred[p];
+        const float4 sk = st[p];
+        const float cY = xmul(d2, xsub(M.yh, yhat[p]));  // d2 (Yhat^{k+1} - Yhat^k), eq:img_cost_top
+        const float cr = xmul(d2, xsub(M.rh, sk.w));     // d2 (rhohat - rho^k), eq:invdepth_cost_top
+        const float wpa[3] = {wp.x, wp.y, wp.z};
+        float x[3];
+        ls_solve3(gh, m, cY, cr, wpa, f.g1, M.valid ? f.g2 : 0.0f, f.g3, x);
+        const float kap = M.valid ? f.kappa : 0.0f;
+        const float rn = xfma(kap, xsub(M.rh, wp.w), wp.w);  // fusion (reading 21)
+        out[p] = make_float4(x[0], x[1], x[2], rn);
+        yhat[p] = M.yh;
+        bad = !(isfinite(x[0]) && isfinite(x[1]) && isfinite(x[2]) && isfinite(rn));
+    }
+    raise_flag(flags, bad, SF_FLAG_NONFINITE);
+}
+
+// 5x5 box smoothing (reading 13): horizontal 5-sum, then vertical 5-sum / 25.
+// .w (rho^{k+1}) rides along unchanged.
+__global__ void __launch_bounds__(BX* BY) k_box_h(const float4* __restrict__ in, float4* __restrict__ out,
+                                                 FrameParams f) {
+    const int j = blockIdx.x * BX + threadIdx.x, i = blockIdx.y * BY + threadIdx.y, b = blockIdx.z;
+    if (i >= f.H || j >= f.W) return;
+    const float4* row = in + ((size_t)b * f.H + i) * f.W;
+    float4 a = row[max(j - 2, 0)];
+#pragma unroll
+    for (int k = -1; k <= 2; ++k) {
+        const float4 v = row[iclamp(j + k, 0, f.W - 1)];
+        a.x = xadd(a.x, v.x);
+        a.y = xadd(a.y, v.y);
+        a.z = xadd(a.z, v.z);
+    }
+    a.w = row[j].w;
+    out[((size_t)b * f.H + i) * f.W + j] = a;
+}
+
+__global__ void __launch_bounds__(BX* BY) k_box_v(const float4* __restrict__ in, float4* __restrict__ out,
+                                                 FrameParams f) {
+    const int j = blockIdx.x * BX + threadIdx.x, i = blockIdx.y * BY + threadIdx.y, b = blockIdx.z;
+    if (i >= f.H || j >= f.W) return;
+    const float4* pl = in + (size_t)b * f.H * f.W;
+    float4 a = pl[(size_t)max(i - 2, 0) * f.W + j];
+#pragma unroll
+    for (int k = -1; k <= 2; ++k) {
+        const float4 v = pl[(size_t)iclamp(i + k, 0, f.H - 1) * f.W + j];
+        a.x = xadd(a.x, v.x);
+        a.y = xadd(a.y, v.y);
+        a.z = xadd(a.z, v.z);
+    }
+    a.x = __fdiv_rn(a.x, 25.0f);
+    a.y = __fdiv_rn(a.y, 25.0f);
+    a.z = __fdiv_rn(a.z, 25.0f);
+    a.w = pl[(size_t)i * f.W + j].w;
+    out[((size_t)b * f.H + i) * f.W + j] = a;
+}
+
+__global__ void k_unpack(const float4* __restrict__ src, float* w, float* rho, size_t n) {
+    size_t p = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    const float4 v = src[p];
+    if (w) {
+        w[3 * p] = v.x;
+        w[3 * p + 1] = v.y;
+        w[3 * p + 2] = v.z;
+    }
+    if (rho) rho[p] = v.w;
+}
+
+__global__ void k_pack(const float* __restrict__ w, const float* __restrict__ rho, float4* dst, size_t n) {
+    size_t p = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    dst[p] = make_float4(w[3 * p], w[3 * p + 1], w[3 * p + 2], rho[p]);
+}
+
+}  // namespace
+
+cudaError_t sf_launch_geometry(sf_ctx* c, const float* g10) {
+    const int n = c->fp.H * c->fp.W;
+    k_geometry<<<(n + 255) / 256, 256, 0, c->stream>>>(g10, c->G0, c->G1, c->G2, n);
+    return cudaGetLastError();
+}
+
+// Prediction: N x (column pass, row pass); state[cur] -> pred, state[cur] kept (reading 9).
+cudaError_t sf_launch_predict_passes(sf_ctx* c) {
+    const FrameParams& f = c->fp;
+    const dim3 g = grid_for(f), blk(BX, BY);
+    const float4* src = c->state[c->cur];
+    for (int n = 0; n < f.N; ++n) {
+        k_pass<0><<<g, blk, 0, c->stream>>>(src, c->tmp, c->G0, c->G1, f, c->flags);
+        k_pass<1><<<g, blk, 0, c->stream>>>(c->tmp, c->pred, c->G0, c->G2, f, c->flags);
+        src = c->pred;
+    }
+    return cudaGetLastError();
+}
+
+// Update: on init, fill state[cur]; otherwise state[cur] (k) + pred (k+) -> state[1-cur] (k+1).
+cudaError_t sf_launch_update_passes(sf_ctx* c, const float* Y, const float* D, bool init) {
+    const FrameParams& f = c->fp;
+    const dim3 g = grid_for(f), blk(BX, BY);
+    k_hconv<<<g, blk, 0, c->stream>>>(Y, c->HG, c->HH, f, c->flags);
+    if (init) {
+        k_init<<<g, blk, 0, c->stream>>>(c->HG, c->HH, D, c->state[c->cur], c->yhat, f);
+        return cudaGetLastError();
+    }
+    float4* nxt = c->state[1 - c->cur];
+    float4* solved = f.S > 0 ? c->tmp : nxt;
+    k_solve<<<g, blk, 0, c->stream>>>(c->HG, c->HH, D, c->pred, c->state[c->cur], c->yhat, solved, c->G0, c->G1,
+                                      c->G2, f, c->flags);
+    for (int s = 0; s < f.S; ++s) {
+        k_box_h<<<g, blk, 0, c->stream>>>(c->tmp, c->tmp2, f);
+        k_box_v<<<g, blk, 0, c->stream>>>(c->tmp2, s == f.S - 1 ? nxt : c->tmp, f);
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t sf_launch_unpack(sf_ctx* c, const float4* src, float* w, float* rho) {
+    const size_t n = (size_t)c->fp.B * c->fp.H * c->fp.W;
+    k_unpack<<<(unsigned)((n + 255) / 256), 256, 0, c->stream>>>(src, w, rho, n);
+    return cudaGetLastError();
+}
+
+cudaError_t sf_launch_pack(sf_ctx* c, const float* w, const float* rho, float4* dst) {
+    const size_t n = (size_t)c->fp.B * c->fp.H * c->fp.W;
+    k_pack<<<(unsigned)((n + 255) / 256), 256, 0, c->stream>>>(w, rho, dst, n);
+    return cudaGetLastError();
+}

@@ -1,0 +1,261 @@
+"""GPU parity: libsf (through the C-ABI) vs the float32 CPU oracle, element by element.
+
+The north-star tolerance (1e-4 abs / 1e-5 rel per frame, 1e-3 after 100 frames) is
+asserted, and so is exact equality: both sides compute the arithmetic order of
+DESIGN.md section 4 in IEEE float32, so every field must agree bit for bit.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import sfgen
+from sfgen import grid
+from sfgen.configs import DOM_PRINTED, Params
+
+torch = pytest.importorskip("torch")
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a CUDA GPU")]
+
+KERNELS = ["passes", "auto"]
+
+
+def _sf():
+    import paper_2406_18031_b200 as sf
+    return sf
+
+
+def _kernel_id(name):
+    sf = _sf()
+    return {"passes": sf.SF_KERNEL_PASSES, "auto": sf.SF_KERNEL_AUTO, "fused": sf.SF_KERNEL_FUSED}[name]
+
+
+def _dev(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+def assert_parity(gpu, ref, what, atol=1e-4, rtol=1e-5, exact=True):
+    gpu = np.asarray(gpu)
+    ref = np.asarray(ref)
+    assert gpu.shape == ref.shape, (what, gpu.shape, ref.shape)
+    assert np.isfinite(ref).all(), what
+    d = np.abs(gpu.astype(np.float64) - ref.astype(np.float64))
+    lim = atol + rtol * np.abs(ref.astype(np.float64))
+    bad = d > lim
+    assert not bad.any(), f"{what}: {bad.sum()} elements out of tolerance, max |diff| {d.max():.3e}"
+    if exact:
+        assert np.array_equal(gpu, ref), f"{what}: not bit-identical, max |diff| {d.max():.3e} at {np.argmax(d)}"
+
+
+def _fields(m, which=0):
+    w, rho, yhat = m.get_fields(which)
+    torch.cuda.synchronize()
+    return w.cpu().numpy(), rho.cpu().numpy(), (yhat.cpu().numpy() if yhat is not None else None)
+
+
+def run_pair(seq, frames, kernel="auto", params=None, check_every=1, tol_final=None):
+    sf = _sf()
+    params = params or seq.params
+    o = oracle.Oracle(seq.geom, params, "f32")
+    m = sf.StructureFlow(seq.geom, params, batch=1, kernel=_kernel_id(kernel))
+    for k in range(frames):
+        m.step(_dev(seq.Y[k]), _dev(seq.depth[k]))
+        o.step(seq.Y[k], seq.depth[k])
+        if (k % check_every == 0) or k == frames - 1:
+            w, rho, yhat = _fields(m)
+            atol = tol_final if (tol_final and k == frames - 1) else 1e-4
+            assert_parity(w[0], o.w, f"w frame {k}", atol=atol)
+            assert_parity(rho[0], o.rho, f"rho frame {k}", atol=atol)
+            assert_parity(yhat[0], o.yhat, f"yhat frame {k}", atol=atol)
+    st, flags = sf.sf_status_flags(m.ctx)
+    assert flags == o.flags, (flags, o.flags)
+    return m, o
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_config1_every_frame(kernel):
+    """configs[0]: 64x64, N = 2, 10 frames, every frame compared."""
+    run_pair(sfgen.config_sequence(1), 10, kernel)
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_predict_only_ragged_random_state(kernel):
+    """sf_predict alone on a random state, ragged 97 x 131 grid (several tiles + tails), N = 3,
+    curved grid, clamp active: the prediction equals the oracle's."""
+    sf = _sf()
+    H, W = 97, 131
+    g = grid.gnomonic(H, W, 75.0)
+    p = Params(max_flow=2.5, gamma=(1e5, 1e6, 1.0, 1.0, 1.0))
+    rng = np.random.default_rng(0)
+    ds = g[..., 9:10]
+    w = (rng.normal(size=(H, W, 3)) * 1.5 * ds).astype(np.float32)
+    rho = rng.uniform(0.05, 0.6, (H, W)).astype(np.float32)
+    o = oracle.Oracle(g, p, "f32")
+    o.set_state(w, rho, np.zeros((H, W), np.float32))
+    wp, rp = o.predict()
+    m = sf.StructureFlow(g, p, kernel=_kernel_id(kernel))
+    m.set_fields(_dev(w[None]), _dev(rho[None]))
+    m.predict()
+    gw, gr, _ = _fields(m, sf.SF_FIELDS_PREDICTED)
+    assert_parity(gw[0], wp, "w^{k+}")
+    assert_parity(gr[0], rp, "rho^{k+}")
+    # the state itself is kept (reading 9)
+    sw, sr, _ = _fields(m, sf.SF_FIELDS_STATE)
+    assert np.array_equal(sw[0], w) and np.array_equal(sr[0], rho)
+    assert sf.sf_status_flags(m.ctx)[1] == o.flags
+
+
+@pytest.mark.parametrize("variant", ["printed", "noclamp", "S0", "S3", "inverse_input", "invalid_depth", "N1", "tiny"])
+def test_variants(variant):
+    """Options and degenerate cases, 6 frames each, bitwise."""
+    seq = sfgen.config_sequence(1, frames=6)
+    p = seq.params
+    Y, D = seq.Y.copy(), seq.depth.copy()
+    kw = dict(max_flow=p.max_flow, gamma=p.gamma, smooth_iters=p.smooth_iters)
+    if variant == "printed":
+        kw["dominant_rule"] = DOM_PRINTED
+    elif variant == "noclamp":
+        kw["clamp_advection"] = 0
+    elif variant == "S0":
+        kw["smooth_iters"] = 0
+    elif variant == "S3":
+        kw["smooth_iters"] = 3
+    elif variant == "inverse_input":
+        kw["input_is_inverse_depth"] = 1
+        D = (1.0 / D).astype(np.float32)
+    elif variant == "invalid_depth":
+        D[:, 10:20, 30:40] = np.nan
+        D[:, 40:44, :] = -1.0
+        D[:, :, 60:] = np.inf
+    elif variant == "N1":
+        kw["max_flow"] = 0.75
+    elif variant == "tiny":
+        g = grid.gnomonic(2, 3, 40.0)
+        rng = np.random.default_rng(1)
+        seq = sfgen.configs.Sequence(g, rng.uniform(0.1, 0.9, (6, 2, 3)).astype(np.float32),
+                                     rng.uniform(1, 3, (6, 2, 3)).astype(np.float32), None, p, None)
+        Y, D = seq.Y, seq.depth
+    seq2 = sfgen.configs.Sequence(seq.geom, Y, D, None, Params(**kw), None)
+    run_pair(seq2, 6, "auto")
+
+
+def test_batch_members_are_independent():
+    """B = 3 different sequences in one context: each equals its own single-sequence oracle."""
+    sf = _sf()
+    seqs = [sfgen.config_sequence(1, frames=4, seed=s) for s in (1, 2, 3)]
+    geom, p = seqs[0].geom, seqs[0].params
+    m = sf.StructureFlow(geom, p, batch=3)
+    os_ = [oracle.Oracle(geom, p, "f32") for _ in seqs]
+    for k in range(4):
+        Y = _dev(np.stack([s.Y[k] for s in seqs]))
+        D = _dev(np.stack([s.depth[k] for s in seqs]))
+        m.step(Y, D)
+        for o, s in zip(os_, seqs):
+            o.step(s.Y[k], s.depth[k])
+    w, rho, yhat = _fields(m)
+    for b, o in enumerate(os_):
+        assert_parity(w[b], o.w, f"w[{b}]")
+        assert_parity(rho[b], o.rho, f"rho[{b}]")
+        assert_parity(yhat[b], o.yhat, f"yhat[{b}]")
+
+
+def test_checkpoint_roundtrip_resumes_bitwise():
+    """sf_get_fields -> sf_set_fields into a fresh context resumes the same trajectory."""
+    sf = _sf()
+    seq = sfgen.config_sequence(1, frames=6)
+    a = sf.StructureFlow(seq.geom, seq.params)
+    for k in range(3):
+        a.step(_dev(seq.Y[k]), _dev(seq.depth[k]))
+    w, rho, yhat = a.get_fields()
+    b = sf.StructureFlow(seq.geom, seq.params)
+    b.set_fields(w.contiguous(), rho.contiguous(), yhat.contiguous())
+    for k in range(3, 6):
+        a.step(_dev(seq.Y[k]), _dev(seq.depth[k]))
+        b.step(_dev(seq.Y[k]), _dev(seq.depth[k]))
+    for x, y in zip(_fields(a), _fields(b)):
+        assert np.array_equal(x, y)
+
+
+def test_step_host_matches_device_path():
+    """The host-buffer entry point (e2e path) gives the device path's bits."""
+    sf = _sf()
+    seq = sfgen.config_sequence(1, frames=4)
+    a = sf.StructureFlow(seq.geom, seq.params)
+    b = sf.StructureFlow(seq.geom, seq.params)
+    H, W = seq.Y.shape[1:]
+    wh = np.empty((1, H, W, 3), np.float32)
+    rh = np.empty((1, H, W), np.float32)
+    for k in range(4):
+        a.step(_dev(seq.Y[k]), _dev(seq.depth[k]))
+        sf.sf_step_host(b.ctx, seq.Y[k].ctypes.data, seq.depth[k].ctypes.data, wh.ctypes.data, rh.ctypes.data)
+    w, rho, _ = _fields(a)
+    assert np.array_equal(w, wh) and np.array_equal(rho, rh)
+
+
+def test_state_machine_errors():
+    sf = _sf()
+    seq = sfgen.config_sequence(1, frames=2)
+    m = sf.StructureFlow(seq.geom, seq.params)
+    with pytest.raises(sf.SFError) as e:
+        m.predict()  # fresh context
+    assert e.value.status == sf.SF_E_STATE
+    with pytest.raises(sf.SFError) as e:
+        m.get_fields()
+    assert e.value.status == sf.SF_E_STATE
+    m.step(_dev(seq.Y[0]), _dev(seq.depth[0]))
+    with pytest.raises(sf.SFError) as e:
+        m.update(_dev(seq.Y[1]), _dev(seq.depth[1]))  # no pending prediction
+    assert e.value.status == sf.SF_E_STATE
+    with pytest.raises(sf.SFError) as e:
+        m.get_fields(sf.SF_FIELDS_PREDICTED)
+    assert e.value.status == sf.SF_E_STATE
+    m.predict()
+    with pytest.raises(sf.SFError) as e:
+        m.predict()  # twice
+    assert e.value.status == sf.SF_E_STATE
+    m.update(_dev(seq.Y[1]), _dev(seq.depth[1]))
+
+
+def test_cfl_flag_reports_stability_error():
+    """clamp_advection = 0 with flows above max_flow: the sticky CFL flag makes
+    sf_status_flags return SF_E_STABILITY (eq:numerical_stability)."""
+    sf = _sf()
+    H, W, ds = 16, 16, 2.0 ** -8
+    g = grid.flat(H, W, ds)
+    p = Params(max_flow=1.0, gamma=(1.0, 1.0, 1.0, 1.0, 1.0), clamp_advection=0)
+    m = sf.StructureFlow(g, p)
+    w = np.zeros((1, H, W, 3), np.float32)
+    w[..., 0] = 3.0 * ds
+    m.set_fields(_dev(w), _dev(np.ones((1, H, W), np.float32)))
+    m.predict()
+    st, flags = sf.sf_status_flags(m.ctx, clear=True)
+    assert st == sf.SF_E_STABILITY and flags & sf.SF_FLAG_CFL
+    assert sf.sf_status_flags(m.ctx)[1] == 0
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_zero_motion_invariance_on_gpu(kernel):
+    """Pin C1 on the GPU: identical frames, zero flow -> state bit-identical over 50 frames."""
+    seq = sfgen.config_sequence(1, frames=1)
+    sf = _sf()
+    m = sf.StructureFlow(seq.geom, seq.params, kernel=_kernel_id(kernel))
+    Y, D = _dev(seq.Y[0]), _dev(seq.depth[0])
+    m.step(Y, D)
+    f0 = _fields(m)
+    for _ in range(50):
+        m.step(Y, D)
+    for a, b in zip(f0, _fields(m)):
+        assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_config2_headline_100_frames(kernel):
+    """configs[1] at full size: 512 x 512, N = 8, 100 frames in the launch configuration
+    bench.py times; checked every 10 frames and at frame 100 (tolerance 1e-3 and exact)."""
+    seq = sfgen.config_sequence(2, frames=100)
+    run_pair(seq, 100, kernel, check_every=10, tol_final=1e-3)
+
+
+def test_config3_1024_n16():
+    """configs[2]: 1024 x 1024, N = 16 (halo 20 in the fused kernel), 4 frames."""
+    seq = sfgen.config_sequence(3, frames=4)
+    run_pair(seq, 4, "auto")
