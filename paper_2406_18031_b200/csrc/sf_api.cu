@@ -46,8 +46,8 @@ static sf_status validate(const sf_config* c) {
 
 static void free_ctx(sf_ctx* c) {
     if (!c) return;
-    void* ptrs[] = {c->G0, c->G1, c->G2, c->state[0], c->state[1], c->pred, c->tmp, c->tmp2,
-                    c->yhat, c->HG, c->HH, c->flags, c->hY, c->hD, c->hw, c->hr};
+    void* ptrs[] = {c->G0, c->G1, c->G2, c->E, c->state[0], c->state[1], c->pred, c->tmp, c->tmp2,
+                    c->yhat[0], c->yhat[1], c->HG, c->HH, c->flags, c->hY, c->hD, c->hw, c->hr};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
@@ -97,12 +97,14 @@ extern "C" sf_status sf_create(const sf_config* cfg, const float* geometry, sf_c
     bool ok = cudaMalloc(&c->G0, npix * sizeof(float4)) == cudaSuccess &&
               cudaMalloc(&c->G1, npix * sizeof(float4)) == cudaSuccess &&
               cudaMalloc(&c->G2, npix * sizeof(float4)) == cudaSuccess &&
+              cudaMalloc(&c->E, 6 * npix * sizeof(float)) == cudaSuccess &&
               cudaMalloc(&c->state[0], nall * sizeof(float4)) == cudaSuccess &&
               cudaMalloc(&c->state[1], nall * sizeof(float4)) == cudaSuccess &&
               cudaMalloc(&c->pred, nall * sizeof(float4)) == cudaSuccess &&
               cudaMalloc(&c->tmp, nall * sizeof(float4)) == cudaSuccess &&
               cudaMalloc(&c->tmp2, nall * sizeof(float4)) == cudaSuccess &&
-              cudaMalloc(&c->yhat, nall * sizeof(float)) == cudaSuccess &&
+              cudaMalloc(&c->yhat[0], nall * sizeof(float)) == cudaSuccess &&
+              cudaMalloc(&c->yhat[1], nall * sizeof(float)) == cudaSuccess &&
               cudaMalloc(&c->HG, nall * sizeof(float)) == cudaSuccess &&
               cudaMalloc(&c->HH, nall * sizeof(float)) == cudaSuccess &&
               cudaMalloc(&c->flags, sizeof(unsigned)) == cudaSuccess;
@@ -126,7 +128,7 @@ extern "C" sf_status sf_create(const sf_config* cfg, const float* geometry, sf_c
     }
     ok = cudaMemsetAsync(c->flags, 0, sizeof(unsigned), c->stream) == cudaSuccess &&
          cudaMemsetAsync(c->state[0], 0, nall * sizeof(float4), c->stream) == cudaSuccess &&
-         cudaMemsetAsync(c->yhat, 0, nall * sizeof(float), c->stream) == cudaSuccess &&
+         cudaMemsetAsync(c->yhat[0], 0, nall * sizeof(float), c->stream) == cudaSuccess &&
          sf_launch_geometry(c, gsrc) == cudaSuccess && cudaStreamSynchronize(c->stream) == cudaSuccess;
     if (gtmp) cudaFree(gtmp);
     if (!ok) {
@@ -219,7 +221,7 @@ extern "C" sf_status sf_get_fields(sf_ctx* c, int32_t which, float* w, float* rh
         return SF_E_CONFIG;
     }
     if (w || rho) SF_TRY(sf_launch_unpack(c, src, w, rho));
-    if (yhat) SF_TRY(cudaMemcpyAsync(yhat, c->yhat, n * sizeof(float), cudaMemcpyDeviceToDevice, c->stream));
+    if (yhat) SF_TRY(cudaMemcpyAsync(yhat, c->yhat[c->cur], n * sizeof(float), cudaMemcpyDeviceToDevice, c->stream));
     return SF_OK;
 }
 
@@ -228,9 +230,9 @@ extern "C" sf_status sf_set_fields(sf_ctx* c, const float* w, const float* rho, 
     const size_t n = (size_t)c->fp.B * c->fp.H * c->fp.W;
     SF_TRY(sf_launch_pack(c, w, rho, c->state[c->cur]));
     if (yhat)
-        SF_TRY(cudaMemcpyAsync(c->yhat, yhat, n * sizeof(float), cudaMemcpyDeviceToDevice, c->stream));
+        SF_TRY(cudaMemcpyAsync(c->yhat[c->cur], yhat, n * sizeof(float), cudaMemcpyDeviceToDevice, c->stream));
     else
-        SF_TRY(cudaMemsetAsync(c->yhat, 0, n * sizeof(float), c->stream));
+        SF_TRY(cudaMemsetAsync(c->yhat[c->cur], 0, n * sizeof(float), c->stream));
     c->initialized = true;
     c->pending = false;
     return SF_OK;

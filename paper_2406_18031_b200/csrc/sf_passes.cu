@@ -12,14 +12,22 @@ inline dim3 grid_for(const FrameParams& f) { return dim3((f.W + BX - 1) / BX, (f
 
 // ------------------------------------------------------------------ geometry
 // e_k = b_k / ds (IEEE division), d2 = ds * ds (reading 5).
-__global__ void k_geometry(const float* __restrict__ g10, float4* G0, float4* G1, float4* G2, int n) {
+__global__ void k_geometry(const float* __restrict__ g10, float4* G0, float4* G1, float4* G2, float* E, int n) {
     int p = blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= n) return;
     const float* g = g10 + 10 * (size_t)p;
     const float ds = g[9];
     G0[p] = make_float4(g[0], g[1], g[2], xmul(ds, ds));
-    G1[p] = make_float4(__fdiv_rn(g[3], ds), __fdiv_rn(g[4], ds), __fdiv_rn(g[5], ds), 0.0f);
-    G2[p] = make_float4(__fdiv_rn(g[6], ds), __fdiv_rn(g[7], ds), __fdiv_rn(g[8], ds), 0.0f);
+    const float4 e1 = make_float4(__fdiv_rn(g[3], ds), __fdiv_rn(g[4], ds), __fdiv_rn(g[5], ds), 0.0f);
+    const float4 e2 = make_float4(__fdiv_rn(g[6], ds), __fdiv_rn(g[7], ds), __fdiv_rn(g[8], ds), 0.0f);
+    G1[p] = e1;
+    G2[p] = e2;
+    E[p] = e1.x;
+    E[(size_t)n + p] = e1.y;
+    E[2 * (size_t)n + p] = e1.z;
+    E[3 * (size_t)n + p] = e2.x;
+    E[4 * (size_t)n + p] = e2.y;
+    E[5 * (size_t)n + p] = e2.z;
 }
 
 // ------------------------------------------------------------------ transport pass (P1-P4)
@@ -129,10 +137,11 @@ __global__ void __launch_bounds__(BX* BY) k_init(const float* __restrict__ HG, c
 }
 
 // Models + per-pixel LS + fusion (U1-U3, U5).  Reads w^{k+}, rho^{k+} (pred), rho^k (st),
-// Yhat^k (yhat, in place); writes (w_LS, rho^{k+1}) to out and Yhat^{k+1} to yhat.
+// Yhat^k (yin); writes (w_LS, rho^{k+1}) to out and Yhat^{k+1} to yout.
 __global__ void __launch_bounds__(BX* BY) k_solve(const float* __restrict__ HG, const float* __restrict__ HH,
                                                  const float* __restrict__ D, const float4* __restrict__ pred,
-                                                 const float4* __restrict__ st, float* yhat, float4* out,
+                                                 const float4* __restrict__ st, const float* __restrict__ yin,
+                                                 float* __restrict__ yout, float4* out,
                                                  const float4* __restrict__ G0, const float4* __restrict__ G1,
                                                  const float4* __restrict__ G2, FrameParams f, unsigned* flags) {
     const int j = blockIdx.x * BX + threadIdx.x, i = blockIdx.y * BY + threadIdx.y, b = blockIdx.z;
@@ -155,7 +164,7 @@ __global__ void __launch_bounds__(BX* BY) k_solve(const float* __restrict__ HG, 
         }
         const float4 wp = pred[p];
         const float4 sk = st[p];
-        const float cY = xmul(d2, xsub(M.yh, yhat[p]));  // d2 (Yhat^{k+1} - Yhat^k), eq:img_cost_top
+        const float cY = xmul(d2, xsub(M.yh, yin[p]));   // d2 (Yhat^{k+1} - Yhat^k), eq:img_cost_top
         const float cr = xmul(d2, xsub(M.rh, sk.w));     // d2 (rhohat - rho^k), eq:invdepth_cost_top
         const float wpa[3] = {wp.x, wp.y, wp.z};
         float x[3];
@@ -163,7 +172,7 @@ __global__ void __launch_bounds__(BX* BY) k_solve(const float* __restrict__ HG, 
         const float kap = M.valid ? f.kappa : 0.0f;
         const float rn = xfma(kap, xsub(M.rh, wp.w), wp.w);  // fusion (reading 21)
         out[p] = make_float4(x[0], x[1], x[2], rn);
-        yhat[p] = M.yh;
+        yout[p] = M.yh;
         bad = !(isfinite(x[0]) && isfinite(x[1]) && isfinite(x[2]) && isfinite(rn));
     }
     raise_flag(flags, bad, SF_FLAG_NONFINITE);
@@ -230,7 +239,7 @@ __global__ void k_pack(const float* __restrict__ w, const float* __restrict__ rh
 
 cudaError_t sf_launch_geometry(sf_ctx* c, const float* g10) {
     const int n = c->fp.H * c->fp.W;
-    k_geometry<<<(n + 255) / 256, 256, 0, c->stream>>>(g10, c->G0, c->G1, c->G2, n);
+    k_geometry<<<(n + 255) / 256, 256, 0, c->stream>>>(g10, c->G0, c->G1, c->G2, c->E, n);
     return cudaGetLastError();
 }
 
@@ -253,13 +262,13 @@ cudaError_t sf_launch_update_passes(sf_ctx* c, const float* Y, const float* D, b
     const dim3 g = grid_for(f), blk(BX, BY);
     k_hconv<<<g, blk, 0, c->stream>>>(Y, c->HG, c->HH, f, c->flags);
     if (init) {
-        k_init<<<g, blk, 0, c->stream>>>(c->HG, c->HH, D, c->state[c->cur], c->yhat, f);
+        k_init<<<g, blk, 0, c->stream>>>(c->HG, c->HH, D, c->state[c->cur], c->yhat[c->cur], f);
         return cudaGetLastError();
     }
     float4* nxt = c->state[1 - c->cur];
     float4* solved = f.S > 0 ? c->tmp : nxt;
-    k_solve<<<g, blk, 0, c->stream>>>(c->HG, c->HH, D, c->pred, c->state[c->cur], c->yhat, solved, c->G0, c->G1,
-                                      c->G2, f, c->flags);
+    k_solve<<<g, blk, 0, c->stream>>>(c->HG, c->HH, D, c->pred, c->state[c->cur], c->yhat[c->cur],
+                                      c->yhat[1 - c->cur], solved, c->G0, c->G1, c->G2, f, c->flags);
     for (int s = 0; s < f.S; ++s) {
         k_box_h<<<g, blk, 0, c->stream>>>(c->tmp, c->tmp2, f);
         k_box_v<<<g, blk, 0, c->stream>>>(c->tmp2, s == f.S - 1 ? nxt : c->tmp, f);

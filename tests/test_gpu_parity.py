@@ -16,7 +16,7 @@ torch = pytest.importorskip("torch")
 pytestmark = [pytest.mark.gpu,
               pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a CUDA GPU")]
 
-KERNELS = ["passes", "auto"]
+KERNELS = ["passes", "fused"]
 
 
 def _sf():
@@ -135,15 +135,17 @@ def test_variants(variant):
                                      rng.uniform(1, 3, (6, 2, 3)).astype(np.float32), None, p, None)
         Y, D = seq.Y, seq.depth
     seq2 = sfgen.configs.Sequence(seq.geom, Y, D, None, Params(**kw), None)
-    run_pair(seq2, 6, "auto")
+    run_pair(seq2, 6, "fused")
+    run_pair(seq2, 6, "passes")
 
 
-def test_batch_members_are_independent():
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_batch_members_are_independent(kernel):
     """B = 3 different sequences in one context: each equals its own single-sequence oracle."""
     sf = _sf()
     seqs = [sfgen.config_sequence(1, frames=4, seed=s) for s in (1, 2, 3)]
     geom, p = seqs[0].geom, seqs[0].params
-    m = sf.StructureFlow(geom, p, batch=3)
+    m = sf.StructureFlow(geom, p, batch=3, kernel=_kernel_id(kernel))
     os_ = [oracle.Oracle(geom, p, "f32") for _ in seqs]
     for k in range(4):
         Y = _dev(np.stack([s.Y[k] for s in seqs]))
@@ -255,7 +257,40 @@ def test_config2_headline_100_frames(kernel):
     run_pair(seq, 100, kernel, check_every=10, tol_final=1e-3)
 
 
-def test_config3_1024_n16():
-    """configs[2]: 1024 x 1024, N = 16 (halo 20 in the fused kernel), 4 frames."""
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_config3_1024_n16(kernel):
+    """configs[2]: 1024 x 1024, N = 16 (two fused launches of 8 substeps), 4 frames."""
     seq = sfgen.config_sequence(3, frames=4)
-    run_pair(seq, 4, "auto")
+    run_pair(seq, 4, kernel)
+
+
+@pytest.mark.parametrize("H,W,N,S,B", [(97, 131, 3, 2, 1), (150, 61, 8, 2, 2), (200, 170, 11, 1, 1),
+                                       (64, 300, 5, 0, 1), (33, 33, 1, 3, 3), (72, 64, 8, 2, 1),
+                                       (300, 257, 17, 2, 1), (5, 7, 2, 2, 2)])
+def test_fused_equals_passes_random_states(H, W, N, S, B):
+    """The fused, temporally blocked kernel (tiles + halos, 1 launch per 8 substeps) gives the
+    per-pass kernels' bits on random states over ragged grids, batches and substep counts
+    (tile edges, grid edges, partial tiles, N > 8 multi-launch, S = 0), 3 frames each."""
+    sf = _sf()
+    g = grid.gnomonic(H, W, 80.0)
+    rng = np.random.default_rng(H * 7 + W)
+    ds = g[..., 9][None, ..., None]
+    p = Params(max_flow=float(N) - 0.5 if N > 1 else 1.0, gamma=(3e5, 3e6, 1.0, 1.0, 2.0), smooth_iters=S)
+    w = (rng.normal(size=(B, H, W, 3)) * 0.6 * N * ds).astype(np.float32)
+    rho = rng.uniform(0.05, 0.6, (B, H, W)).astype(np.float32)
+    yh = rng.uniform(0.1, 0.9, (B, H, W)).astype(np.float32)
+    Ys = rng.uniform(0.1, 0.9, (3, B, H, W)).astype(np.float32)
+    Ds = rng.uniform(1.0, 9.0, (3, B, H, W)).astype(np.float32)
+    Ds[:, :, ::7, ::5] = np.nan
+    ms = {}
+    for kern in ("passes", "fused"):
+        m = sf.StructureFlow(g, p, batch=B, kernel=_kernel_id(kern))
+        assert m.kernel == _kernel_id(kern)
+        m.set_fields(_dev(w), _dev(rho), _dev(yh))
+        for k in range(3):
+            m.step(_dev(Ys[k]), _dev(Ds[k]))
+        ms[kern] = m
+    a, b = _fields(ms["passes"]), _fields(ms["fused"])
+    for name, x, y in zip(("w", "rho", "yhat"), a, b):
+        assert_parity(y, x, name)
+    assert sf.sf_status_flags(ms["passes"].ctx)[1] == sf.sf_status_flags(ms["fused"].ctx)[1]
