@@ -2,20 +2,23 @@
 // N <= 8 (ceil(N/8) launches beyond).  Same bits as sf_passes.cu.
 //
 // Layout.  A CTA owns an output tile TH x TW and computes on a
-// region RH x RW = (TH + 2R) x (TW + 2R), R = max(M, 2) + 2S (M substeps in this launch,
-// S box passes).  Thread (warp w, lane l) owns a vertical run of K cells of region column
-// c = 32*(w % NWX) + l, rows K*(w / NWX) ... + K-1:
-//   * its fields (w.x, w.y, w.z, rho) and its direction s stay in REGISTERS for the whole
-//     frame; e1/e2 live in shared-memory planes;
-//   * column pass (j +- 1): neighbours are lanes +- 1 -> warp shuffles (the upwind value
-//     with a per-lane source lane); warp-edge lanes swap through shared memory;
-//   * row pass (i +- 1): neighbours are in the thread's own run (registers); only the run
-//     ends swap through shared memory;
-//   * one __syncthreads per pass; the valid (exact) region shrinks by one cell per pass at
-//     cut edges and stays exact at grid edges (replicate boundary, reading 10);
-//   * update: Y and rhohat planes are loaded with the grid clamp baked in (replicated
-//     borders), separable brightness taps + occlusion-aware rho differences + the 3x3
-//     LDL^T solve per cell, then S box passes, rho fusion, one coalesced store per tile.
+// region RH x RW = (TH + 2R) x (TW + 2R), RW = 64 = one warp of lanes owning 2 adjacent
+// columns each, RH = K * NWY (NWY warps stacked vertically, K rows per thread).
+// R = max(M, 2) + 2S (M substeps in this launch, S box passes), rounded up to even.
+//   * each thread owns a 2 x K micro-tile; its fields (w.x, w.y, w.z, rho) and directions s
+//     stay in REGISTERS for the whole frame; e1/e2 live in shared-memory planes;
+//   * column pass (j +- 1): the partner column is in registers, the other neighbour is one
+//     lane away -> warp shuffles only; no shared memory, no barrier;
+//   * row pass (i +- 1): neighbours are in the thread's own rows except the run ends, which
+//     are swapped through a double-buffered shared row buffer: one __syncthreads per pass;
+//   * CTAs whose region touches the grid border take the EDGE instantiation (replicate
+//     boundary, reading 10); interior CTAs carry no boundary logic at all;
+//   * cut region edges produce inexact ("garbage") cells that never reach the tile: the
+//     halo R covers the dependency radius (M per axis for the transport, 2S + 2 for the
+//     update); flags are taken only from tile cells, which are exact at every pass;
+//   * Y and depth for the update are prefetched with cp.async at kernel start and land
+//     while the transport runs; the update computes the brightness / inverse-depth models,
+//     the 3x3 LDL^T solve and S box passes on shared planes, then fuses rho and stores.
 // The transport update of the 4 fields uses paired f32x2 ops (FADD2/FMUL2/FFMA2).
 #include "sf_internal.cuh"
 
@@ -61,6 +64,27 @@ __device__ __forceinline__ float4 transport(float4 v, float4 fu, float a, float 
 __device__ __forceinline__ float dot3s(float ax, float ay, float az, float4 x) {
     return xfma(az, x.z, xfma(ay, x.y, xmul(ax, x.x)));
 }
+__device__ __forceinline__ float4 sel4(bool p, float4 a, float4 b) { return p ? a : b; }
+__device__ __forceinline__ float4 shfl_up4(float4 v) {
+    return make_float4(__shfl_up_sync(FULL, v.x, 1), __shfl_up_sync(FULL, v.y, 1), __shfl_up_sync(FULL, v.z, 1),
+                       __shfl_up_sync(FULL, v.w, 1));
+}
+__device__ __forceinline__ float4 shfl_dn4(float4 v) {
+    return make_float4(__shfl_down_sync(FULL, v.x, 1), __shfl_down_sync(FULL, v.y, 1), __shfl_down_sync(FULL, v.z, 1),
+                       __shfl_down_sync(FULL, v.w, 1));
+}
+
+__device__ __forceinline__ void cp_async4(float* sdst, const float* gsrc) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(sdst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gsrc));
+}
+__device__ __forceinline__ void cp_async16(float* sdst, const float* gsrc) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(sdst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gsrc));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
 struct FusedArgs {
     const float4* fin;  // fields at launch start (state k or a partial prediction)
@@ -76,243 +100,293 @@ struct FusedArgs {
     FrameParams f;
     int M;    // substeps in this launch
     int upd;  // 1: run the update after the substeps
-    int R;    // halo
+    int R;    // halo (even)
     int TH, TW;
 };
 
-template <int K, int NWX, int NWY>
+template <int K, int NWY>
 struct Cfg {
-    static constexpr int RW = 32 * NWX, RH = K * NWY, P = RW * RH, NT = 32 * NWX * NWY;
-    static constexpr int NXC = ((NWY * NWX * 2 * K) + 3) & ~3;  // column-exchange slots (padded)
-    static constexpr int NXR = NWY * 2 * RW;                    // row-exchange slots
-    static constexpr int XFLOATS = 5 * NXC + 5 * NXR;
-    static constexpr int UFLOATS = 4 * P > XFLOATS ? 4 * P : XFLOATS;
-    static constexpr size_t SMEM = sizeof(float) * (6 * (size_t)P + UFLOATS);
+    static constexpr int RW = 64, RH = K * NWY, P = RW * RH, NT = 32 * NWY;
+    static constexpr int XR = NWY * 2 * RW;  // float4 slots of one row-exchange buffer
+    // smem floats: E planes 6P | Ys P | Ds/Rs P | XR buffers 2 x 4 XR (>= 2P for HG/HH, and
+    // Ys..end >= 3P for the box planes)
+    static constexpr int XRF = 2 * 4 * XR > 2 * P ? 2 * 4 * XR : 2 * P;
+    static constexpr size_t SMEM = sizeof(float) * (8 * (size_t)P + XRF);
 };
 
-template <int K, int NWX, int NWY>
-__global__ void __launch_bounds__(32 * NWX * NWY, 1) k_fused(const FusedArgs a) {
-    using C = Cfg<K, NWX, NWY>;
-    constexpr int RW = C::RW, RH = C::RH, P = C::P, NT = C::NT;
-    extern __shared__ float4 smem4[];
-    float* const Es = reinterpret_cast<float*>(smem4);
-    float* const Ub = Es + 6 * P;
-    float4* const XCf = reinterpret_cast<float4*>(Ub);
-    float* const XCu = reinterpret_cast<float*>(XCf + C::NXC);
-    float4* const XRf = reinterpret_cast<float4*>(XCu + C::NXC);
-    float* const XRv = reinterpret_cast<float*>(XRf + C::NXR);
+template <int K, int NWY, bool EDGE>
+__device__ __forceinline__ void fused_body(const FusedArgs& a, float* sm) {
+    using C = Cfg<K, NWY>;
+    constexpr int RW = C::RW, P = C::P, NT = C::NT;
+    float* const Es = sm;               // 6 planes
+    float* const Ys = sm + 6 * P;       // Y (replicated clamp), later box plane Wx
+    float* const Ds = sm + 7 * P;       // depth -> rhohat (NaN = invalid), later box plane Wy
+    float* const Xb = sm + 8 * P;       // row-exchange buffers, later HG/HH, then box plane Wz
+    float4* const XR0 = reinterpret_cast<float4*>(Xb);
 
     const FrameParams& f = a.f;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int wx = warp % NWX, wy = warp / NWX;
-    const int c = 32 * wx + lane, r0 = K * wy;
-    const int b = blockIdx.z;
-    const int R = a.R;
-    const int gi0 = blockIdx.y * a.TH - R, gj0 = blockIdx.x * a.TW - R;
-    // in-grid cells of the region: rows [rmin, rmax], cols [cmin, cmax] (also the clamp bounds)
+    const int tid = threadIdx.x, lane = tid & 31, wy = tid >> 5;
+    const int c0 = 2 * lane, r0 = K * wy;
+    const int b = blockIdx.z, R = a.R, TH = a.TH, TW = a.TW;
+    const int gi0 = blockIdx.y * TH - R, gj0 = blockIdx.x * TW - R;
     const int cmin = max(0, -gj0), cmax = min(RW - 1, f.W - 1 - gj0);
-    const int rmin = max(0, -gi0), rmax = min(RH - 1, f.H - 1 - gi0);
+    const int rmin = max(0, -gi0), rmax = min(C::RH - 1, f.H - 1 - gi0);
     const size_t HW = (size_t)f.H * f.W, plane = (size_t)b * HW;
-    const int gj = iclamp(gj0 + c, 0, f.W - 1);
-    const bool incol = c >= cmin && c <= cmax;
 
-    // ---- load e1/e2 planes (replicated clamp) and this thread's cells
-    for (int idx = tid; idx < P; idx += NT) {
-        const int rr = idx / RW, cc = idx % RW;
-        const size_t g = (size_t)iclamp(gi0 + rr, 0, f.H - 1) * f.W + iclamp(gj0 + cc, 0, f.W - 1);
-#pragma unroll
-        for (int p = 0; p < 6; ++p) Es[p * P + idx] = __ldg(a.E + p * HW + g);
-    }
-    float4 fv[K];
-    float sx[K], sy[K], sz[K];
+    // ---------------- prefetch: e planes (own cells), then Y / depth (whole region) via cp.async
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-        const size_t g = (size_t)iclamp(gi0 + r0 + k, 0, f.H - 1) * f.W + gj;
-        fv[k] = a.fin[plane + g];
-        const float4 s4 = __ldg(a.G0 + g);
-        sx[k] = s4.x;
-        sy[k] = s4.y;
-        sz[k] = s4.z;
+        const int r = r0 + k;
+        const size_t gr = (size_t)iclamp(gi0 + r, 0, f.H - 1) * f.W;
+        const size_t ga = gr + iclamp(gj0 + c0, 0, f.W - 1), gb = gr + iclamp(gj0 + c0 + 1, 0, f.W - 1);
+#pragma unroll
+        for (int p = 0; p < 6; ++p) {
+            cp_async4(Es + p * P + r * RW + c0, a.E + p * HW + ga);
+            cp_async4(Es + p * P + r * RW + c0 + 1, a.E + p * HW + gb);
+        }
     }
-    __syncthreads();
+    cp_async_commit();
+    if (a.upd) {
+        const bool vec = !EDGE && ((f.W & 3) == 0) && ((gj0 & 3) == 0);
+        if (vec) {
+            for (int idx = tid; idx < P / 4; idx += NT) {
+                const int r = idx / (RW / 4), c = (idx % (RW / 4)) * 4;
+                const size_t g = plane + (size_t)(gi0 + r) * f.W + (gj0 + c);
+                cp_async16(Ys + r * RW + c, a.Y + g);
+                cp_async16(Ds + r * RW + c, a.D + g);
+            }
+        } else {
+            for (int idx = tid; idx < P; idx += NT) {
+                const int r = idx / RW, c = idx % RW;
+                const size_t g = plane + (size_t)iclamp(gi0 + r, 0, f.H - 1) * f.W + iclamp(gj0 + c, 0, f.W - 1);
+                cp_async4(Ys + idx, a.Y + g);
+                cp_async4(Ds + idx, a.D + g);
+            }
+        }
+    }
+    cp_async_commit();
 
-    // exactness bookkeeping: a cut edge (region edge inside the grid) loses one exact cell per pass
-    const int cutL = gj0 > 0, cutR = gj0 + RW - 1 < f.W - 1, cutT = gi0 > 0, cutB = gi0 + RH - 1 < f.H - 1;
-    int eL = 0, eR = RW - 1, eT = 0, eB = RH - 1;
-    const float ndt = -f.dt;
-    unsigned fl = 0;
+    // ---------------- own fields and directions (registers)
+    float4 f0[K], f1[K];
+    float s0x[K], s0y[K], s0z[K], s1x[K], s1y[K], s1z[K];
+    float mx[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        const size_t gr = (size_t)iclamp(gi0 + r0 + k, 0, f.H - 1) * f.W;
+        const size_t ga = gr + iclamp(gj0 + c0, 0, f.W - 1), gb = gr + iclamp(gj0 + c0 + 1, 0, f.W - 1);
+        f0[k] = a.fin[plane + ga];
+        f1[k] = a.fin[plane + gb];
+        const float4 sa = __ldg(a.G0 + ga), sb = __ldg(a.G0 + gb);
+        s0x[k] = sa.x;
+        s0y[k] = sa.y;
+        s0z[k] = sa.z;
+        s1x[k] = sb.x;
+        s1y[k] = sb.y;
+        s1z[k] = sb.z;
+        mx[k] = 0.0f;
+    }
+    cp_async_wait<1>();  // own e planes landed (each thread copied exactly the cells it reads)
+
+    // boundary predicates (EDGE only): grid edge at the thread's columns / rows
+    const bool atL = EDGE && c0 <= cmin;      // cell 0 is at (or left of) the grid's left edge
+    const bool atR1 = EDGE && c0 + 1 >= cmax; // cell 1 is at (or right of) the grid's right edge
+    const bool atR0 = EDGE && c0 >= cmax;     // odd W: cell 0 is the right edge, cell 1 outside
+    const float ndt = -f.dt, U = f.U;
 
     for (int n = 0; n < a.M; ++n) {
-        // ================= column pass (beta_1)
-        {
-            float u[K];
+        // ================= column pass (beta_1): registers + shuffles only
 #pragma unroll
-            for (int k = 0; k < K; ++k) {
-                const int idx = (r0 + k) * RW + c;
-                u[k] = dot3s(Es[idx], Es[P + idx], Es[2 * P + idx], fv[k]);
+        for (int k = 0; k < K; ++k) {
+            const int ib = (r0 + k) * RW + c0;
+            const float2 ex = *reinterpret_cast<const float2*>(Es + ib);
+            const float2 ey = *reinterpret_cast<const float2*>(Es + P + ib);
+            const float2 ez = *reinterpret_cast<const float2*>(Es + 2 * P + ib);
+            const float u0 = dot3s(ex.x, ey.x, ez.x, f0[k]);
+            const float u1 = dot3s(ex.y, ey.y, ez.y, f1[k]);
+            float uL = __shfl_up_sync(FULL, u1, 1);   // lane-1's cell 1: left of cell 0
+            float uR = __shfl_down_sync(FULL, u0, 1); // lane+1's cell 0: right of cell 1
+            float4 fL = shfl_up4(f1[k]);
+            float4 fR = shfl_dn4(f0[k]);
+            float u1n = u1;       // right neighbour of cell 0
+            float4 f1n = f1[k];
+            if (EDGE) {
+                uL = atL ? u0 : uL;
+                fL = sel4(atL, f0[k], fL);
+                uR = atR1 ? u1 : uR;
+                fR = sel4(atR1, f1[k], fR);
+                u1n = atR0 ? u0 : u1;
+                f1n = sel4(atR0, f0[k], f1[k]);
             }
-            if (lane == 0 || lane == 31) {
-                const int base = ((wy * NWX + wx) * 2 + (lane == 31)) * K;
-#pragma unroll
-                for (int k = 0; k < K; ++k) {
-                    XCf[base + k] = fv[k];
-                    XCu[base + k] = u[k];
-                }
+            float uh0 = dominant(uL, u1n, f.rule);
+            float uh1 = dominant(u0, uR, f.rule);
+            // (odd W, EDGE: cell 1 may be outside the grid; keep its |u_hat| out of the flag max)
+            mx[k] = fmaxf(mx[k], fmaxf(fabsf(uh0), fabsf(atR0 ? uh0 : uh1)));
+            if (f.clamp) {
+                uh0 = fminf(fmaxf(uh0, -U), U);
+                uh1 = fminf(fmaxf(uh1, -U), U);
             }
-            __syncthreads();
-            const int nL = eL + cutL, nR = eR - cutR;
-            const bool cex = incol && c >= nL && c <= nR;
-            const int lbase = ((wy * NWX + wx - 1) * 2 + 1) * K, rbase = ((wy * NWX + wx + 1) * 2 + 0) * K;
-#pragma unroll
-            for (int k = 0; k < K; ++k) {
-                float um = __shfl_up_sync(FULL, u[k], 1), up = __shfl_down_sync(FULL, u[k], 1);
-                if (lane == 0 && wx > 0) um = XCu[lbase + k];
-                if (lane == 31 && wx < NWX - 1) up = XCu[rbase + k];
-                if (c <= cmin) um = u[k];
-                if (c >= cmax) up = u[k];
-                float uh = dominant(um, up, f.rule);
-                const int r = r0 + k;
-                const bool ex = cex && r >= eT && r <= eB && r >= rmin && r <= rmax;
-                if (f.clamp) {
-                    if (ex && fabsf(uh) > f.U) fl |= SF_FLAG_CLAMPED;
-                    uh = fminf(fmaxf(uh, -f.U), f.U);
-                } else if (ex && xmul(f.dt, fabsf(uh)) > 1.0f) {
-                    fl |= SF_FLAG_CFL;
-                }
-                const bool fwd = uh > 0.0f;
-                const int src = (fwd ? lane - 1 : lane + 1) & 31;
-                float4 fu;
-                fu.x = __shfl_sync(FULL, fv[k].x, src);
-                fu.y = __shfl_sync(FULL, fv[k].y, src);
-                fu.z = __shfl_sync(FULL, fv[k].z, src);
-                fu.w = __shfl_sync(FULL, fv[k].w, src);
-                if (fwd) {
-                    if (c <= cmin) fu = fv[k];
-                    else if (lane == 0) fu = XCf[lbase + k];
-                } else {
-                    if (c >= cmax) fu = fv[k];
-                    else if (lane == 31) fu = XCf[rbase + k];
-                }
-                const float q = xmul(f.sigma, dot3s(sx[k], sy[k], sz[k], fv[k]));
-                fv[k] = transport(fv[k], fu, fabsf(uh), q, ndt);
-            }
-            eL = nL;
-            eR = nR;
+            const float4 fu0 = sel4(uh0 > 0.0f, fL, f1n);
+            const float4 fu1 = sel4(uh1 > 0.0f, f0[k], fR);
+            const float q0 = xmul(f.sigma, dot3s(s0x[k], s0y[k], s0z[k], f0[k]));
+            const float q1 = xmul(f.sigma, dot3s(s1x[k], s1y[k], s1z[k], f1[k]));
+            f0[k] = transport(f0[k], fu0, fabsf(uh0), q0, ndt);
+            f1[k] = transport(f1[k], fu1, fabsf(uh1), q1, ndt);
         }
         // ================= row pass (beta_2, reading 3)
         {
-            float v[K];
+            float4* const XR = XR0 + (n & 1) * C::XR;
+            // publish the run ends (fields only; neighbours recompute v from the e2 planes)
+            XR[(wy * 2 + 0) * RW + c0] = f0[0];
+            XR[(wy * 2 + 0) * RW + c0 + 1] = f1[0];
+            XR[(wy * 2 + 1) * RW + c0] = f0[K - 1];
+            XR[(wy * 2 + 1) * RW + c0 + 1] = f1[K - 1];
+            float v0[K], v1[K];
 #pragma unroll
             for (int k = 0; k < K; ++k) {
-                const int idx = (r0 + k) * RW + c;
-                v[k] = dot3s(Es[3 * P + idx], Es[4 * P + idx], Es[5 * P + idx], fv[k]);
+                const int ib = (r0 + k) * RW + c0;
+                const float2 ex = *reinterpret_cast<const float2*>(Es + 3 * P + ib);
+                const float2 ey = *reinterpret_cast<const float2*>(Es + 4 * P + ib);
+                const float2 ez = *reinterpret_cast<const float2*>(Es + 5 * P + ib);
+                v0[k] = dot3s(ex.x, ey.x, ez.x, f0[k]);
+                v1[k] = dot3s(ex.y, ey.y, ez.y, f1[k]);
             }
-            XRf[(wy * 2 + 0) * RW + c] = fv[0];
-            XRv[(wy * 2 + 0) * RW + c] = v[0];
-            XRf[(wy * 2 + 1) * RW + c] = fv[K - 1];
-            XRv[(wy * 2 + 1) * RW + c] = v[K - 1];
             __syncthreads();
-            float4 ftop = fv[0], fbot = fv[K - 1];
-            float vtop = v[0], vbot = v[K - 1];
+            float4 t0 = f0[0], t1 = f1[0], b0 = f0[K - 1], b1 = f1[K - 1];
+            float vt0 = v0[0], vt1 = v1[0], vb0 = v0[K - 1], vb1 = v1[K - 1];
             if (wy > 0) {
-                ftop = XRf[((wy - 1) * 2 + 1) * RW + c];
-                vtop = XRv[((wy - 1) * 2 + 1) * RW + c];
+                const int rt = r0 - 1;
+                t0 = XR[((wy - 1) * 2 + 1) * RW + c0];
+                t1 = XR[((wy - 1) * 2 + 1) * RW + c0 + 1];
+                const int ib = rt * RW + c0;
+                const float2 ex = *reinterpret_cast<const float2*>(Es + 3 * P + ib);
+                const float2 ey = *reinterpret_cast<const float2*>(Es + 4 * P + ib);
+                const float2 ez = *reinterpret_cast<const float2*>(Es + 5 * P + ib);
+                vt0 = dot3s(ex.x, ey.x, ez.x, t0);
+                vt1 = dot3s(ex.y, ey.y, ez.y, t1);
             }
             if (wy < NWY - 1) {
-                fbot = XRf[((wy + 1) * 2 + 0) * RW + c];
-                vbot = XRv[((wy + 1) * 2 + 0) * RW + c];
+                const int rb = r0 + K;
+                b0 = XR[((wy + 1) * 2 + 0) * RW + c0];
+                b1 = XR[((wy + 1) * 2 + 0) * RW + c0 + 1];
+                const int ib = rb * RW + c0;
+                const float2 ex = *reinterpret_cast<const float2*>(Es + 3 * P + ib);
+                const float2 ey = *reinterpret_cast<const float2*>(Es + 4 * P + ib);
+                const float2 ez = *reinterpret_cast<const float2*>(Es + 5 * P + ib);
+                vb0 = dot3s(ex.x, ey.x, ez.x, b0);
+                vb1 = dot3s(ex.y, ey.y, ez.y, b1);
             }
-            const int nT = eT + cutT, nB = eB - cutB;
-            const bool cex = incol && c >= eL && c <= eR;
-            float4 prev = ftop;
+            float4 p0 = t0, p1 = t1;  // old values of the row above
 #pragma unroll
             for (int k = 0; k < K; ++k) {
-                const int r = r0 + k;
-                float vm = (k > 0) ? v[k - 1] : vtop;
-                float vp = (k < K - 1) ? v[k + 1] : vbot;
-                float4 fm = prev;
-                float4 fp = (k < K - 1) ? fv[k + 1] : fbot;
-                if (r <= rmin) {
-                    vm = v[k];
-                    fm = fv[k];
+                float vm0 = (k > 0) ? v0[k - 1] : vt0, vm1 = (k > 0) ? v1[k - 1] : vt1;
+                float vp0 = (k < K - 1) ? v0[k + 1] : vb0, vp1 = (k < K - 1) ? v1[k + 1] : vb1;
+                float4 fm0 = p0, fm1 = p1;
+                float4 fp0 = (k < K - 1) ? f0[k + 1] : b0, fp1 = (k < K - 1) ? f1[k + 1] : b1;
+                if (EDGE) {
+                    const int r = r0 + k;
+                    if (r <= rmin) {
+                        vm0 = v0[k];
+                        vm1 = v1[k];
+                        fm0 = f0[k];
+                        fm1 = f1[k];
+                    }
+                    if (r >= rmax) {
+                        vp0 = v0[k];
+                        vp1 = v1[k];
+                        fp0 = f0[k];
+                        fp1 = f1[k];
+                    }
                 }
-                if (r >= rmax) {
-                    vp = v[k];
-                    fp = fv[k];
-                }
-                float vh = dominant(vm, vp, f.rule);
-                const bool ex = cex && r >= nT && r <= nB && r >= rmin && r <= rmax;
+                float vh0 = dominant(vm0, vp0, f.rule);
+                float vh1 = dominant(vm1, vp1, f.rule);
+                mx[k] = fmaxf(mx[k], fmaxf(fabsf(vh0), fabsf(atR0 ? vh0 : vh1)));
                 if (f.clamp) {
-                    if (ex && fabsf(vh) > f.U) fl |= SF_FLAG_CLAMPED;
-                    vh = fminf(fmaxf(vh, -f.U), f.U);
-                } else if (ex && xmul(f.dt, fabsf(vh)) > 1.0f) {
-                    fl |= SF_FLAG_CFL;
+                    vh0 = fminf(fmaxf(vh0, -U), U);
+                    vh1 = fminf(fmaxf(vh1, -U), U);
                 }
-                const float4 fu = (vh > 0.0f) ? fm : fp;
-                prev = fv[k];
-                const float q = xmul(f.sigma, dot3s(sx[k], sy[k], sz[k], fv[k]));
-                fv[k] = transport(fv[k], fu, fabsf(vh), q, ndt);
+                const float4 fu0 = sel4(vh0 > 0.0f, fm0, fp0);
+                const float4 fu1 = sel4(vh1 > 0.0f, fm1, fp1);
+                p0 = f0[k];
+                p1 = f1[k];
+                const float q0 = xmul(f.sigma, dot3s(s0x[k], s0y[k], s0z[k], f0[k]));
+                const float q1 = xmul(f.sigma, dot3s(s1x[k], s1y[k], s1z[k], f1[k]));
+                f0[k] = transport(f0[k], fu0, fabsf(vh0), q0, ndt);
+                f1[k] = transport(f1[k], fu1, fabsf(vh1), q1, ndt);
             }
-            eT = nT;
-            eB = nB;
         }
     }
 
-    const int TH = a.TH, TW = a.TW;
-    if (a.upd) {
-        const int S = f.S;
-        __syncthreads();  // exchange buffers are reused below
-        float* const Ys = Ub;
-        float* const Rs = Ub + P;
-        float* const HGs = Ub + 2 * P;
-        float* const HHs = Ub + 3 * P;
-        const float qnan = __int_as_float(0x7fffffff);
-        for (int idx = tid; idx < P; idx += NT) {
-            const int rr = idx / RW, cc = idx % RW;
-            const size_t g = (size_t)iclamp(gi0 + rr, 0, f.H - 1) * f.W + iclamp(gj0 + cc, 0, f.W - 1);
-            const float y = a.Y[plane + g];
-            const float d = a.D[plane + g];
-            Ys[idx] = y;
-            Rs[idx] = depth_valid(d, f.is_inv) ? rho_hat(d, f.is_inv) : qnan;  // NaN = no measurement
-            const bool tile = rr >= R && rr < R + TH && cc >= R && cc < R + TW && rr >= rmin && rr <= rmax &&
-                              cc >= cmin && cc <= cmax;
-            if (tile && !isfinite(y)) fl |= SF_FLAG_NONFINITE;
-        }
-        __syncthreads();
-        for (int idx = tid; idx < P; idx += NT) {  // horizontal brightness taps
-            const int cc = idx % RW;
-            if (cc >= 2 && cc <= RW - 3) {
-                const float x0 = Ys[idx - 2], x1 = Ys[idx - 1], x2 = Ys[idx], x3 = Ys[idx + 1], x4 = Ys[idx + 2];
-                HGs[idx] = tap_g(x0, x1, x2, x3, x4);
-                HHs[idx] = tap_h(x0, x1, x2, x3, x4);
+    // ---------------- flags from tile cells (exact at every pass); |u_hat| before the clamp
+    unsigned fl = 0;
+    const bool tcol = c0 >= R && c0 < R + TW && c0 >= cmin && c0 <= cmax;  // c0 even, R/TW even: both or none
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        const int r = r0 + k;
+        const bool t = tcol && r >= R && r < R + TH && r >= rmin && r <= rmax;
+        if (t) {
+            if (f.clamp) {
+                if (mx[k] > U) fl |= SF_FLAG_CLAMPED;
+            } else if (xmul(f.dt, mx[k]) > 1.0f) {
+                fl |= SF_FLAG_CFL;
             }
         }
+    }
+
+    if (a.upd) {
+        const int S = f.S;
+        cp_async_wait<0>();
+        __syncthreads();  // Y / depth planes complete; row buffers free
+        float* const HG = Xb;
+        float* const HH = Xb + P;
+        const float qnan = __int_as_float(0x7fffffff);
+        // rhohat plane (NaN = no measurement) in place of depth; horizontal brightness taps
+        for (int idx = tid; idx < P; idx += NT) {
+            const float d = Ds[idx];
+            Ds[idx] = depth_valid(d, f.is_inv) ? rho_hat(d, f.is_inv) : qnan;
+            const int c = idx % RW;
+            if (c >= 2 && c <= RW - 3) {
+                const float x0 = Ys[idx - 2], x1 = Ys[idx - 1], x2 = Ys[idx], x3 = Ys[idx + 1], x4 = Ys[idx + 2];
+                HG[idx] = tap_g(x0, x1, x2, x3, x4);
+                HH[idx] = tap_h(x0, x1, x2, x3, x4);
+            }
+            const int r = idx / RW;
+            if (r >= R && r < R + TH && c >= R && c < R + TW && r >= rmin && r <= rmax && c >= cmin && c <= cmax &&
+                !isfinite(Ys[idx]))
+                fl |= SF_FLAG_NONFINITE;
+        }
         __syncthreads();
-        const int slo = R - 2 * S;  // solve region: tile + 2S
+        const int slo = R - 2 * S, shi_r = R + TH + 2 * S, shi_c = R + TW + 2 * S;
+        const bool scol0 = c0 >= slo && c0 < shi_c && c0 >= cmin && c0 <= cmax;
+        const bool scol1 = c0 + 1 >= slo && c0 + 1 < shi_c && c0 + 1 >= cmin && c0 + 1 <= cmax;
 #pragma unroll
         for (int k = 0; k < K; ++k) {
             const int r = r0 + k;
-            const bool solve = r >= slo && r < R + TH + 2 * S && c >= slo && c < R + TW + 2 * S && r >= rmin &&
-                               r <= rmax && incol;
-            if (solve) {
+            const bool srow = r >= slo && r < shi_r && r >= rmin && r <= rmax;
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                float4& fv = j ? f1[k] : f0[k];
+                const bool solve = srow && (j ? scol1 : scol0);
+                if (!solve) {
+                    fv = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+                    continue;
+                }
+                const int c = c0 + j;
                 const int idx = r * RW + c;
-                const float g0 = HGs[idx - 2 * RW], g1 = HGs[idx - RW], g2 = HGs[idx], g3 = HGs[idx + RW],
-                            g4 = HGs[idx + 2 * RW];
-                const float h0 = HHs[idx - 2 * RW], h1 = HHs[idx - RW], h2 = HHs[idx], h3 = HHs[idx + RW],
-                            h4 = HHs[idx + 2 * RW];
-                const float yh = tap_g(g0, g1, g2, g3, g4);  // Yhat^{k+1}
+                const float g0 = HG[idx - 2 * RW], g1 = HG[idx - RW], g2 = HG[idx], g3 = HG[idx + RW], g4 = HG[idx + 2 * RW];
+                const float h0 = HH[idx - 2 * RW], h1 = HH[idx - RW], h2 = HH[idx], h3 = HH[idx + RW], h4 = HH[idx + 2 * RW];
+                const float yh = tap_g(g0, g1, g2, g3, g4);  // Yhat^{k+1} (P:L446-452)
                 const float be1 = tap_g(h0, h1, h2, h3, h4);
                 const float be2 = tap_h(g0, g1, g2, g3, g4);
-                const float rc = Rs[idx], rl = Rs[idx - 1], rr = Rs[idx + 1], ru = Rs[idx - RW], rd = Rs[idx + RW];
+                const float rc = Ds[idx], rl = Ds[idx - 1], rr = Ds[idx + 1], ru = Ds[idx - RW], rd = Ds[idx + RW];
                 const bool vc = !isnan(rc), vl = !isnan(rl), vr = !isnan(rr), vu = !isnan(ru), vd = !isnan(rd);
                 const float rh = vc ? rc : 0.0f;
-                const float br1 = pick_side(rh, vc, rl, vl, rr, vr);
-                const float br2 = pick_side(rh, vc, ru, vu, rd, vd);
+                const float br1 = pick_side(rh, vc, rl, vl, rr, vr);  // eq:dominant_b1
+                const float br2 = pick_side(rh, vc, ru, vu, rd, vd);  // eq:dominant_b2
                 const size_t g = (size_t)(gi0 + r) * f.W + (gj0 + c);
                 const float d2 = __ldg(&a.G0[g].w);
                 const float e1a[3] = {Es[idx], Es[P + idx], Es[2 * P + idx]};
                 const float e2a[3] = {Es[3 * P + idx], Es[4 * P + idx], Es[5 * P + idx]};
-                const float sa[3] = {sx[k], sy[k], sz[k]};
+                const float sa[3] = {j ? s1x[k] : s0x[k], j ? s1y[k] : s0y[k], j ? s1z[k] : s0z[k]};
                 float gh[3], m[3];
                 const float d2r = xmul(d2, rh);
 #pragma unroll
@@ -321,81 +395,125 @@ __global__ void __launch_bounds__(32 * NWX * NWY, 1) k_fused(const FusedArgs a) 
                     const float dr = xmul(d2, xfma(e2a[q], br2, xmul(e1a[q], br1)));
                     m[q] = xfma(d2r, sa[q], dr);
                 }
-                const float cY = xmul(d2, xsub(yh, a.yin[plane + g]));
-                const float cr = xmul(d2, xsub(rh, a.sk[plane + g].w));
-                const float wp[3] = {fv[k].x, fv[k].y, fv[k].z};
+                const float cY = xmul(d2, xsub(yh, a.yin[plane + g]));  // eq:img_cost_top
+                const float cr = xmul(d2, xsub(rh, a.sk[plane + g].w));  // eq:invdepth_cost_top
+                const float wp[3] = {fv.x, fv.y, fv.z};
                 float x[3];
                 ls_solve3(gh, m, cY, cr, wp, f.g1, vc ? f.g2 : 0.0f, f.g3, x);
                 const float kap = vc ? f.kappa : 0.0f;
-                const float rn = xfma(kap, xsub(rh, fv[k].w), fv[k].w);
-                fv[k] = make_float4(x[0], x[1], x[2], rn);
+                const float rn = xfma(kap, xsub(rh, fv.w), fv.w);  // fusion
+                fv = make_float4(x[0], x[1], x[2], rn);
                 if (!(isfinite(x[0]) && isfinite(x[1]) && isfinite(x[2]) && isfinite(rn))) fl |= SF_FLAG_NONFINITE;
                 if (r >= R && r < R + TH && c >= R && c < R + TW) a.yout[plane + g] = yh;
-            } else {
-                fv[k] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
             }
         }
         // ---- S x 5x5 box: horizontal 5-sum, vertical 5-sum, / 25; replicate border
-        float* const Wx = Ub;
-        float* const Wy = Ub + P;
-        float* const Wz = Ub + 2 * P;
+        float* const Wx = Ys;
+        float* const Wy = Ds;
+        float* const Wz = Xb;
         for (int it = 0; it < S; ++it) {
             __syncthreads();
 #pragma unroll
             for (int k = 0; k < K; ++k) {
-                const int idx = (r0 + k) * RW + c;
-                Wx[idx] = fv[k].x;
-                Wy[idx] = fv[k].y;
-                Wz[idx] = fv[k].z;
+                const int ib = (r0 + k) * RW + c0;
+                *reinterpret_cast<float2*>(Wx + ib) = make_float2(f0[k].x, f1[k].x);
+                *reinterpret_cast<float2*>(Wy + ib) = make_float2(f0[k].y, f1[k].y);
+                *reinterpret_cast<float2*>(Wz + ib) = make_float2(f0[k].z, f1[k].z);
             }
             __syncthreads();
-            const int c0 = iclamp(c - 2, cmin, cmax), c1 = iclamp(c - 1, cmin, cmax), c3 = iclamp(c + 1, cmin, cmax),
-                      c4 = iclamp(c + 2, cmin, cmax);
-            float hx[K], hy[K], hz[K];
+            float hx0[K], hy0[K], hz0[K], hx1[K], hy1[K], hz1[K];
 #pragma unroll
             for (int k = 0; k < K; ++k) {
                 const int rb = (r0 + k) * RW;
-                hx[k] = xadd(xadd(xadd(xadd(Wx[rb + c0], Wx[rb + c1]), Wx[rb + c]), Wx[rb + c3]), Wx[rb + c4]);
-                hy[k] = xadd(xadd(xadd(xadd(Wy[rb + c0], Wy[rb + c1]), Wy[rb + c]), Wy[rb + c3]), Wy[rb + c4]);
-                hz[k] = xadd(xadd(xadd(xadd(Wz[rb + c0], Wz[rb + c1]), Wz[rb + c]), Wz[rb + c3]), Wz[rb + c4]);
+                int cc[6];
+#pragma unroll
+                for (int t = 0; t < 6; ++t) {
+                    const int cx = c0 - 2 + t;
+                    cc[t] = EDGE ? iclamp(cx, max(cmin, 0), min(cmax, RW - 1)) : max(0, min(cx, RW - 1));
+                }
+                const float* P3[3] = {Wx, Wy, Wz};
+                float o0[3], o1[3];
+#pragma unroll
+                for (int q = 0; q < 3; ++q) {
+                    const float* Wq = P3[q] + rb;
+                    const float a0 = Wq[cc[0]], a1 = Wq[cc[1]], a2 = Wq[cc[2]], a3 = Wq[cc[3]], a4 = Wq[cc[4]],
+                                a5 = Wq[cc[5]];
+                    o0[q] = xadd(xadd(xadd(xadd(a0, a1), a2), a3), a4);  // columns c0-2 .. c0+2
+                    o1[q] = xadd(xadd(xadd(xadd(a1, a2), a3), a4), a5);  // columns c0-1 .. c0+3
+                }
+                hx0[k] = o0[0];
+                hy0[k] = o0[1];
+                hz0[k] = o0[2];
+                hx1[k] = o1[0];
+                hy1[k] = o1[1];
+                hz1[k] = o1[2];
             }
             __syncthreads();
 #pragma unroll
             for (int k = 0; k < K; ++k) {
-                const int idx = (r0 + k) * RW + c;
-                Wx[idx] = hx[k];
-                Wy[idx] = hy[k];
-                Wz[idx] = hz[k];
+                const int ib = (r0 + k) * RW + c0;
+                *reinterpret_cast<float2*>(Wx + ib) = make_float2(hx0[k], hx1[k]);
+                *reinterpret_cast<float2*>(Wy + ib) = make_float2(hy0[k], hy1[k]);
+                *reinterpret_cast<float2*>(Wz + ib) = make_float2(hz0[k], hz1[k]);
             }
             __syncthreads();
 #pragma unroll
             for (int k = 0; k < K; ++k) {
                 const int r = r0 + k;
-                const int i0 = iclamp(r - 2, rmin, rmax) * RW, i1 = iclamp(r - 1, rmin, rmax) * RW,
-                          i2 = r * RW, i3 = iclamp(r + 1, rmin, rmax) * RW, i4 = iclamp(r + 2, rmin, rmax) * RW;
-                const float vx = xadd(xadd(xadd(xadd(Wx[i0 + c], Wx[i1 + c]), Wx[i2 + c]), Wx[i3 + c]), Wx[i4 + c]);
-                const float vy = xadd(xadd(xadd(xadd(Wy[i0 + c], Wy[i1 + c]), Wy[i2 + c]), Wy[i3 + c]), Wy[i4 + c]);
-                const float vz = xadd(xadd(xadd(xadd(Wz[i0 + c], Wz[i1 + c]), Wz[i2 + c]), Wz[i3 + c]), Wz[i4 + c]);
-                fv[k].x = __fdiv_rn(vx, 25.0f);
-                fv[k].y = __fdiv_rn(vy, 25.0f);
-                fv[k].z = __fdiv_rn(vz, 25.0f);
+                int ri[5];
+#pragma unroll
+                for (int t = 0; t < 5; ++t) {
+                    const int rx = r - 2 + t;
+                    ri[t] = (EDGE ? iclamp(rx, rmin, rmax) : max(0, min(rx, C::RH - 1))) * RW + c0;
+                }
+                const float2 x0 = *reinterpret_cast<const float2*>(Wx + ri[0]), x1 = *reinterpret_cast<const float2*>(Wx + ri[1]),
+                             x2 = *reinterpret_cast<const float2*>(Wx + ri[2]), x3 = *reinterpret_cast<const float2*>(Wx + ri[3]),
+                             x4 = *reinterpret_cast<const float2*>(Wx + ri[4]);
+                const float2 y0 = *reinterpret_cast<const float2*>(Wy + ri[0]), y1 = *reinterpret_cast<const float2*>(Wy + ri[1]),
+                             y2 = *reinterpret_cast<const float2*>(Wy + ri[2]), y3 = *reinterpret_cast<const float2*>(Wy + ri[3]),
+                             y4 = *reinterpret_cast<const float2*>(Wy + ri[4]);
+                const float2 z0 = *reinterpret_cast<const float2*>(Wz + ri[0]), z1 = *reinterpret_cast<const float2*>(Wz + ri[1]),
+                             z2 = *reinterpret_cast<const float2*>(Wz + ri[2]), z3 = *reinterpret_cast<const float2*>(Wz + ri[3]),
+                             z4 = *reinterpret_cast<const float2*>(Wz + ri[4]);
+                f0[k].x = __fdiv_rn(xadd(xadd(xadd(xadd(x0.x, x1.x), x2.x), x3.x), x4.x), 25.0f);
+                f1[k].x = __fdiv_rn(xadd(xadd(xadd(xadd(x0.y, x1.y), x2.y), x3.y), x4.y), 25.0f);
+                f0[k].y = __fdiv_rn(xadd(xadd(xadd(xadd(y0.x, y1.x), y2.x), y3.x), y4.x), 25.0f);
+                f1[k].y = __fdiv_rn(xadd(xadd(xadd(xadd(y0.y, y1.y), y2.y), y3.y), y4.y), 25.0f);
+                f0[k].z = __fdiv_rn(xadd(xadd(xadd(xadd(z0.x, z1.x), z2.x), z3.x), z4.x), 25.0f);
+                f1[k].z = __fdiv_rn(xadd(xadd(xadd(xadd(z0.y, z1.y), z2.y), z3.y), z4.y), 25.0f);
             }
         }
     }
-    // ---- store the tile
+    // ---------------- store the tile (2 adjacent cells per thread per row: coalesced)
 #pragma unroll
     for (int k = 0; k < K; ++k) {
         const int r = r0 + k;
-        if (r >= R && r < R + TH && c >= R && c < R + TW && r >= rmin && r <= rmax && incol)
-            a.fout[plane + (size_t)(gi0 + r) * f.W + (gj0 + c)] = fv[k];
+        if (r >= R && r < R + TH && r >= rmin && r <= rmax) {
+            const size_t g = plane + (size_t)(gi0 + r) * f.W + (gj0 + c0);
+            if (c0 >= R && c0 < R + TW && c0 >= cmin && c0 <= cmax) a.fout[g] = f0[k];
+            if (c0 + 1 >= R && c0 + 1 < R + TW && c0 + 1 >= cmin && c0 + 1 <= cmax) a.fout[g + 1] = f1[k];
+        }
     }
     const unsigned any = __reduce_or_sync(FULL, fl);
     if (lane == 0 && any) atomicOr(a.flags, any);
 }
 
-// The one configuration used today: RW = 64, RH = 72, 384 threads, 1 CTA / SM.
-constexpr int FK = 12, FNWX = 2, FNWY = 6;
-using FC = Cfg<FK, FNWX, FNWY>;
+template <int K, int NWY>
+__global__ void __launch_bounds__(32 * NWY, 1) k_fused(const FusedArgs a) {
+    extern __shared__ float4 smem4[];
+    float* sm = reinterpret_cast<float*>(smem4);
+    using C = Cfg<K, NWY>;
+    const int gi0 = blockIdx.y * a.TH - a.R, gj0 = blockIdx.x * a.TW - a.R;
+    const bool edge = gi0 < 0 || gj0 < 0 || gi0 + C::RH > a.f.H || gj0 + C::RW > a.f.W;
+    if (edge)
+        fused_body<K, NWY, true>(a, sm);
+    else
+        fused_body<K, NWY, false>(a, sm);
+}
+
+// The configuration used today: RW = 64, RH = 72 (K = 6 rows x 12 warps), 384 threads, 1 CTA / SM.
+constexpr int FK = 6, FNWY = 12;
+using FC = Cfg<FK, FNWY>;
 constexpr int MMAX = 8;  // substeps per launch
 
 struct Plan {
@@ -410,7 +528,8 @@ Plan make_plan(const FrameParams& f) {
     for (int l = 0; l < p.launches; ++l) {
         p.M[l] = (l < p.launches - 1) ? MMAX : f.N - MMAX * (p.launches - 1);
         const bool upd = l == p.launches - 1;
-        p.R[l] = upd ? (p.M[l] > 2 ? p.M[l] : 2) + 2 * f.S : p.M[l];
+        int R = upd ? (p.M[l] > 2 ? p.M[l] : 2) + 2 * f.S : p.M[l];
+        p.R[l] = (R + 1) & ~1;  // even: tiles start at even columns (2 cells per lane)
     }
     return p;
 }
@@ -423,8 +542,8 @@ bool sf_fused_supported(const sf_ctx* c) {
     for (int l = 0; l < p.launches; ++l)
         if (FC::RW - 2 * p.R[l] < 8 || FC::RH - 2 * p.R[l] < 8) return false;
     // opt in to the large dynamic shared-memory carve-out (one CTA per SM)
-    return cudaFuncSetAttribute(k_fused<FK, FNWX, FNWY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)FC::SMEM) == cudaSuccess;
+    return cudaFuncSetAttribute(k_fused<FK, FNWY>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FC::SMEM) ==
+           cudaSuccess;
 }
 
 int sf_fused_launches(const sf_ctx* c) { return make_plan(c->fp).launches; }
@@ -454,7 +573,7 @@ cudaError_t sf_launch_fused_step(sf_ctx* c, const float* Y, const float* D) {
         a.TW = FC::RW - 2 * a.R;
         a.TH = FC::RH - 2 * a.R;
         const dim3 grid((f.W + a.TW - 1) / a.TW, (f.H + a.TH - 1) / a.TH, f.B);
-        k_fused<FK, FNWX, FNWY><<<grid, FC::NT, FC::SMEM, c->stream>>>(a);
+        k_fused<FK, FNWY><<<grid, FC::NT, FC::SMEM, c->stream>>>(a);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
         src = a.fout;

@@ -294,3 +294,21 @@ def test_fused_equals_passes_random_states(H, W, N, S, B):
     for name, x, y in zip(("w", "rho", "yhat"), a, b):
         assert_parity(y, x, name)
     assert sf.sf_status_flags(ms["passes"].ctx)[1] == sf.sf_status_flags(ms["fused"].ctx)[1]
+
+
+def test_fused_equals_passes_on_bench_ring():
+    """The bench workload (configs[1] scene, frames replayed from a ring with a wrap-around
+    jump back to frame 0): fused and per-pass kernels stay bit-identical, flags included."""
+    sf = _sf()
+    seq = sfgen.config_sequence(2, frames=16)
+    ms = {k: sf.StructureFlow(seq.geom, seq.params, kernel=_kernel_id(k)) for k in ("passes", "fused")}
+    Yd = [_dev(y) for y in seq.Y]
+    Dd = [_dev(d) for d in seq.depth]
+    for i in range(40):
+        for m in ms.values():
+            m.step(Yd[i % 16], Dd[i % 16])
+        if i % 8 == 7:
+            a, b = _fields(ms["passes"]), _fields(ms["fused"])
+            for name, x, y in zip(("w", "rho", "yhat"), a, b):
+                assert_parity(y, x, f"{name} step {i}")
+            assert sf.sf_status_flags(ms["passes"].ctx)[1] == sf.sf_status_flags(ms["fused"].ctx)[1], i
