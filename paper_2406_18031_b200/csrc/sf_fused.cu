@@ -78,6 +78,10 @@ __device__ __forceinline__ void cp_async4(float* sdst, const float* gsrc) {
     const unsigned s = (unsigned)__cvta_generic_to_shared(sdst);
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gsrc));
 }
+__device__ __forceinline__ void cp_async8(float* sdst, const float* gsrc) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(sdst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gsrc));
+}
 __device__ __forceinline__ void cp_async16(float* sdst, const float* gsrc) {
     const unsigned s = (unsigned)__cvta_generic_to_shared(sdst);
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gsrc));
@@ -95,7 +99,9 @@ struct FusedArgs {
     const float* Y;
     const float* D;
     const float4* G0;   // (s, d2)
-    const float* E;     // [6][H*W]
+    const float4* G1;   // e1
+    const float4* G2;   // e2
+    const float* E;     // [6][H*W] (e1.xyz, e2.xyz planes)
     unsigned* flags;
     FrameParams f;
     int M;    // substeps in this launch
@@ -114,14 +120,16 @@ struct Cfg {
     static constexpr size_t SMEM = sizeof(float) * (8 * (size_t)P + XRF);
 };
 
-template <int K, int NWY, bool EDGE>
-__device__ __forceinline__ void fused_body(const FusedArgs& a, float* sm) {
+template <int K, int NWY>
+__global__ void __launch_bounds__(32 * NWY, 1) k_fused(const FusedArgs a) {
     using C = Cfg<K, NWY>;
-    constexpr int RW = C::RW, P = C::P, NT = C::NT;
-    float* const Es = sm;               // 6 planes
-    float* const Ys = sm + 6 * P;       // Y (replicated clamp), later box plane Wx
-    float* const Ds = sm + 7 * P;       // depth -> rhohat (NaN = invalid), later box plane Wy
-    float* const Xb = sm + 8 * P;       // row-exchange buffers, later HG/HH, then box plane Wz
+    constexpr int RW = C::RW, RH = C::RH, P = C::P, NT = C::NT;
+    extern __shared__ float4 smem4[];
+    float* const sm = reinterpret_cast<float*>(smem4);
+    float* const Es = sm;          // transport: 6 planes e1.xyz, e2.xyz
+    float* const Ys = sm + 6 * P;  // Y (replicated clamp)
+    float* const Ds = sm + 7 * P;  // depth -> rhohat (NaN = invalid)
+    float* const Xb = sm + 8 * P;  // transport: 2 row-exchange buffers
     float4* const XR0 = reinterpret_cast<float4*>(Xb);
 
     const FrameParams& f = a.f;
@@ -129,44 +137,54 @@ __device__ __forceinline__ void fused_body(const FusedArgs& a, float* sm) {
     const int c0 = 2 * lane, r0 = K * wy;
     const int b = blockIdx.z, R = a.R, TH = a.TH, TW = a.TW;
     const int gi0 = blockIdx.y * TH - R, gj0 = blockIdx.x * TW - R;
+    // in-grid part of the region (also the replicate-clamp bounds)
     const int cmin = max(0, -gj0), cmax = min(RW - 1, f.W - 1 - gj0);
-    const int rmin = max(0, -gi0), rmax = min(C::RH - 1, f.H - 1 - gi0);
+    const int rmin = max(0, -gi0), rmax = min(RH - 1, f.H - 1 - gi0);
+    const bool edgeC = cmin > 0 || cmax < RW - 1;  // block-uniform
+    const bool edgeR = rmin > 0 || rmax < RH - 1;
     const size_t HW = (size_t)f.H * f.W, plane = (size_t)b * HW;
 
-    // ---------------- prefetch: e planes (own cells), then Y / depth (whole region) via cp.async
+    // ---------------- prefetch (cp.async): own e1/e2 cells (group 0), Y and depth (group 1)
+    {
+        const bool pair = !edgeC && (f.W & 1) == 0;  // both cells contiguous and 8-byte aligned
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-        const int r = r0 + k;
-        const size_t gr = (size_t)iclamp(gi0 + r, 0, f.H - 1) * f.W;
-        const size_t ga = gr + iclamp(gj0 + c0, 0, f.W - 1), gb = gr + iclamp(gj0 + c0 + 1, 0, f.W - 1);
+        for (int k = 0; k < K; ++k) {
+            const int r = r0 + k;
+            const size_t gr = (size_t)iclamp(gi0 + r, 0, f.H - 1) * f.W;
+            const size_t ga = gr + iclamp(gj0 + c0, 0, f.W - 1), gb = gr + iclamp(gj0 + c0 + 1, 0, f.W - 1);
 #pragma unroll
-        for (int p = 0; p < 6; ++p) {
-            cp_async4(Es + p * P + r * RW + c0, a.E + p * HW + ga);
-            cp_async4(Es + p * P + r * RW + c0 + 1, a.E + p * HW + gb);
-        }
-    }
-    cp_async_commit();
-    if (a.upd) {
-        const bool vec = !EDGE && ((f.W & 3) == 0) && ((gj0 & 3) == 0);
-        if (vec) {
-            for (int idx = tid; idx < P / 4; idx += NT) {
-                const int r = idx / (RW / 4), c = (idx % (RW / 4)) * 4;
-                const size_t g = plane + (size_t)(gi0 + r) * f.W + (gj0 + c);
-                cp_async16(Ys + r * RW + c, a.Y + g);
-                cp_async16(Ds + r * RW + c, a.D + g);
-            }
-        } else {
-            for (int idx = tid; idx < P; idx += NT) {
-                const int r = idx / RW, c = idx % RW;
-                const size_t g = plane + (size_t)iclamp(gi0 + r, 0, f.H - 1) * f.W + iclamp(gj0 + c, 0, f.W - 1);
-                cp_async4(Ys + idx, a.Y + g);
-                cp_async4(Ds + idx, a.D + g);
+            for (int p = 0; p < 6; ++p) {
+                float* dst = Es + p * P + r * RW + c0;
+                if (pair) {
+                    cp_async8(dst, a.E + p * HW + ga);
+                } else {
+                    cp_async4(dst, a.E + p * HW + ga);
+                    cp_async4(dst + 1, a.E + p * HW + gb);
+                }
             }
         }
+        cp_async_commit();
+        if (a.upd) {
+            if (!edgeC && !edgeR && (f.W & 3) == 0 && (gj0 & 3) == 0) {
+                for (int idx = tid; idx < P / 4; idx += NT) {
+                    const int r = idx / (RW / 4), c = (idx % (RW / 4)) * 4;
+                    const size_t g = plane + (size_t)(gi0 + r) * f.W + (gj0 + c);
+                    cp_async16(Ys + r * RW + c, a.Y + g);
+                    cp_async16(Ds + r * RW + c, a.D + g);
+                }
+            } else {
+                for (int idx = tid; idx < P; idx += NT) {
+                    const int r = idx / RW, c = idx % RW;
+                    const size_t g = plane + (size_t)iclamp(gi0 + r, 0, f.H - 1) * f.W + iclamp(gj0 + c, 0, f.W - 1);
+                    cp_async4(Ys + idx, a.Y + g);
+                    cp_async4(Ds + idx, a.D + g);
+                }
+            }
+        }
+        cp_async_commit();
     }
-    cp_async_commit();
 
-    // ---------------- own fields and directions (registers)
+    // ---------------- own fields and directions -> registers
     float4 f0[K], f1[K];
     float s0x[K], s0y[K], s0z[K], s1x[K], s1y[K], s1z[K];
     float mx[K];
@@ -185,13 +203,13 @@ __device__ __forceinline__ void fused_body(const FusedArgs& a, float* sm) {
         s1z[k] = sb.z;
         mx[k] = 0.0f;
     }
-    cp_async_wait<1>();  // own e planes landed (each thread copied exactly the cells it reads)
+    cp_async_wait<1>();  // own e cells landed (each thread reads only what it copied until the 1st barrier)
 
-    // boundary predicates (EDGE only): grid edge at the thread's columns / rows
-    const bool atL = EDGE && c0 <= cmin;      // cell 0 is at (or left of) the grid's left edge
-    const bool atR1 = EDGE && c0 + 1 >= cmax; // cell 1 is at (or right of) the grid's right edge
-    const bool atR0 = EDGE && c0 >= cmax;     // odd W: cell 0 is the right edge, cell 1 outside
+    const bool atL = c0 <= cmin;       // cell 0 at / left of the grid's left edge
+    const bool atR1 = c0 + 1 >= cmax;  // cell 1 at / right of the grid's right edge
+    const bool atR0 = c0 >= cmax;      // odd W: cell 0 is the right edge, cell 1 outside
     const float ndt = -f.dt, U = f.U;
+    const int srcL = lane - 1, srcR = lane + 1;
 
     for (int n = 0; n < a.M; ++n) {
         // ================= column pass (beta_1): registers + shuffles only
@@ -203,30 +221,38 @@ __device__ __forceinline__ void fused_body(const FusedArgs& a, float* sm) {
             const float2 ez = *reinterpret_cast<const float2*>(Es + 2 * P + ib);
             const float u0 = dot3s(ex.x, ey.x, ez.x, f0[k]);
             const float u1 = dot3s(ex.y, ey.y, ez.y, f1[k]);
-            float uL = __shfl_up_sync(FULL, u1, 1);   // lane-1's cell 1: left of cell 0
-            float uR = __shfl_down_sync(FULL, u0, 1); // lane+1's cell 0: right of cell 1
-            float4 fL = shfl_up4(f1[k]);
-            float4 fR = shfl_dn4(f0[k]);
-            float u1n = u1;       // right neighbour of cell 0
-            float4 f1n = f1[k];
-            if (EDGE) {
+            float uL = __shfl_up_sync(FULL, u1, 1);    // lane-1's cell 1 = left of cell 0
+            float uR = __shfl_down_sync(FULL, u0, 1);  // lane+1's cell 0 = right of cell 1
+            float u1n = u1;                            // right of cell 0
+            if (edgeC) {
                 uL = atL ? u0 : uL;
-                fL = sel4(atL, f0[k], fL);
                 uR = atR1 ? u1 : uR;
-                fR = sel4(atR1, f1[k], fR);
                 u1n = atR0 ? u0 : u1;
-                f1n = sel4(atR0, f0[k], f1[k]);
             }
             float uh0 = dominant(uL, u1n, f.rule);
             float uh1 = dominant(u0, uR, f.rule);
-            // (odd W, EDGE: cell 1 may be outside the grid; keep its |u_hat| out of the flag max)
             mx[k] = fmaxf(mx[k], fmaxf(fabsf(uh0), fabsf(atR0 ? uh0 : uh1)));
             if (f.clamp) {
                 uh0 = fminf(fmaxf(uh0, -U), U);
                 uh1 = fminf(fmaxf(uh1, -U), U);
             }
-            const float4 fu0 = sel4(uh0 > 0.0f, fL, f1n);
-            const float4 fu1 = sel4(uh1 > 0.0f, f0[k], fR);
+            const bool fw0 = uh0 > 0.0f, fw1 = uh1 > 0.0f;
+            // upwind value by per-lane source: cell 0 takes lane-1's cell 1 (fw) or its own cell 1;
+            // cell 1 takes its own cell 0 (fw) or lane+1's cell 0
+            const int s0 = fw0 ? srcL : lane, s1 = fw1 ? lane : srcR;
+            float4 fu0, fu1;
+            fu0.x = __shfl_sync(FULL, f1[k].x, s0);
+            fu0.y = __shfl_sync(FULL, f1[k].y, s0);
+            fu0.z = __shfl_sync(FULL, f1[k].z, s0);
+            fu0.w = __shfl_sync(FULL, f1[k].w, s0);
+            fu1.x = __shfl_sync(FULL, f0[k].x, s1);
+            fu1.y = __shfl_sync(FULL, f0[k].y, s1);
+            fu1.z = __shfl_sync(FULL, f0[k].z, s1);
+            fu1.w = __shfl_sync(FULL, f0[k].w, s1);
+            if (edgeC) {
+                fu0 = sel4((atL && fw0) || (atR0 && !fw0), f0[k], fu0);
+                fu1 = sel4(atR1 && !fw1, f1[k], fu1);
+            }
             const float q0 = xmul(f.sigma, dot3s(s0x[k], s0y[k], s0z[k], f0[k]));
             const float q1 = xmul(f.sigma, dot3s(s1x[k], s1y[k], s1z[k], f1[k]));
             f0[k] = transport(f0[k], fu0, fabsf(uh0), q0, ndt);
@@ -235,7 +261,6 @@ __device__ __forceinline__ void fused_body(const FusedArgs& a, float* sm) {
         // ================= row pass (beta_2, reading 3)
         {
             float4* const XR = XR0 + (n & 1) * C::XR;
-            // publish the run ends (fields only; neighbours recompute v from the e2 planes)
             XR[(wy * 2 + 0) * RW + c0] = f0[0];
             XR[(wy * 2 + 0) * RW + c0 + 1] = f1[0];
             XR[(wy * 2 + 1) * RW + c0] = f0[K - 1];
@@ -254,10 +279,9 @@ __device__ __forceinline__ void fused_body(const FusedArgs& a, float* sm) {
             float4 t0 = f0[0], t1 = f1[0], b0 = f0[K - 1], b1 = f1[K - 1];
             float vt0 = v0[0], vt1 = v1[0], vb0 = v0[K - 1], vb1 = v1[K - 1];
             if (wy > 0) {
-                const int rt = r0 - 1;
                 t0 = XR[((wy - 1) * 2 + 1) * RW + c0];
                 t1 = XR[((wy - 1) * 2 + 1) * RW + c0 + 1];
-                const int ib = rt * RW + c0;
+                const int ib = (r0 - 1) * RW + c0;
                 const float2 ex = *reinterpret_cast<const float2*>(Es + 3 * P + ib);
                 const float2 ey = *reinterpret_cast<const float2*>(Es + 4 * P + ib);
                 const float2 ez = *reinterpret_cast<const float2*>(Es + 5 * P + ib);
@@ -265,24 +289,23 @@ __device__ __forceinline__ void fused_body(const FusedArgs& a, float* sm) {
                 vt1 = dot3s(ex.y, ey.y, ez.y, t1);
             }
             if (wy < NWY - 1) {
-                const int rb = r0 + K;
                 b0 = XR[((wy + 1) * 2 + 0) * RW + c0];
                 b1 = XR[((wy + 1) * 2 + 0) * RW + c0 + 1];
-                const int ib = rb * RW + c0;
+                const int ib = (r0 + K) * RW + c0;
                 const float2 ex = *reinterpret_cast<const float2*>(Es + 3 * P + ib);
                 const float2 ey = *reinterpret_cast<const float2*>(Es + 4 * P + ib);
                 const float2 ez = *reinterpret_cast<const float2*>(Es + 5 * P + ib);
                 vb0 = dot3s(ex.x, ey.x, ez.x, b0);
                 vb1 = dot3s(ex.y, ey.y, ez.y, b1);
             }
-            float4 p0 = t0, p1 = t1;  // old values of the row above
+            float4 p0 = t0, p1 = t1;  // pre-pass values of the row above
 #pragma unroll
             for (int k = 0; k < K; ++k) {
                 float vm0 = (k > 0) ? v0[k - 1] : vt0, vm1 = (k > 0) ? v1[k - 1] : vt1;
                 float vp0 = (k < K - 1) ? v0[k + 1] : vb0, vp1 = (k < K - 1) ? v1[k + 1] : vb1;
                 float4 fm0 = p0, fm1 = p1;
                 float4 fp0 = (k < K - 1) ? f0[k + 1] : b0, fp1 = (k < K - 1) ? f1[k + 1] : b1;
-                if (EDGE) {
+                if (edgeR) {
                     const int r = r0 + k;
                     if (r <= rmin) {
                         vm0 = v0[k];
@@ -318,197 +341,155 @@ __device__ __forceinline__ void fused_body(const FusedArgs& a, float* sm) {
 
     // ---------------- flags from tile cells (exact at every pass); |u_hat| before the clamp
     unsigned fl = 0;
-    const bool tcol = c0 >= R && c0 < R + TW && c0 >= cmin && c0 <= cmax;  // c0 even, R/TW even: both or none
+    {
+        const bool tcol = c0 >= R && c0 < R + TW && c0 >= cmin && c0 <= cmax;  // R, TW even: both cells or none
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-        const int r = r0 + k;
-        const bool t = tcol && r >= R && r < R + TH && r >= rmin && r <= rmax;
-        if (t) {
-            if (f.clamp) {
-                if (mx[k] > U) fl |= SF_FLAG_CLAMPED;
-            } else if (xmul(f.dt, mx[k]) > 1.0f) {
-                fl |= SF_FLAG_CFL;
+        for (int k = 0; k < K; ++k) {
+            const int r = r0 + k;
+            if (tcol && r >= R && r < R + TH && r >= rmin && r <= rmax) {
+                if (f.clamp) {
+                    if (mx[k] > U) fl |= SF_FLAG_CLAMPED;
+                } else if (xmul(f.dt, mx[k]) > 1.0f) {
+                    fl |= SF_FLAG_CFL;
+                }
             }
         }
     }
 
-    if (a.upd) {
-        const int S = f.S;
+    if (!a.upd) {  // intermediate launch: store the partial prediction of the tile
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const int r = r0 + k;
+            if (r >= R && r < R + TH && r >= rmin && r <= rmax) {
+                const size_t g = plane + (size_t)(gi0 + r) * f.W + (gj0 + c0);
+                if (c0 >= R && c0 < R + TW && c0 >= cmin && c0 <= cmax) a.fout[g] = f0[k];
+                if (c0 + 1 >= R && c0 + 1 < R + TW && c0 + 1 >= cmin && c0 + 1 <= cmax) a.fout[g + 1] = f1[k];
+            }
+        }
+    } else {
+        // =========================== update (U1-U5) on shared planes, compact runtime loops
+        float* const Fx = sm;  // w^{k+}, rho^{k+} -> w_LS, rho^{k+1} (in place)
+        float* const Fy = sm + P;
+        float* const Fz = sm + 2 * P;
+        float* const Fw = sm + 3 * P;
+        float* const HG = sm + 4 * P;
+        float* const HH = sm + 5 * P;
+        __syncthreads();  // e planes and row buffers are dead from here on
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const int ib = (r0 + k) * RW + c0;
+            *reinterpret_cast<float2*>(Fx + ib) = make_float2(f0[k].x, f1[k].x);
+            *reinterpret_cast<float2*>(Fy + ib) = make_float2(f0[k].y, f1[k].y);
+            *reinterpret_cast<float2*>(Fz + ib) = make_float2(f0[k].z, f1[k].z);
+            *reinterpret_cast<float2*>(Fw + ib) = make_float2(f0[k].w, f1[k].w);
+        }
         cp_async_wait<0>();
-        __syncthreads();  // Y / depth planes complete; row buffers free
-        float* const HG = Xb;
-        float* const HH = Xb + P;
+        __syncthreads();
         const float qnan = __int_as_float(0x7fffffff);
-        // rhohat plane (NaN = no measurement) in place of depth; horizontal brightness taps
-        for (int idx = tid; idx < P; idx += NT) {
+#pragma unroll 1
+        for (int idx = tid; idx < P; idx += NT) {  // rhohat plane + horizontal brightness taps
             const float d = Ds[idx];
             Ds[idx] = depth_valid(d, f.is_inv) ? rho_hat(d, f.is_inv) : qnan;
-            const int c = idx % RW;
+            const int r = idx / RW, c = idx % RW;
             if (c >= 2 && c <= RW - 3) {
                 const float x0 = Ys[idx - 2], x1 = Ys[idx - 1], x2 = Ys[idx], x3 = Ys[idx + 1], x4 = Ys[idx + 2];
                 HG[idx] = tap_g(x0, x1, x2, x3, x4);
                 HH[idx] = tap_h(x0, x1, x2, x3, x4);
             }
-            const int r = idx / RW;
             if (r >= R && r < R + TH && c >= R && c < R + TW && r >= rmin && r <= rmax && c >= cmin && c <= cmax &&
                 !isfinite(Ys[idx]))
                 fl |= SF_FLAG_NONFINITE;
         }
         __syncthreads();
-        const int slo = R - 2 * S, shi_r = R + TH + 2 * S, shi_c = R + TW + 2 * S;
-        const bool scol0 = c0 >= slo && c0 < shi_c && c0 >= cmin && c0 <= cmax;
-        const bool scol1 = c0 + 1 >= slo && c0 + 1 < shi_c && c0 + 1 >= cmin && c0 + 1 <= cmax;
+        const int S = f.S;
+        const int rlo = max(R - 2 * S, rmin), rhi = min(R + TH + 2 * S - 1, rmax);
+        const int clo = max(R - 2 * S, cmin), chi = min(R + TW + 2 * S - 1, cmax);
+        const int nc = chi - clo + 1, ncell = (rhi - rlo + 1) * nc;
+#pragma unroll 1
+        for (int t = tid; t < ncell; t += NT) {  // per-pixel LS (eq:LS_update) + fusion, solve region
+            const int r = rlo + t / nc, c = clo + t % nc;
+            const int idx = r * RW + c;
+            const float g0 = HG[idx - 2 * RW], g1 = HG[idx - RW], g2 = HG[idx], g3 = HG[idx + RW], g4 = HG[idx + 2 * RW];
+            const float h0 = HH[idx - 2 * RW], h1 = HH[idx - RW], h2 = HH[idx], h3 = HH[idx + RW], h4 = HH[idx + 2 * RW];
+            const float yh = tap_g(g0, g1, g2, g3, g4);  // Yhat^{k+1}
+            const float be1 = tap_g(h0, h1, h2, h3, h4);
+            const float be2 = tap_h(g0, g1, g2, g3, g4);
+            const float rc = Ds[idx], rl = Ds[idx - 1], rr = Ds[idx + 1], ru = Ds[idx - RW], rd = Ds[idx + RW];
+            const bool vc = !isnan(rc), vl = !isnan(rl), vr = !isnan(rr), vu = !isnan(ru), vd = !isnan(rd);
+            const float rh = vc ? rc : 0.0f;
+            const float br1 = pick_side(rh, vc, rl, vl, rr, vr);  // eq:dominant_b1
+            const float br2 = pick_side(rh, vc, ru, vu, rd, vd);  // eq:dominant_b2
+            const size_t g = (size_t)(gi0 + r) * f.W + (gj0 + c);
+            const float4 s4 = __ldg(a.G0 + g);
+            const float4 e1 = __ldg(a.G1 + g), e2 = __ldg(a.G2 + g);
+            const float d2 = s4.w;
+            const float e1a[3] = {e1.x, e1.y, e1.z}, e2a[3] = {e2.x, e2.y, e2.z}, sa[3] = {s4.x, s4.y, s4.z};
+            float gh[3], m[3];
+            const float d2r = xmul(d2, rh);
 #pragma unroll
-        for (int k = 0; k < K; ++k) {
-            const int r = r0 + k;
-            const bool srow = r >= slo && r < shi_r && r >= rmin && r <= rmax;
-#pragma unroll
-            for (int j = 0; j < 2; ++j) {
-                float4& fv = j ? f1[k] : f0[k];
-                const bool solve = srow && (j ? scol1 : scol0);
-                if (!solve) {
-                    fv = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-                    continue;
-                }
-                const int c = c0 + j;
-                const int idx = r * RW + c;
-                const float g0 = HG[idx - 2 * RW], g1 = HG[idx - RW], g2 = HG[idx], g3 = HG[idx + RW], g4 = HG[idx + 2 * RW];
-                const float h0 = HH[idx - 2 * RW], h1 = HH[idx - RW], h2 = HH[idx], h3 = HH[idx + RW], h4 = HH[idx + 2 * RW];
-                const float yh = tap_g(g0, g1, g2, g3, g4);  // Yhat^{k+1}
-                const float be1 = tap_g(h0, h1, h2, h3, h4);
-                const float be2 = tap_h(g0, g1, g2, g3, g4);
-                const float rc = Ds[idx], rl = Ds[idx - 1], rr = Ds[idx + 1], ru = Ds[idx - RW], rd = Ds[idx + RW];
-                const bool vc = !isnan(rc), vl = !isnan(rl), vr = !isnan(rr), vu = !isnan(ru), vd = !isnan(rd);
-                const float rh = vc ? rc : 0.0f;
-                const float br1 = pick_side(rh, vc, rl, vl, rr, vr);  // eq:dominant_b1
-                const float br2 = pick_side(rh, vc, ru, vu, rd, vd);  // eq:dominant_b2
-                const size_t g = (size_t)(gi0 + r) * f.W + (gj0 + c);
-                const float d2 = __ldg(&a.G0[g].w);
-                const float e1a[3] = {Es[idx], Es[P + idx], Es[2 * P + idx]};
-                const float e2a[3] = {Es[3 * P + idx], Es[4 * P + idx], Es[5 * P + idx]};
-                const float sa[3] = {j ? s1x[k] : s0x[k], j ? s1y[k] : s0y[k], j ? s1z[k] : s0z[k]};
-                float gh[3], m[3];
-                const float d2r = xmul(d2, rh);
-#pragma unroll
-                for (int q = 0; q < 3; ++q) {
-                    gh[q] = xmul(d2, xfma(e2a[q], be2, xmul(e1a[q], be1)));
-                    const float dr = xmul(d2, xfma(e2a[q], br2, xmul(e1a[q], br1)));
-                    m[q] = xfma(d2r, sa[q], dr);
-                }
-                const float cY = xmul(d2, xsub(yh, a.yin[plane + g]));  // eq:img_cost_top
-                const float cr = xmul(d2, xsub(rh, a.sk[plane + g].w));  // eq:invdepth_cost_top
-                const float wp[3] = {fv.x, fv.y, fv.z};
-                float x[3];
-                ls_solve3(gh, m, cY, cr, wp, f.g1, vc ? f.g2 : 0.0f, f.g3, x);
-                const float kap = vc ? f.kappa : 0.0f;
-                const float rn = xfma(kap, xsub(rh, fv.w), fv.w);  // fusion
-                fv = make_float4(x[0], x[1], x[2], rn);
-                if (!(isfinite(x[0]) && isfinite(x[1]) && isfinite(x[2]) && isfinite(rn))) fl |= SF_FLAG_NONFINITE;
-                if (r >= R && r < R + TH && c >= R && c < R + TW) a.yout[plane + g] = yh;
+            for (int q = 0; q < 3; ++q) {
+                gh[q] = xmul(d2, xfma(e2a[q], be2, xmul(e1a[q], be1)));
+                const float dr = xmul(d2, xfma(e2a[q], br2, xmul(e1a[q], br1)));
+                m[q] = xfma(d2r, sa[q], dr);
             }
+            const float cY = xmul(d2, xsub(yh, a.yin[plane + g]));  // eq:img_cost_top
+            const float cr = xmul(d2, xsub(rh, a.sk[plane + g].w));  // eq:invdepth_cost_top
+            const float wp[3] = {Fx[idx], Fy[idx], Fz[idx]};
+            const float rp = Fw[idx];
+            float x[3];
+            ls_solve3(gh, m, cY, cr, wp, f.g1, vc ? f.g2 : 0.0f, f.g3, x);
+            const float kap = vc ? f.kappa : 0.0f;
+            const float rn = xfma(kap, xsub(rh, rp), rp);  // fusion
+            Fx[idx] = x[0];
+            Fy[idx] = x[1];
+            Fz[idx] = x[2];
+            Fw[idx] = rn;
+            if (!(isfinite(x[0]) && isfinite(x[1]) && isfinite(x[2]) && isfinite(rn))) fl |= SF_FLAG_NONFINITE;
+            if (r >= R && r < R + TH && c >= R && c < R + TW) a.yout[plane + g] = yh;
         }
-        // ---- S x 5x5 box: horizontal 5-sum, vertical 5-sum, / 25; replicate border
-        float* const Wx = Ys;
-        float* const Wy = Ds;
-        float* const Wz = Xb;
+        // ---- S x 5x5 box (reading 13): horizontal 5-sum -> Tq, vertical 5-sum / 25 -> Fq
+        float* const Tx = Ys;
+        float* const Ty = Ds;
+        float* const Tz = HG;
         for (int it = 0; it < S; ++it) {
             __syncthreads();
-#pragma unroll
-            for (int k = 0; k < K; ++k) {
-                const int ib = (r0 + k) * RW + c0;
-                *reinterpret_cast<float2*>(Wx + ib) = make_float2(f0[k].x, f1[k].x);
-                *reinterpret_cast<float2*>(Wy + ib) = make_float2(f0[k].y, f1[k].y);
-                *reinterpret_cast<float2*>(Wz + ib) = make_float2(f0[k].z, f1[k].z);
+#pragma unroll 1
+            for (int idx = tid; idx < P; idx += NT) {
+                const int r = idx / RW, c = idx % RW;
+                const int rb = r * RW;
+                const int j0 = rb + iclamp(c - 2, cmin, cmax), j1 = rb + iclamp(c - 1, cmin, cmax),
+                          j2 = rb + iclamp(c, cmin, cmax), j3 = rb + iclamp(c + 1, cmin, cmax),
+                          j4 = rb + iclamp(c + 2, cmin, cmax);
+                Tx[idx] = xadd(xadd(xadd(xadd(Fx[j0], Fx[j1]), Fx[j2]), Fx[j3]), Fx[j4]);
+                Ty[idx] = xadd(xadd(xadd(xadd(Fy[j0], Fy[j1]), Fy[j2]), Fy[j3]), Fy[j4]);
+                Tz[idx] = xadd(xadd(xadd(xadd(Fz[j0], Fz[j1]), Fz[j2]), Fz[j3]), Fz[j4]);
             }
             __syncthreads();
-            float hx0[K], hy0[K], hz0[K], hx1[K], hy1[K], hz1[K];
-#pragma unroll
-            for (int k = 0; k < K; ++k) {
-                const int rb = (r0 + k) * RW;
-                int cc[6];
-#pragma unroll
-                for (int t = 0; t < 6; ++t) {
-                    const int cx = c0 - 2 + t;
-                    cc[t] = EDGE ? iclamp(cx, max(cmin, 0), min(cmax, RW - 1)) : max(0, min(cx, RW - 1));
-                }
-                const float* P3[3] = {Wx, Wy, Wz};
-                float o0[3], o1[3];
-#pragma unroll
-                for (int q = 0; q < 3; ++q) {
-                    const float* Wq = P3[q] + rb;
-                    const float a0 = Wq[cc[0]], a1 = Wq[cc[1]], a2 = Wq[cc[2]], a3 = Wq[cc[3]], a4 = Wq[cc[4]],
-                                a5 = Wq[cc[5]];
-                    o0[q] = xadd(xadd(xadd(xadd(a0, a1), a2), a3), a4);  // columns c0-2 .. c0+2
-                    o1[q] = xadd(xadd(xadd(xadd(a1, a2), a3), a4), a5);  // columns c0-1 .. c0+3
-                }
-                hx0[k] = o0[0];
-                hy0[k] = o0[1];
-                hz0[k] = o0[2];
-                hx1[k] = o1[0];
-                hy1[k] = o1[1];
-                hz1[k] = o1[2];
-            }
-            __syncthreads();
-#pragma unroll
-            for (int k = 0; k < K; ++k) {
-                const int ib = (r0 + k) * RW + c0;
-                *reinterpret_cast<float2*>(Wx + ib) = make_float2(hx0[k], hx1[k]);
-                *reinterpret_cast<float2*>(Wy + ib) = make_float2(hy0[k], hy1[k]);
-                *reinterpret_cast<float2*>(Wz + ib) = make_float2(hz0[k], hz1[k]);
-            }
-            __syncthreads();
-#pragma unroll
-            for (int k = 0; k < K; ++k) {
-                const int r = r0 + k;
-                int ri[5];
-#pragma unroll
-                for (int t = 0; t < 5; ++t) {
-                    const int rx = r - 2 + t;
-                    ri[t] = (EDGE ? iclamp(rx, rmin, rmax) : max(0, min(rx, C::RH - 1))) * RW + c0;
-                }
-                const float2 x0 = *reinterpret_cast<const float2*>(Wx + ri[0]), x1 = *reinterpret_cast<const float2*>(Wx + ri[1]),
-                             x2 = *reinterpret_cast<const float2*>(Wx + ri[2]), x3 = *reinterpret_cast<const float2*>(Wx + ri[3]),
-                             x4 = *reinterpret_cast<const float2*>(Wx + ri[4]);
-                const float2 y0 = *reinterpret_cast<const float2*>(Wy + ri[0]), y1 = *reinterpret_cast<const float2*>(Wy + ri[1]),
-                             y2 = *reinterpret_cast<const float2*>(Wy + ri[2]), y3 = *reinterpret_cast<const float2*>(Wy + ri[3]),
-                             y4 = *reinterpret_cast<const float2*>(Wy + ri[4]);
-                const float2 z0 = *reinterpret_cast<const float2*>(Wz + ri[0]), z1 = *reinterpret_cast<const float2*>(Wz + ri[1]),
-                             z2 = *reinterpret_cast<const float2*>(Wz + ri[2]), z3 = *reinterpret_cast<const float2*>(Wz + ri[3]),
-                             z4 = *reinterpret_cast<const float2*>(Wz + ri[4]);
-                f0[k].x = __fdiv_rn(xadd(xadd(xadd(xadd(x0.x, x1.x), x2.x), x3.x), x4.x), 25.0f);
-                f1[k].x = __fdiv_rn(xadd(xadd(xadd(xadd(x0.y, x1.y), x2.y), x3.y), x4.y), 25.0f);
-                f0[k].y = __fdiv_rn(xadd(xadd(xadd(xadd(y0.x, y1.x), y2.x), y3.x), y4.x), 25.0f);
-                f1[k].y = __fdiv_rn(xadd(xadd(xadd(xadd(y0.y, y1.y), y2.y), y3.y), y4.y), 25.0f);
-                f0[k].z = __fdiv_rn(xadd(xadd(xadd(xadd(z0.x, z1.x), z2.x), z3.x), z4.x), 25.0f);
-                f1[k].z = __fdiv_rn(xadd(xadd(xadd(xadd(z0.y, z1.y), z2.y), z3.y), z4.y), 25.0f);
+#pragma unroll 1
+            for (int idx = tid; idx < P; idx += NT) {
+                const int r = idx / RW, c = idx % RW;
+                const int i0 = iclamp(r - 2, rmin, rmax) * RW + c, i1 = iclamp(r - 1, rmin, rmax) * RW + c,
+                          i2 = iclamp(r, rmin, rmax) * RW + c, i3 = iclamp(r + 1, rmin, rmax) * RW + c,
+                          i4 = iclamp(r + 2, rmin, rmax) * RW + c;
+                Fx[idx] = __fdiv_rn(xadd(xadd(xadd(xadd(Tx[i0], Tx[i1]), Tx[i2]), Tx[i3]), Tx[i4]), 25.0f);
+                Fy[idx] = __fdiv_rn(xadd(xadd(xadd(xadd(Ty[i0], Ty[i1]), Ty[i2]), Ty[i3]), Ty[i4]), 25.0f);
+                Fz[idx] = __fdiv_rn(xadd(xadd(xadd(xadd(Tz[i0], Tz[i1]), Tz[i2]), Tz[i3]), Tz[i4]), 25.0f);
             }
         }
-    }
-    // ---------------- store the tile (2 adjacent cells per thread per row: coalesced)
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-        const int r = r0 + k;
-        if (r >= R && r < R + TH && r >= rmin && r <= rmax) {
-            const size_t g = plane + (size_t)(gi0 + r) * f.W + (gj0 + c0);
-            if (c0 >= R && c0 < R + TW && c0 >= cmin && c0 <= cmax) a.fout[g] = f0[k];
-            if (c0 + 1 >= R && c0 + 1 < R + TW && c0 + 1 >= cmin && c0 + 1 <= cmax) a.fout[g + 1] = f1[k];
+        __syncthreads();
+        // ---- store the tile: (w^{k+1}, rho^{k+1}), coalesced along rows
+        const int tr0 = max(R, rmin), tr1 = min(R + TH - 1, rmax);
+        const int tc0 = max(R, cmin), tc1 = min(R + TW - 1, cmax);
+        const int tnc = tc1 - tc0 + 1, tn = (tr1 - tr0 + 1) * tnc;
+#pragma unroll 1
+        for (int t = tid; t < tn; t += NT) {
+            const int r = tr0 + t / tnc, c = tc0 + t % tnc;
+            const int idx = r * RW + c;
+            a.fout[plane + (size_t)(gi0 + r) * f.W + (gj0 + c)] = make_float4(Fx[idx], Fy[idx], Fz[idx], Fw[idx]);
         }
     }
     const unsigned any = __reduce_or_sync(FULL, fl);
     if (lane == 0 && any) atomicOr(a.flags, any);
-}
-
-template <int K, int NWY>
-__global__ void __launch_bounds__(32 * NWY, 1) k_fused(const FusedArgs a) {
-    extern __shared__ float4 smem4[];
-    float* sm = reinterpret_cast<float*>(smem4);
-    using C = Cfg<K, NWY>;
-    const int gi0 = blockIdx.y * a.TH - a.R, gj0 = blockIdx.x * a.TW - a.R;
-    const bool edge = gi0 < 0 || gj0 < 0 || gi0 + C::RH > a.f.H || gj0 + C::RW > a.f.W;
-    if (edge)
-        fused_body<K, NWY, true>(a, sm);
-    else
-        fused_body<K, NWY, false>(a, sm);
 }
 
 // The configuration used today: RW = 64, RH = 72 (K = 6 rows x 12 warps), 384 threads, 1 CTA / SM.
@@ -564,6 +545,8 @@ cudaError_t sf_launch_fused_step(sf_ctx* c, const float* Y, const float* D) {
         a.Y = Y;
         a.D = D;
         a.G0 = c->G0;
+        a.G1 = c->G1;
+        a.G2 = c->G2;
         a.E = c->E;
         a.flags = c->flags;
         a.f = f;
