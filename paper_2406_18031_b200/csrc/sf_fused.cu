@@ -120,7 +120,7 @@ struct Cfg {
     static constexpr size_t SMEM = sizeof(float) * (8 * (size_t)P + XRF);
 };
 
-template <int K, int NWY>
+template <int K, int NWY, int RULE, bool CLAMP>
 __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const FusedArgs a) {
     using C = Cfg<K, NWY>;
     constexpr int RW = C::RW, RH = C::RH, P = C::P, NT = C::NT;
@@ -229,10 +229,10 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const FusedArgs a) {
                 uR = atR1 ? u1 : uR;
                 u1n = atR0 ? u0 : u1;
             }
-            float uh0 = dominant(uL, u1n, f.rule);
-            float uh1 = dominant(u0, uR, f.rule);
+            float uh0 = dominant(uL, u1n, RULE);
+            float uh1 = dominant(u0, uR, RULE);
             mx[k] = fmaxf(mx[k], fmaxf(fabsf(uh0), fabsf(atR0 ? uh0 : uh1)));
-            if (f.clamp) {
+            if (CLAMP) {
                 uh0 = fminf(fmaxf(uh0, -U), U);
                 uh1 = fminf(fmaxf(uh1, -U), U);
             }
@@ -320,10 +320,10 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const FusedArgs a) {
                         fp1 = f1[k];
                     }
                 }
-                float vh0 = dominant(vm0, vp0, f.rule);
-                float vh1 = dominant(vm1, vp1, f.rule);
+                float vh0 = dominant(vm0, vp0, RULE);
+                float vh1 = dominant(vm1, vp1, RULE);
                 mx[k] = fmaxf(mx[k], fmaxf(fabsf(vh0), fabsf(atR0 ? vh0 : vh1)));
-                if (f.clamp) {
+                if (CLAMP) {
                     vh0 = fminf(fmaxf(vh0, -U), U);
                     vh1 = fminf(fmaxf(vh1, -U), U);
                 }
@@ -347,7 +347,7 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const FusedArgs a) {
         for (int k = 0; k < K; ++k) {
             const int r = r0 + k;
             if (tcol && r >= R && r < R + TH && r >= rmin && r <= rmax) {
-                if (f.clamp) {
+                if (CLAMP) {
                     if (mx[k] > U) fl |= SF_FLAG_CLAMPED;
                 } else if (xmul(f.dt, mx[k]) > 1.0f) {
                     fl |= SF_FLAG_CFL;
@@ -386,24 +386,27 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const FusedArgs a) {
         cp_async_wait<0>();
         __syncthreads();
         const float qnan = __int_as_float(0x7fffffff);
+        const int S = f.S;
+        // solve region = tile + 2S (clipped to the grid); models needed on it +-2 rows, +-1 cols
+        const int rlo = max(R - 2 * S, rmin), rhi = min(R + TH + 2 * S - 1, rmax);
+        const int clo = max(R - 2 * S, cmin), chi = min(R + TW + 2 * S - 1, cmax);
+        {
+            const int mr0 = rlo - 2, mc0 = clo - 1, mnc = (chi + 1) - mc0 + 1, mn = ((rhi + 2) - mr0 + 1) * mnc;
 #pragma unroll 1
-        for (int idx = tid; idx < P; idx += NT) {  // rhohat plane + horizontal brightness taps
-            const float d = Ds[idx];
-            Ds[idx] = depth_valid(d, f.is_inv) ? rho_hat(d, f.is_inv) : qnan;
-            const int r = idx / RW, c = idx % RW;
-            if (c >= 2 && c <= RW - 3) {
+            for (int t = tid; t < mn; t += NT) {  // rhohat plane + horizontal brightness taps
+                const int r = mr0 + t / mnc, c = mc0 + t % mnc;
+                const int idx = r * RW + c;
+                const float d = Ds[idx];
+                Ds[idx] = depth_valid(d, f.is_inv) ? rho_hat(d, f.is_inv) : qnan;
                 const float x0 = Ys[idx - 2], x1 = Ys[idx - 1], x2 = Ys[idx], x3 = Ys[idx + 1], x4 = Ys[idx + 2];
                 HG[idx] = tap_g(x0, x1, x2, x3, x4);
                 HH[idx] = tap_h(x0, x1, x2, x3, x4);
+                if (r >= R && r < R + TH && c >= R && c < R + TW && r >= rmin && r <= rmax && c >= cmin &&
+                    c <= cmax && !isfinite(x2))
+                    fl |= SF_FLAG_NONFINITE;
             }
-            if (r >= R && r < R + TH && c >= R && c < R + TW && r >= rmin && r <= rmax && c >= cmin && c <= cmax &&
-                !isfinite(Ys[idx]))
-                fl |= SF_FLAG_NONFINITE;
         }
         __syncthreads();
-        const int S = f.S;
-        const int rlo = max(R - 2 * S, rmin), rhi = min(R + TH + 2 * S - 1, rmax);
-        const int clo = max(R - 2 * S, cmin), chi = min(R + TW + 2 * S - 1, cmax);
         const int nc = chi - clo + 1, ncell = (rhi - rlo + 1) * nc;
 #pragma unroll 1
         for (int t = tid; t < ncell; t += NT) {  // per-pixel LS (eq:LS_update) + fusion, solve region
@@ -451,29 +454,48 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const FusedArgs a) {
         float* const Tx = Ys;
         float* const Ty = Ds;
         float* const Tz = HG;
+        const bool edge = edgeC || edgeR;
         for (int it = 0; it < S; ++it) {
+            // output of this pass: tile + 2(S-1-it); its horizontal sums are needed 2 rows further
+            const int m = 2 * (S - 1 - it);
+            const int or0 = max(R - m, rmin), or1 = min(R + TH + m - 1, rmax);
+            const int oc0 = max(R - m, cmin), oc1 = min(R + TW + m - 1, cmax);
+            const int hr0 = max(or0 - 2, rmin), hr1 = min(or1 + 2, rmax);
+            const int onc = oc1 - oc0 + 1;
             __syncthreads();
+            const int hn = (hr1 - hr0 + 1) * onc;
 #pragma unroll 1
-            for (int idx = tid; idx < P; idx += NT) {
-                const int r = idx / RW, c = idx % RW;
-                const int rb = r * RW;
-                const int j0 = rb + iclamp(c - 2, cmin, cmax), j1 = rb + iclamp(c - 1, cmin, cmax),
-                          j2 = rb + iclamp(c, cmin, cmax), j3 = rb + iclamp(c + 1, cmin, cmax),
-                          j4 = rb + iclamp(c + 2, cmin, cmax);
-                Tx[idx] = xadd(xadd(xadd(xadd(Fx[j0], Fx[j1]), Fx[j2]), Fx[j3]), Fx[j4]);
-                Ty[idx] = xadd(xadd(xadd(xadd(Fy[j0], Fy[j1]), Fy[j2]), Fy[j3]), Fy[j4]);
-                Tz[idx] = xadd(xadd(xadd(xadd(Fz[j0], Fz[j1]), Fz[j2]), Fz[j3]), Fz[j4]);
+            for (int t = tid; t < hn; t += NT) {
+                const int r = hr0 + t / onc, c = oc0 + t % onc;
+                const int idx = r * RW + c;
+                int j0 = idx - 2, j1 = idx - 1, j3 = idx + 1, j4 = idx + 2;
+                if (edge) {
+                    const int rb = r * RW;
+                    j0 = rb + max(c - 2, cmin);
+                    j1 = rb + max(c - 1, cmin);
+                    j3 = rb + min(c + 1, cmax);
+                    j4 = rb + min(c + 2, cmax);
+                }
+                Tx[idx] = xadd(xadd(xadd(xadd(Fx[j0], Fx[j1]), Fx[idx]), Fx[j3]), Fx[j4]);
+                Ty[idx] = xadd(xadd(xadd(xadd(Fy[j0], Fy[j1]), Fy[idx]), Fy[j3]), Fy[j4]);
+                Tz[idx] = xadd(xadd(xadd(xadd(Fz[j0], Fz[j1]), Fz[idx]), Fz[j3]), Fz[j4]);
             }
             __syncthreads();
+            const int on = (or1 - or0 + 1) * onc;
 #pragma unroll 1
-            for (int idx = tid; idx < P; idx += NT) {
-                const int r = idx / RW, c = idx % RW;
-                const int i0 = iclamp(r - 2, rmin, rmax) * RW + c, i1 = iclamp(r - 1, rmin, rmax) * RW + c,
-                          i2 = iclamp(r, rmin, rmax) * RW + c, i3 = iclamp(r + 1, rmin, rmax) * RW + c,
-                          i4 = iclamp(r + 2, rmin, rmax) * RW + c;
-                Fx[idx] = __fdiv_rn(xadd(xadd(xadd(xadd(Tx[i0], Tx[i1]), Tx[i2]), Tx[i3]), Tx[i4]), 25.0f);
-                Fy[idx] = __fdiv_rn(xadd(xadd(xadd(xadd(Ty[i0], Ty[i1]), Ty[i2]), Ty[i3]), Ty[i4]), 25.0f);
-                Fz[idx] = __fdiv_rn(xadd(xadd(xadd(xadd(Tz[i0], Tz[i1]), Tz[i2]), Tz[i3]), Tz[i4]), 25.0f);
+            for (int t = tid; t < on; t += NT) {
+                const int r = or0 + t / onc, c = oc0 + t % onc;
+                const int idx = r * RW + c;
+                int i0 = idx - 2 * RW, i1 = idx - RW, i3 = idx + RW, i4 = idx + 2 * RW;
+                if (edge) {
+                    i0 = max(r - 2, rmin) * RW + c;
+                    i1 = max(r - 1, rmin) * RW + c;
+                    i3 = min(r + 1, rmax) * RW + c;
+                    i4 = min(r + 2, rmax) * RW + c;
+                }
+                Fx[idx] = __fdiv_rn(xadd(xadd(xadd(xadd(Tx[i0], Tx[i1]), Tx[idx]), Tx[i3]), Tx[i4]), 25.0f);
+                Fy[idx] = __fdiv_rn(xadd(xadd(xadd(xadd(Ty[i0], Ty[i1]), Ty[idx]), Ty[i3]), Ty[i4]), 25.0f);
+                Fz[idx] = __fdiv_rn(xadd(xadd(xadd(xadd(Tz[i0], Tz[i1]), Tz[idx]), Tz[i3]), Tz[i4]), 25.0f);
             }
         }
         __syncthreads();
@@ -523,8 +545,14 @@ bool sf_fused_supported(const sf_ctx* c) {
     for (int l = 0; l < p.launches; ++l)
         if (FC::RW - 2 * p.R[l] < 8 || FC::RH - 2 * p.R[l] < 8) return false;
     // opt in to the large dynamic shared-memory carve-out (one CTA per SM)
-    return cudaFuncSetAttribute(k_fused<FK, FNWY>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FC::SMEM) ==
-           cudaSuccess;
+    const void* fns[] = {(const void*)k_fused<FK, FNWY, SF_DOM_LARGEST, true>,
+                         (const void*)k_fused<FK, FNWY, SF_DOM_LARGEST, false>,
+                         (const void*)k_fused<FK, FNWY, SF_DOM_PRINTED, true>,
+                         (const void*)k_fused<FK, FNWY, SF_DOM_PRINTED, false>};
+    for (const void* fn : fns)
+        if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FC::SMEM) != cudaSuccess)
+            return false;
+    return true;
 }
 
 int sf_fused_launches(const sf_ctx* c) { return make_plan(c->fp).launches; }
@@ -556,7 +584,17 @@ cudaError_t sf_launch_fused_step(sf_ctx* c, const float* Y, const float* D) {
         a.TW = FC::RW - 2 * a.R;
         a.TH = FC::RH - 2 * a.R;
         const dim3 grid((f.W + a.TW - 1) / a.TW, (f.H + a.TH - 1) / a.TH, f.B);
-        k_fused<FK, FNWY><<<grid, FC::NT, FC::SMEM, c->stream>>>(a);
+        if (f.rule == SF_DOM_PRINTED) {
+            if (f.clamp)
+                k_fused<FK, FNWY, SF_DOM_PRINTED, true><<<grid, FC::NT, FC::SMEM, c->stream>>>(a);
+            else
+                k_fused<FK, FNWY, SF_DOM_PRINTED, false><<<grid, FC::NT, FC::SMEM, c->stream>>>(a);
+        } else {
+            if (f.clamp)
+                k_fused<FK, FNWY, SF_DOM_LARGEST, true><<<grid, FC::NT, FC::SMEM, c->stream>>>(a);
+            else
+                k_fused<FK, FNWY, SF_DOM_LARGEST, false><<<grid, FC::NT, FC::SMEM, c->stream>>>(a);
+        }
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
         src = a.fout;
