@@ -120,6 +120,160 @@ struct Cfg {
     static constexpr size_t SMEM = sizeof(float) * (8 * (size_t)P + XRF);
 };
 
+// The transport: M substeps of a column pass then a row pass on the thread's
+// 2 x K cells.  EDGE: the CTA's region touches the grid border (replicate clamp, reading 10).
+template <int K, int NWY, int RULE, bool CLAMP, bool EDGE>
+__device__ __forceinline__ void transport_passes(const FrameParams& f, int M, float4 (&f0)[K], float4 (&f1)[K],
+                                                 const float (&s0x)[K], const float (&s0y)[K], const float (&s0z)[K],
+                                                 const float (&s1x)[K], const float (&s1y)[K], const float (&s1z)[K],
+                                                 float (&mx)[K], const float* Es, float4* XR0, int lane, int wy,
+                                                 int cmin, int cmax, int rmin, int rmax) {
+    using C = Cfg<K, NWY>;
+    constexpr int RW = C::RW, P = C::P;
+    const int c0 = 2 * lane, r0 = K * wy;
+    const bool atL = c0 <= cmin;       // cell 0 at / left of the grid's left edge
+    const bool atR1 = c0 + 1 >= cmax;  // cell 1 at / right of the grid's right edge
+    const bool atR0 = c0 >= cmax;      // odd W: cell 0 is the right edge, cell 1 outside
+    const float ndt = -f.dt, U = f.U;
+    const int srcL = lane - 1, srcR = lane + 1;
+
+    for (int n = 0; n < M; ++n) {
+        // ================= column pass (beta_1, P:L663-673): registers + shuffles only
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const int ib = (r0 + k) * RW + c0;
+            const float2 ex = *reinterpret_cast<const float2*>(Es + ib);
+            const float2 ey = *reinterpret_cast<const float2*>(Es + P + ib);
+            const float2 ez = *reinterpret_cast<const float2*>(Es + 2 * P + ib);
+            const float u0 = dot3s(ex.x, ey.x, ez.x, f0[k]);
+            const float u1 = dot3s(ex.y, ey.y, ez.y, f1[k]);
+            float uL = __shfl_up_sync(FULL, u1, 1);    // lane-1's cell 1 = left of cell 0
+            float uR = __shfl_down_sync(FULL, u0, 1);  // lane+1's cell 0 = right of cell 1
+            float u1n = u1;                            // right of cell 0
+            if (EDGE) {
+                uL = atL ? u0 : uL;
+                uR = atR1 ? u1 : uR;
+                u1n = atR0 ? u0 : u1;
+            }
+            float uh0 = dominant(uL, u1n, RULE);
+            float uh1 = dominant(u0, uR, RULE);
+            mx[k] = fmaxf(mx[k], fmaxf(fabsf(uh0), fabsf(atR0 ? uh0 : uh1)));
+            if (CLAMP) {
+                uh0 = fminf(fmaxf(uh0, -U), U);
+                uh1 = fminf(fmaxf(uh1, -U), U);
+            }
+            const bool fw0 = uh0 > 0.0f, fw1 = uh1 > 0.0f;
+            // upwind value by per-lane source: cell 0 takes lane-1's cell 1 (fw) or its own cell 1;
+            // cell 1 takes its own cell 0 (fw) or lane+1's cell 0
+            const int s0 = fw0 ? srcL : lane, s1 = fw1 ? lane : srcR;
+            float4 fu0, fu1;
+            fu0.x = __shfl_sync(FULL, f1[k].x, s0);
+            fu0.y = __shfl_sync(FULL, f1[k].y, s0);
+            fu0.z = __shfl_sync(FULL, f1[k].z, s0);
+            fu0.w = __shfl_sync(FULL, f1[k].w, s0);
+            fu1.x = __shfl_sync(FULL, f0[k].x, s1);
+            fu1.y = __shfl_sync(FULL, f0[k].y, s1);
+            fu1.z = __shfl_sync(FULL, f0[k].z, s1);
+            fu1.w = __shfl_sync(FULL, f0[k].w, s1);
+            if (EDGE) {
+                fu0 = sel4((atL && fw0) || (atR0 && !fw0), f0[k], fu0);
+                fu1 = sel4(atR1 && !fw1, f1[k], fu1);
+            }
+            const float q0 = xmul(f.sigma, dot3s(s0x[k], s0y[k], s0z[k], f0[k]));
+            const float q1 = xmul(f.sigma, dot3s(s1x[k], s1y[k], s1z[k], f1[k]));
+            f0[k] = transport(f0[k], fu0, fabsf(uh0), q0, ndt);
+            f1[k] = transport(f1[k], fu1, fabsf(uh1), q1, ndt);
+        }
+        // ================= row pass (beta_2, P:L674-683, reading 3)
+        {
+            float4* const XR = XR0 + (n & 1) * C::XR;
+            XR[(wy * 2 + 0) * RW + c0] = f0[0];
+            XR[(wy * 2 + 0) * RW + c0 + 1] = f1[0];
+            XR[(wy * 2 + 1) * RW + c0] = f0[K - 1];
+            XR[(wy * 2 + 1) * RW + c0 + 1] = f1[K - 1];
+            float v0[K], v1[K];
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                const int ib = (r0 + k) * RW + c0;
+                const float2 ex = *reinterpret_cast<const float2*>(Es + 3 * P + ib);
+                const float2 ey = *reinterpret_cast<const float2*>(Es + 4 * P + ib);
+                const float2 ez = *reinterpret_cast<const float2*>(Es + 5 * P + ib);
+                v0[k] = dot3s(ex.x, ey.x, ez.x, f0[k]);
+                v1[k] = dot3s(ex.y, ey.y, ez.y, f1[k]);
+            }
+            __syncthreads();
+            float4 t0 = f0[0], t1 = f1[0], b0 = f0[K - 1], b1 = f1[K - 1];
+            float vt0 = v0[0], vt1 = v1[0], vb0 = v0[K - 1], vb1 = v1[K - 1];
+            if (wy > 0) {
+                t0 = XR[((wy - 1) * 2 + 1) * RW + c0];
+                t1 = XR[((wy - 1) * 2 + 1) * RW + c0 + 1];
+                const int ib = (r0 - 1) * RW + c0;
+                const float2 ex = *reinterpret_cast<const float2*>(Es + 3 * P + ib);
+                const float2 ey = *reinterpret_cast<const float2*>(Es + 4 * P + ib);
+                const float2 ez = *reinterpret_cast<const float2*>(Es + 5 * P + ib);
+                vt0 = dot3s(ex.x, ey.x, ez.x, t0);
+                vt1 = dot3s(ex.y, ey.y, ez.y, t1);
+            }
+            if (wy < NWY - 1) {
+                b0 = XR[((wy + 1) * 2 + 0) * RW + c0];
+                b1 = XR[((wy + 1) * 2 + 0) * RW + c0 + 1];
+                const int ib = (r0 + K) * RW + c0;
+                const float2 ex = *reinterpret_cast<const float2*>(Es + 3 * P + ib);
+                const float2 ey = *reinterpret_cast<const float2*>(Es + 4 * P + ib);
+                const float2 ez = *reinterpret_cast<const float2*>(Es + 5 * P + ib);
+                vb0 = dot3s(ex.x, ey.x, ez.x, b0);
+                vb1 = dot3s(ex.y, ey.y, ez.y, b1);
+            }
+            // new values are written back one row late, so rows k-1, k, k+1 are all pre-pass here
+            float4 n0 = f0[0], n1 = f1[0];
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                float vm0 = (k > 0) ? v0[k - 1] : vt0, vm1 = (k > 0) ? v1[k - 1] : vt1;
+                float vp0 = (k < K - 1) ? v0[k + 1] : vb0, vp1 = (k < K - 1) ? v1[k + 1] : vb1;
+                float4 fm0 = (k > 0) ? f0[k - 1] : t0, fm1 = (k > 0) ? f1[k - 1] : t1;
+                float4 fp0 = (k < K - 1) ? f0[k + 1] : b0, fp1 = (k < K - 1) ? f1[k + 1] : b1;
+                if (EDGE) {
+                    const int r = r0 + k;
+                    if (r <= rmin) {
+                        vm0 = v0[k];
+                        vm1 = v1[k];
+                        fm0 = f0[k];
+                        fm1 = f1[k];
+                    }
+                    if (r >= rmax) {
+                        vp0 = v0[k];
+                        vp1 = v1[k];
+                        fp0 = f0[k];
+                        fp1 = f1[k];
+                    }
+                }
+                float vh0 = dominant(vm0, vp0, RULE);
+                float vh1 = dominant(vm1, vp1, RULE);
+                mx[k] = fmaxf(mx[k], fmaxf(fabsf(vh0), fabsf(atR0 ? vh0 : vh1)));
+                if (CLAMP) {
+                    vh0 = fminf(fmaxf(vh0, -U), U);
+                    vh1 = fminf(fmaxf(vh1, -U), U);
+                }
+                const float4 fu0 = sel4(vh0 > 0.0f, fm0, fp0);
+                const float4 fu1 = sel4(vh1 > 0.0f, fm1, fp1);
+                const float q0 = xmul(f.sigma, dot3s(s0x[k], s0y[k], s0z[k], f0[k]));
+                const float q1 = xmul(f.sigma, dot3s(s1x[k], s1y[k], s1z[k], f1[k]));
+                const float4 m0 = transport(f0[k], fu0, fabsf(vh0), q0, ndt);
+                const float4 m1 = transport(f1[k], fu1, fabsf(vh1), q1, ndt);
+                if (k > 0) {
+                    f0[k - 1] = n0;
+                    f1[k - 1] = n1;
+                }
+                n0 = m0;
+                n1 = m1;
+            }
+            f0[K - 1] = n0;
+            f1[K - 1] = n1;
+        }
+    }
+
+}
+
 template <int K, int NWY, int RULE, bool CLAMP>
 __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const FusedArgs a) {
     using C = Cfg<K, NWY>;
@@ -205,139 +359,14 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const FusedArgs a) {
     }
     cp_async_wait<1>();  // own e cells landed (each thread reads only what it copied until the 1st barrier)
 
-    const bool atL = c0 <= cmin;       // cell 0 at / left of the grid's left edge
-    const bool atR1 = c0 + 1 >= cmax;  // cell 1 at / right of the grid's right edge
-    const bool atR0 = c0 >= cmax;      // odd W: cell 0 is the right edge, cell 1 outside
-    const float ndt = -f.dt, U = f.U;
-    const int srcL = lane - 1, srcR = lane + 1;
-
-    for (int n = 0; n < a.M; ++n) {
-        // ================= column pass (beta_1, P:L663-673): registers + shuffles only
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-            const int ib = (r0 + k) * RW + c0;
-            const float2 ex = *reinterpret_cast<const float2*>(Es + ib);
-            const float2 ey = *reinterpret_cast<const float2*>(Es + P + ib);
-            const float2 ez = *reinterpret_cast<const float2*>(Es + 2 * P + ib);
-            const float u0 = dot3s(ex.x, ey.x, ez.x, f0[k]);
-            const float u1 = dot3s(ex.y, ey.y, ez.y, f1[k]);
-            float uL = __shfl_up_sync(FULL, u1, 1);    // lane-1's cell 1 = left of cell 0
-            float uR = __shfl_down_sync(FULL, u0, 1);  // lane+1's cell 0 = right of cell 1
-            float u1n = u1;                            // right of cell 0
-            if (edgeC) {
-                uL = atL ? u0 : uL;
-                uR = atR1 ? u1 : uR;
-                u1n = atR0 ? u0 : u1;
-            }
-            float uh0 = dominant(uL, u1n, RULE);
-            float uh1 = dominant(u0, uR, RULE);
-            mx[k] = fmaxf(mx[k], fmaxf(fabsf(uh0), fabsf(atR0 ? uh0 : uh1)));
-            if (CLAMP) {
-                uh0 = fminf(fmaxf(uh0, -U), U);
-                uh1 = fminf(fmaxf(uh1, -U), U);
-            }
-            const bool fw0 = uh0 > 0.0f, fw1 = uh1 > 0.0f;
-            // upwind value by per-lane source: cell 0 takes lane-1's cell 1 (fw) or its own cell 1;
-            // cell 1 takes its own cell 0 (fw) or lane+1's cell 0
-            const int s0 = fw0 ? srcL : lane, s1 = fw1 ? lane : srcR;
-            float4 fu0, fu1;
-            fu0.x = __shfl_sync(FULL, f1[k].x, s0);
-            fu0.y = __shfl_sync(FULL, f1[k].y, s0);
-            fu0.z = __shfl_sync(FULL, f1[k].z, s0);
-            fu0.w = __shfl_sync(FULL, f1[k].w, s0);
-            fu1.x = __shfl_sync(FULL, f0[k].x, s1);
-            fu1.y = __shfl_sync(FULL, f0[k].y, s1);
-            fu1.z = __shfl_sync(FULL, f0[k].z, s1);
-            fu1.w = __shfl_sync(FULL, f0[k].w, s1);
-            if (edgeC) {
-                fu0 = sel4((atL && fw0) || (atR0 && !fw0), f0[k], fu0);
-                fu1 = sel4(atR1 && !fw1, f1[k], fu1);
-            }
-            const float q0 = xmul(f.sigma, dot3s(s0x[k], s0y[k], s0z[k], f0[k]));
-            const float q1 = xmul(f.sigma, dot3s(s1x[k], s1y[k], s1z[k], f1[k]));
-            f0[k] = transport(f0[k], fu0, fabsf(uh0), q0, ndt);
-            f1[k] = transport(f1[k], fu1, fabsf(uh1), q1, ndt);
-        }
-        // ================= row pass (beta_2, P:L674-683, reading 3)
-        {
-            float4* const XR = XR0 + (n & 1) * C::XR;
-            XR[(wy * 2 + 0) * RW + c0] = f0[0];
-            XR[(wy * 2 + 0) * RW + c0 + 1] = f1[0];
-            XR[(wy * 2 + 1) * RW + c0] = f0[K - 1];
-            XR[(wy * 2 + 1) * RW + c0 + 1] = f1[K - 1];
-            float v0[K], v1[K];
-#pragma unroll
-            for (int k = 0; k < K; ++k) {
-                const int ib = (r0 + k) * RW + c0;
-                const float2 ex = *reinterpret_cast<const float2*>(Es + 3 * P + ib);
-                const float2 ey = *reinterpret_cast<const float2*>(Es + 4 * P + ib);
-                const float2 ez = *reinterpret_cast<const float2*>(Es + 5 * P + ib);
-                v0[k] = dot3s(ex.x, ey.x, ez.x, f0[k]);
-                v1[k] = dot3s(ex.y, ey.y, ez.y, f1[k]);
-            }
-            __syncthreads();
-            float4 t0 = f0[0], t1 = f1[0], b0 = f0[K - 1], b1 = f1[K - 1];
-            float vt0 = v0[0], vt1 = v1[0], vb0 = v0[K - 1], vb1 = v1[K - 1];
-            if (wy > 0) {
-                t0 = XR[((wy - 1) * 2 + 1) * RW + c0];
-                t1 = XR[((wy - 1) * 2 + 1) * RW + c0 + 1];
-                const int ib = (r0 - 1) * RW + c0;
-                const float2 ex = *reinterpret_cast<const float2*>(Es + 3 * P + ib);
-                const float2 ey = *reinterpret_cast<const float2*>(Es + 4 * P + ib);
-                const float2 ez = *reinterpret_cast<const float2*>(Es + 5 * P + ib);
-                vt0 = dot3s(ex.x, ey.x, ez.x, t0);
-                vt1 = dot3s(ex.y, ey.y, ez.y, t1);
-            }
-            if (wy < NWY - 1) {
-                b0 = XR[((wy + 1) * 2 + 0) * RW + c0];
-                b1 = XR[((wy + 1) * 2 + 0) * RW + c0 + 1];
-                const int ib = (r0 + K) * RW + c0;
-                const float2 ex = *reinterpret_cast<const float2*>(Es + 3 * P + ib);
-                const float2 ey = *reinterpret_cast<const float2*>(Es + 4 * P + ib);
-                const float2 ez = *reinterpret_cast<const float2*>(Es + 5 * P + ib);
-                vb0 = dot3s(ex.x, ey.x, ez.x, b0);
-                vb1 = dot3s(ex.y, ey.y, ez.y, b1);
-            }
-            float4 p0 = t0, p1 = t1;  // pre-pass values of the row above
-#pragma unroll
-            for (int k = 0; k < K; ++k) {
-                float vm0 = (k > 0) ? v0[k - 1] : vt0, vm1 = (k > 0) ? v1[k - 1] : vt1;
-                float vp0 = (k < K - 1) ? v0[k + 1] : vb0, vp1 = (k < K - 1) ? v1[k + 1] : vb1;
-                float4 fm0 = p0, fm1 = p1;
-                float4 fp0 = (k < K - 1) ? f0[k + 1] : b0, fp1 = (k < K - 1) ? f1[k + 1] : b1;
-                if (edgeR) {
-                    const int r = r0 + k;
-                    if (r <= rmin) {
-                        vm0 = v0[k];
-                        vm1 = v1[k];
-                        fm0 = f0[k];
-                        fm1 = f1[k];
-                    }
-                    if (r >= rmax) {
-                        vp0 = v0[k];
-                        vp1 = v1[k];
-                        fp0 = f0[k];
-                        fp1 = f1[k];
-                    }
-                }
-                float vh0 = dominant(vm0, vp0, RULE);
-                float vh1 = dominant(vm1, vp1, RULE);
-                mx[k] = fmaxf(mx[k], fmaxf(fabsf(vh0), fabsf(atR0 ? vh0 : vh1)));
-                if (CLAMP) {
-                    vh0 = fminf(fmaxf(vh0, -U), U);
-                    vh1 = fminf(fmaxf(vh1, -U), U);
-                }
-                const float4 fu0 = sel4(vh0 > 0.0f, fm0, fp0);
-                const float4 fu1 = sel4(vh1 > 0.0f, fm1, fp1);
-                p0 = f0[k];
-                p1 = f1[k];
-                const float q0 = xmul(f.sigma, dot3s(s0x[k], s0y[k], s0z[k], f0[k]));
-                const float q1 = xmul(f.sigma, dot3s(s1x[k], s1y[k], s1z[k], f1[k]));
-                f0[k] = transport(f0[k], fu0, fabsf(vh0), q0, ndt);
-                f1[k] = transport(f1[k], fu1, fabsf(vh1), q1, ndt);
-            }
-        }
-    }
+    if (edgeC || edgeR)
+        transport_passes<K, NWY, RULE, CLAMP, true>(f, a.M, f0, f1, s0x, s0y, s0z, s1x, s1y, s1z, mx, Es, XR0, lane,
+                                                    wy, cmin, cmax, rmin, rmax);
+    else
+        transport_passes<K, NWY, RULE, CLAMP, false>(f, a.M, f0, f1, s0x, s0y, s0z, s1x, s1y, s1z, mx, Es, XR0, lane,
+                                                     wy, cmin, cmax, rmin, rmax);
+    const bool atR0 = c0 >= cmax;
+    const float U = f.U;
 
     // ---------------- flags from tile cells (exact at every pass); |u_hat| before the clamp
     unsigned fl = 0;
