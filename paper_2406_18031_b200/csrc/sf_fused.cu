@@ -121,21 +121,30 @@ struct Cfg {
 };
 
 // The transport: M substeps of a column pass then a row pass on the thread's
-// 2 x K cells.  EDGE: the CTA's region touches the grid border (replicate clamp, reading 10).
-template <int K, int NWY, int RULE, bool CLAMP, bool EDGE>
+// 2 x K cells.  Grid borders (replicate clamp, reading 10) are handled by REPLICA cells: the
+// out-of-grid cell next to a grid edge is kept equal to the edge cell (loaded that way, and
+// refreshed after each pass that changed the edge), so the neighbour read of the edge cell
+// returns its own value and the pass bodies carry no boundary logic.  A grid edge on the
+// region border itself needs no replica: it lies R cells from the tile, outside the tile's
+// dependency cone, like any cut edge.
+template <int K, int NWY, int RULE, bool CLAMP>
 __device__ __forceinline__ void transport_passes(const FrameParams& f, int M, float4 (&f0)[K], float4 (&f1)[K],
                                                  const float (&s0x)[K], const float (&s0y)[K], const float (&s0z)[K],
                                                  const float (&s1x)[K], const float (&s1y)[K], const float (&s1z)[K],
                                                  float (&mx)[K], const float* Es, float4* XR0, int lane, int wy,
                                                  int cmin, int cmax, int rmin, int rmax) {
     using C = Cfg<K, NWY>;
-    constexpr int RW = C::RW, P = C::P;
+    constexpr int RW = C::RW, RH = C::RH, P = C::P;
     const int c0 = 2 * lane, r0 = K * wy;
-    const bool atL = c0 <= cmin;       // cell 0 at / left of the grid's left edge
-    const bool atR1 = c0 + 1 >= cmax;  // cell 1 at / right of the grid's right edge
-    const bool atR0 = c0 >= cmax;      // odd W: cell 0 is the right edge, cell 1 outside
     const float ndt = -f.dt, U = f.U;
     const int srcL = lane - 1, srcR = lane + 1;
+    // replica bookkeeping (block-uniform except for the lane / k tests)
+    const bool repL = cmin > 0, repR = cmax < RW - 1, repT = rmin > 0, repB = rmax < RH - 1;
+    const int laneL = cmin / 2 - 1;                            // owns replica column cmin-1 as its cell 1
+    const int laneR = (cmax & 1) ? (cmax + 1) / 2 : cmax / 2;  // owns replica column cmax+1
+    const bool rOdd = (cmax & 1) != 0;                         // replica is cell 0 of laneR (else its cell 1)
+    const bool in1 = c0 + 1 <= cmax;                           // cell 1 inside the grid (for the flag max)
+    const int keT = rmin - r0, keB = rmax - r0;                // edge rows in this thread's run
 
     for (int n = 0; n < M; ++n) {
         // ================= column pass (beta_1): registers + shuffles only
@@ -147,25 +156,18 @@ __device__ __forceinline__ void transport_passes(const FrameParams& f, int M, fl
             const float2 ez = *reinterpret_cast<const float2*>(Es + 2 * P + ib);
             const float u0 = dot3s(ex.x, ey.x, ez.x, f0[k]);
             const float u1 = dot3s(ex.y, ey.y, ez.y, f1[k]);
-            float uL = __shfl_up_sync(FULL, u1, 1);    // lane-1's cell 1 = left of cell 0
-            float uR = __shfl_down_sync(FULL, u0, 1);  // lane+1's cell 0 = right of cell 1
-            float u1n = u1;                            // right of cell 0
-            if (EDGE) {
-                uL = atL ? u0 : uL;
-                uR = atR1 ? u1 : uR;
-                u1n = atR0 ? u0 : u1;
-            }
-            float uh0 = dominant(uL, u1n, RULE);
+            const float uL = __shfl_up_sync(FULL, u1, 1);    // lane-1's cell 1 = left of cell 0
+            const float uR = __shfl_down_sync(FULL, u0, 1);  // lane+1's cell 0 = right of cell 1
+            float uh0 = dominant(uL, u1, RULE);
             float uh1 = dominant(u0, uR, RULE);
-            mx[k] = fmaxf(mx[k], fmaxf(fabsf(uh0), fabsf(atR0 ? uh0 : uh1)));
+            mx[k] = fmaxf(mx[k], fmaxf(fabsf(uh0), in1 ? fabsf(uh1) : 0.0f));
             if (CLAMP) {
                 uh0 = fminf(fmaxf(uh0, -U), U);
                 uh1 = fminf(fmaxf(uh1, -U), U);
             }
-            const bool fw0 = uh0 > 0.0f, fw1 = uh1 > 0.0f;
-            // upwind value by per-lane source: cell 0 takes lane-1's cell 1 (fw) or its own cell 1;
-            // cell 1 takes its own cell 0 (fw) or lane+1's cell 0
-            const int s0 = fw0 ? srcL : lane, s1 = fw1 ? lane : srcR;
+            // upwind value by per-lane source: cell 0 takes lane-1's cell 1 (u_hat > 0) or its own
+            // cell 1; cell 1 takes its own cell 0 (u_hat > 0) or lane+1's cell 0
+            const int s0 = uh0 > 0.0f ? srcL : lane, s1 = uh1 > 0.0f ? lane : srcR;
             float4 fu0, fu1;
             fu0.x = __shfl_sync(FULL, f1[k].x, s0);
             fu0.y = __shfl_sync(FULL, f1[k].y, s0);
@@ -175,14 +177,48 @@ __device__ __forceinline__ void transport_passes(const FrameParams& f, int M, fl
             fu1.y = __shfl_sync(FULL, f0[k].y, s1);
             fu1.z = __shfl_sync(FULL, f0[k].z, s1);
             fu1.w = __shfl_sync(FULL, f0[k].w, s1);
-            if (EDGE) {
-                fu0 = sel4((atL && fw0) || (atR0 && !fw0), f0[k], fu0);
-                fu1 = sel4(atR1 && !fw1, f1[k], fu1);
-            }
             const float q0 = xmul(f.sigma, dot3s(s0x[k], s0y[k], s0z[k], f0[k]));
             const float q1 = xmul(f.sigma, dot3s(s1x[k], s1y[k], s1z[k], f1[k]));
             f0[k] = transport(f0[k], fu0, fabsf(uh0), q0, ndt);
             f1[k] = transport(f1[k], fu1, fabsf(uh1), q1, ndt);
+        }
+        // column replicas <- their edge cells
+        if (repL) {
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                const float4 e = shfl_dn4(f0[k]);
+                if (lane == laneL) f1[k] = e;
+            }
+        }
+        if (repR) {
+            if (rOdd) {
+#pragma unroll
+                for (int k = 0; k < K; ++k) {
+                    const float4 e = shfl_up4(f1[k]);
+                    if (lane == laneR) f0[k] = e;
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < K; ++k)
+                    if (lane == laneR) f1[k] = f0[k];
+            }
+        }
+        // row replicas inside this thread's run <- their edge rows (before the row pass reads)
+        if (repT && keT >= 1 && keT <= K - 1) {
+#pragma unroll
+            for (int k = 0; k < K - 1; ++k) {
+                const bool p = (keT - 1 - k) == 0;
+                f0[k] = sel4(p, f0[k + 1], f0[k]);
+                f1[k] = sel4(p, f1[k + 1], f1[k]);
+            }
+        }
+        if (repB && keB >= 0 && keB <= K - 2) {
+#pragma unroll
+            for (int k = K - 1; k >= 1; --k) {
+                const bool p = (keB + 1 - k) == 0;
+                f0[k] = sel4(p, f0[k - 1], f0[k]);
+                f1[k] = sel4(p, f1[k - 1], f1[k]);
+            }
         }
         // ================= row pass (beta_2, reading 3)
         {
@@ -204,7 +240,8 @@ __device__ __forceinline__ void transport_passes(const FrameParams& f, int M, fl
             __syncthreads();
             float4 t0 = f0[0], t1 = f1[0], b0 = f0[K - 1], b1 = f1[K - 1];
             float vt0 = v0[0], vt1 = v1[0], vb0 = v0[K - 1], vb1 = v1[K - 1];
-            if (wy > 0) {
+            // neighbour run ends; at an edge row on a run boundary the replica is the row itself
+            if (wy > 0 && !(repT && keT == 0)) {
                 t0 = XR[((wy - 1) * 2 + 1) * RW + c0];
                 t1 = XR[((wy - 1) * 2 + 1) * RW + c0 + 1];
                 const int ib = (r0 - 1) * RW + c0;
@@ -214,7 +251,7 @@ __device__ __forceinline__ void transport_passes(const FrameParams& f, int M, fl
                 vt0 = dot3s(ex.x, ey.x, ez.x, t0);
                 vt1 = dot3s(ex.y, ey.y, ez.y, t1);
             }
-            if (wy < NWY - 1) {
+            if (wy < NWY - 1 && !(repB && keB == K - 1)) {
                 b0 = XR[((wy + 1) * 2 + 0) * RW + c0];
                 b1 = XR[((wy + 1) * 2 + 0) * RW + c0 + 1];
                 const int ib = (r0 + K) * RW + c0;
@@ -228,28 +265,13 @@ __device__ __forceinline__ void transport_passes(const FrameParams& f, int M, fl
             float4 n0 = f0[0], n1 = f1[0];
 #pragma unroll
             for (int k = 0; k < K; ++k) {
-                float vm0 = (k > 0) ? v0[k - 1] : vt0, vm1 = (k > 0) ? v1[k - 1] : vt1;
-                float vp0 = (k < K - 1) ? v0[k + 1] : vb0, vp1 = (k < K - 1) ? v1[k + 1] : vb1;
-                float4 fm0 = (k > 0) ? f0[k - 1] : t0, fm1 = (k > 0) ? f1[k - 1] : t1;
-                float4 fp0 = (k < K - 1) ? f0[k + 1] : b0, fp1 = (k < K - 1) ? f1[k + 1] : b1;
-                if (EDGE) {
-                    const int r = r0 + k;
-                    if (r <= rmin) {
-                        vm0 = v0[k];
-                        vm1 = v1[k];
-                        fm0 = f0[k];
-                        fm1 = f1[k];
-                    }
-                    if (r >= rmax) {
-                        vp0 = v0[k];
-                        vp1 = v1[k];
-                        fp0 = f0[k];
-                        fp1 = f1[k];
-                    }
-                }
+                const float vm0 = (k > 0) ? v0[k - 1] : vt0, vm1 = (k > 0) ? v1[k - 1] : vt1;
+                const float vp0 = (k < K - 1) ? v0[k + 1] : vb0, vp1 = (k < K - 1) ? v1[k + 1] : vb1;
+                const float4 fm0 = (k > 0) ? f0[k - 1] : t0, fm1 = (k > 0) ? f1[k - 1] : t1;
+                const float4 fp0 = (k < K - 1) ? f0[k + 1] : b0, fp1 = (k < K - 1) ? f1[k + 1] : b1;
                 float vh0 = dominant(vm0, vp0, RULE);
                 float vh1 = dominant(vm1, vp1, RULE);
-                mx[k] = fmaxf(mx[k], fmaxf(fabsf(vh0), fabsf(atR0 ? vh0 : vh1)));
+                mx[k] = fmaxf(mx[k], fmaxf(fabsf(vh0), in1 ? fabsf(vh1) : 0.0f));
                 if (CLAMP) {
                     vh0 = fminf(fmaxf(vh0, -U), U);
                     vh1 = fminf(fmaxf(vh1, -U), U);
@@ -270,8 +292,9 @@ __device__ __forceinline__ void transport_passes(const FrameParams& f, int M, fl
             f0[K - 1] = n0;
             f1[K - 1] = n1;
         }
+        // (row passes keep column replicas valid; the next column pass keeps row replicas as
+        //  they are and they are refreshed again before the next row pass)
     }
-
 }
 
 template <int K, int NWY, int RULE, bool CLAMP>
@@ -359,13 +382,8 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const FusedArgs a) {
     }
     cp_async_wait<1>();  // own e cells landed (each thread reads only what it copied until the 1st barrier)
 
-    if (edgeC || edgeR)
-        transport_passes<K, NWY, RULE, CLAMP, true>(f, a.M, f0, f1, s0x, s0y, s0z, s1x, s1y, s1z, mx, Es, XR0, lane,
-                                                    wy, cmin, cmax, rmin, rmax);
-    else
-        transport_passes<K, NWY, RULE, CLAMP, false>(f, a.M, f0, f1, s0x, s0y, s0z, s1x, s1y, s1z, mx, Es, XR0, lane,
-                                                     wy, cmin, cmax, rmin, rmax);
-    const bool atR0 = c0 >= cmax;
+    transport_passes<K, NWY, RULE, CLAMP>(f, a.M, f0, f1, s0x, s0y, s0z, s1x, s1y, s1z, mx, Es, XR0, lane, wy, cmin,
+                                          cmax, rmin, rmax);
     const float U = f.U;
 
     // ---------------- flags from tile cells (exact at every pass); |u_hat| before the clamp
@@ -420,10 +438,11 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const FusedArgs a) {
         const int rlo = max(R - 2 * S, rmin), rhi = min(R + TH + 2 * S - 1, rmax);
         const int clo = max(R - 2 * S, cmin), chi = min(R + TW + 2 * S - 1, cmax);
         {
-            const int mr0 = rlo - 2, mc0 = clo - 1, mnc = (chi + 1) - mc0 + 1, mn = ((rhi + 2) - mr0 + 1) * mnc;
+            // rhohat plane + horizontal brightness taps on the solve region +-2 rows, +-1 cols
 #pragma unroll 1
-            for (int t = tid; t < mn; t += NT) {  // rhohat plane + horizontal brightness taps
-                const int r = mr0 + t / mnc, c = mc0 + t % mnc;
+            for (int r = rlo - 2 + wy; r <= rhi + 2; r += NWY)
+#pragma unroll 1
+            for (int c = clo - 1 + lane; c <= chi + 1; c += 32) {
                 const int idx = r * RW + c;
                 const float d = Ds[idx];
                 Ds[idx] = depth_valid(d, f.is_inv) ? rho_hat(d, f.is_inv) : qnan;
@@ -436,10 +455,10 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const FusedArgs a) {
             }
         }
         __syncthreads();
-        const int nc = chi - clo + 1, ncell = (rhi - rlo + 1) * nc;
 #pragma unroll 1
-        for (int t = tid; t < ncell; t += NT) {  // per-pixel LS (eq:LS_update) + fusion, solve region
-            const int r = rlo + t / nc, c = clo + t % nc;
+        for (int r = rlo + wy; r <= rhi; r += NWY)  // per-pixel LS (eq:LS_update) + fusion, solve region
+#pragma unroll 1
+        for (int c = clo + lane; c <= chi; c += 32) {
             const int idx = r * RW + c;
             const float g0 = HG[idx - 2 * RW], g1 = HG[idx - RW], g2 = HG[idx], g3 = HG[idx + RW], g4 = HG[idx + 2 * RW];
             const float h0 = HH[idx - 2 * RW], h1 = HH[idx - RW], h2 = HH[idx], h3 = HH[idx + RW], h4 = HH[idx + 2 * RW];
@@ -490,12 +509,11 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const FusedArgs a) {
             const int or0 = max(R - m, rmin), or1 = min(R + TH + m - 1, rmax);
             const int oc0 = max(R - m, cmin), oc1 = min(R + TW + m - 1, cmax);
             const int hr0 = max(or0 - 2, rmin), hr1 = min(or1 + 2, rmax);
-            const int onc = oc1 - oc0 + 1;
             __syncthreads();
-            const int hn = (hr1 - hr0 + 1) * onc;
 #pragma unroll 1
-            for (int t = tid; t < hn; t += NT) {
-                const int r = hr0 + t / onc, c = oc0 + t % onc;
+            for (int r = hr0 + wy; r <= hr1; r += NWY)
+#pragma unroll 1
+            for (int c = oc0 + lane; c <= oc1; c += 32) {
                 const int idx = r * RW + c;
                 int j0 = idx - 2, j1 = idx - 1, j3 = idx + 1, j4 = idx + 2;
                 if (edge) {
@@ -510,10 +528,10 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const FusedArgs a) {
                 Tz[idx] = xadd(xadd(xadd(xadd(Fz[j0], Fz[j1]), Fz[idx]), Fz[j3]), Fz[j4]);
             }
             __syncthreads();
-            const int on = (or1 - or0 + 1) * onc;
 #pragma unroll 1
-            for (int t = tid; t < on; t += NT) {
-                const int r = or0 + t / onc, c = oc0 + t % onc;
+            for (int r = or0 + wy; r <= or1; r += NWY)
+#pragma unroll 1
+            for (int c = oc0 + lane; c <= oc1; c += 32) {
                 const int idx = r * RW + c;
                 int i0 = idx - 2 * RW, i1 = idx - RW, i3 = idx + RW, i4 = idx + 2 * RW;
                 if (edge) {
@@ -531,10 +549,10 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const FusedArgs a) {
         // ---- store the tile: (w^{k+1}, rho^{k+1}), coalesced along rows
         const int tr0 = max(R, rmin), tr1 = min(R + TH - 1, rmax);
         const int tc0 = max(R, cmin), tc1 = min(R + TW - 1, cmax);
-        const int tnc = tc1 - tc0 + 1, tn = (tr1 - tr0 + 1) * tnc;
 #pragma unroll 1
-        for (int t = tid; t < tn; t += NT) {
-            const int r = tr0 + t / tnc, c = tc0 + t % tnc;
+        for (int r = tr0 + wy; r <= tr1; r += NWY)
+#pragma unroll 1
+        for (int c = tc0 + lane; c <= tc1; c += 32) {
             const int idx = r * RW + c;
             a.fout[plane + (size_t)(gi0 + r) * f.W + (gj0 + c)] = make_float4(Fx[idx], Fy[idx], Fz[idx], Fw[idx]);
         }
