@@ -20,6 +20,8 @@
 //     while the transport runs; the update computes the brightness / inverse-depth models,
 //     the 3x3 LDL^T solve and S box passes on shared planes, then fuses rho and stores.
 // The transport update of the 4 fields uses paired f32x2 ops (FADD2/FMUL2/FFMA2).
+#include <stdlib.h>
+
 #include "sf_internal.cuh"
 
 namespace {
@@ -89,6 +91,14 @@ __device__ __forceinline__ void cp_async16(float* sdst, const float* gsrc) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+
+// Iterate the cells of the rectangle [r0, r1] x [c0, c1] with NT threads, row-major, full lane
+// utilisation and no per-iteration integer division.
+#define SF_FOR_RECT(r, c, R0, R1, C0, C1, NT, tid)                                                  \
+    for (int nc_ = (C1) - (C0) + 1, dr_ = (NT) / nc_, dc_ = (NT) % nc_, r = (R0) + (tid) / nc_,   \
+             c = (C0) + (tid) % nc_;                                                             \
+         nc_ > 0 && r <= (R1); r += dr_ + ((c + dc_ > (C1)) ? 1 : 0), c = (c + dc_ > (C1)) ? c + dc_ - nc_ : c + dc_)
 
 struct FusedArgs {
     const float4* fin;  // fields at launch start (state k or a partial prediction)
@@ -440,9 +450,7 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const FusedArgs a) {
         {
             // rhohat plane + horizontal brightness taps on the solve region +-2 rows, +-1 cols
 #pragma unroll 1
-            for (int r = rlo - 2 + wy; r <= rhi + 2; r += NWY)
-#pragma unroll 1
-            for (int c = clo - 1 + lane; c <= chi + 1; c += 32) {
+            SF_FOR_RECT(r, c, rlo - 2, rhi + 2, clo - 1, chi + 1, NT, tid) {
                 const int idx = r * RW + c;
                 const float d = Ds[idx];
                 Ds[idx] = depth_valid(d, f.is_inv) ? rho_hat(d, f.is_inv) : qnan;
@@ -455,10 +463,8 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const FusedArgs a) {
             }
         }
         __syncthreads();
-#pragma unroll 1
-        for (int r = rlo + wy; r <= rhi; r += NWY)  // per-pixel LS (eq:LS_update) + fusion, solve region
-#pragma unroll 1
-        for (int c = clo + lane; c <= chi; c += 32) {
+#pragma unroll 2
+        SF_FOR_RECT(r, c, rlo, rhi, clo, chi, NT, tid) {  // per-pixel LS (eq:LS_update) + fusion, solve region
             const int idx = r * RW + c;
             const float g0 = HG[idx - 2 * RW], g1 = HG[idx - RW], g2 = HG[idx], g3 = HG[idx + RW], g4 = HG[idx + 2 * RW];
             const float h0 = HH[idx - 2 * RW], h1 = HH[idx - RW], h2 = HH[idx], h3 = HH[idx + RW], h4 = HH[idx + 2 * RW];
@@ -511,9 +517,7 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const FusedArgs a) {
             const int hr0 = max(or0 - 2, rmin), hr1 = min(or1 + 2, rmax);
             __syncthreads();
 #pragma unroll 1
-            for (int r = hr0 + wy; r <= hr1; r += NWY)
-#pragma unroll 1
-            for (int c = oc0 + lane; c <= oc1; c += 32) {
+            SF_FOR_RECT(r, c, hr0, hr1, oc0, oc1, NT, tid) {
                 const int idx = r * RW + c;
                 int j0 = idx - 2, j1 = idx - 1, j3 = idx + 1, j4 = idx + 2;
                 if (edge) {
@@ -529,9 +533,7 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const FusedArgs a) {
             }
             __syncthreads();
 #pragma unroll 1
-            for (int r = or0 + wy; r <= or1; r += NWY)
-#pragma unroll 1
-            for (int c = oc0 + lane; c <= oc1; c += 32) {
+            SF_FOR_RECT(r, c, or0, or1, oc0, oc1, NT, tid) {
                 const int idx = r * RW + c;
                 int i0 = idx - 2 * RW, i1 = idx - RW, i3 = idx + RW, i4 = idx + 2 * RW;
                 if (edge) {
@@ -550,9 +552,7 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const FusedArgs a) {
         const int tr0 = max(R, rmin), tr1 = min(R + TH - 1, rmax);
         const int tc0 = max(R, cmin), tc1 = min(R + TW - 1, cmax);
 #pragma unroll 1
-        for (int r = tr0 + wy; r <= tr1; r += NWY)
-#pragma unroll 1
-        for (int c = tc0 + lane; c <= tc1; c += 32) {
+        SF_FOR_RECT(r, c, tr0, tr1, tc0, tc1, NT, tid) {
             const int idx = r * RW + c;
             a.fout[plane + (size_t)(gi0 + r) * f.W + (gj0 + c)] = make_float4(Fx[idx], Fy[idx], Fz[idx], Fw[idx]);
         }
@@ -562,8 +562,6 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const FusedArgs a) {
 }
 
 // The configuration used today: RW = 64, RH = 72 (K = 6 rows x 12 warps), 384 threads, 1 CTA / SM.
-constexpr int FK = 6, FNWY = 12;
-using FC = Cfg<FK, FNWY>;
 constexpr int MMAX = 8;  // substeps per launch
 
 struct Plan {
@@ -584,27 +582,34 @@ Plan make_plan(const FrameParams& f) {
     return p;
 }
 
-}  // namespace
+// Region shapes (both RW = 64 x RH = 72, one CTA per SM):
+//   cfg 0: K = 6 rows x 12 warps (384 threads, ~168 registers)
+//   cfg 1: K = 4 rows x 18 warps (576 threads, <= 112 registers)
+int fused_cfg() {
+    static int cfg = -1;
+    if (cfg < 0) {
+        const char* e = getenv("SF_FUSED_CFG");
+        cfg = (e && e[0] == '1') ? 1 : 0;
+    }
+    return cfg;
+}
 
-bool sf_fused_supported(const sf_ctx* c) {
-    const Plan p = make_plan(c->fp);
-    if (p.launches > 8) return false;
-    for (int l = 0; l < p.launches; ++l)
-        if (FC::RW - 2 * p.R[l] < 8 || FC::RH - 2 * p.R[l] < 8) return false;
-    // opt in to the large dynamic shared-memory carve-out (one CTA per SM)
-    const void* fns[] = {(const void*)k_fused<FK, FNWY, SF_DOM_LARGEST, true>,
-                         (const void*)k_fused<FK, FNWY, SF_DOM_LARGEST, false>,
-                         (const void*)k_fused<FK, FNWY, SF_DOM_PRINTED, true>,
-                         (const void*)k_fused<FK, FNWY, SF_DOM_PRINTED, false>};
+template <int K, int NWY>
+bool prepare_cfg() {
+    using FC = Cfg<K, NWY>;
+    const void* fns[] = {(const void*)k_fused<K, NWY, SF_DOM_LARGEST, true>,
+                         (const void*)k_fused<K, NWY, SF_DOM_LARGEST, false>,
+                         (const void*)k_fused<K, NWY, SF_DOM_PRINTED, true>,
+                         (const void*)k_fused<K, NWY, SF_DOM_PRINTED, false>};
     for (const void* fn : fns)
         if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FC::SMEM) != cudaSuccess)
             return false;
     return true;
 }
 
-int sf_fused_launches(const sf_ctx* c) { return make_plan(c->fp).launches; }
-
-cudaError_t sf_launch_fused_step(sf_ctx* c, const float* Y, const float* D) {
+template <int K, int NWY>
+cudaError_t launch_cfg(sf_ctx* c, const float* Y, const float* D) {
+    using FC = Cfg<K, NWY>;
     const FrameParams& f = c->fp;
     const Plan p = make_plan(f);
     const float4* src = c->state[c->cur];
@@ -633,18 +638,35 @@ cudaError_t sf_launch_fused_step(sf_ctx* c, const float* Y, const float* D) {
         const dim3 grid((f.W + a.TW - 1) / a.TW, (f.H + a.TH - 1) / a.TH, f.B);
         if (f.rule == SF_DOM_PRINTED) {
             if (f.clamp)
-                k_fused<FK, FNWY, SF_DOM_PRINTED, true><<<grid, FC::NT, FC::SMEM, c->stream>>>(a);
+                k_fused<K, NWY, SF_DOM_PRINTED, true><<<grid, FC::NT, FC::SMEM, c->stream>>>(a);
             else
-                k_fused<FK, FNWY, SF_DOM_PRINTED, false><<<grid, FC::NT, FC::SMEM, c->stream>>>(a);
+                k_fused<K, NWY, SF_DOM_PRINTED, false><<<grid, FC::NT, FC::SMEM, c->stream>>>(a);
         } else {
             if (f.clamp)
-                k_fused<FK, FNWY, SF_DOM_LARGEST, true><<<grid, FC::NT, FC::SMEM, c->stream>>>(a);
+                k_fused<K, NWY, SF_DOM_LARGEST, true><<<grid, FC::NT, FC::SMEM, c->stream>>>(a);
             else
-                k_fused<FK, FNWY, SF_DOM_LARGEST, false><<<grid, FC::NT, FC::SMEM, c->stream>>>(a);
+                k_fused<K, NWY, SF_DOM_LARGEST, false><<<grid, FC::NT, FC::SMEM, c->stream>>>(a);
         }
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
         src = a.fout;
     }
     return cudaSuccess;
+}
+
+}  // namespace
+
+bool sf_fused_supported(const sf_ctx* c) {
+    const Plan p = make_plan(c->fp);
+    if (p.launches > 8) return false;
+    for (int l = 0; l < p.launches; ++l)
+        if (64 - 2 * p.R[l] < 8 || 72 - 2 * p.R[l] < 8) return false;
+    // opt in to the large dynamic shared-memory carve-out (one CTA per SM)
+    return fused_cfg() == 1 ? prepare_cfg<4, 18>() : prepare_cfg<6, 12>();
+}
+
+int sf_fused_launches(const sf_ctx* c) { return make_plan(c->fp).launches; }
+
+cudaError_t sf_launch_fused_step(sf_ctx* c, const float* Y, const float* D) {
+    return fused_cfg() == 1 ? launch_cfg<4, 18>(c, Y, D) : launch_cfg<6, 12>(c, Y, D);
 }
