@@ -16,10 +16,12 @@
 //   * cut region edges produce inexact ("garbage") cells that never reach the tile: the
 //     halo R covers the dependency radius (M per axis for the transport, 2S + 2 for the
 //     update); flags are taken only from tile cells, which are exact at every pass;
-//   * Y and depth for the update are prefetched with cp.async at kernel start and land
+//   * e planes, Y and depth are staged by TMA bulk tensor copies issued at kernel start (Y and
+//     depth land while the transport runs; cp.async fallback when W % 4 != 0), and
 //     while the transport runs; the update computes the brightness / inverse-depth models,
 //     the 3x3 LDL^T solve and S box passes on shared planes, then fuses rho and stores.
 // The transport update of the 4 fields uses paired f32x2 ops (FADD2/FMUL2/FFMA2).
+#include <cuda.h>
 #include <stdlib.h>
 
 #include "sf_internal.cuh"
@@ -92,6 +94,32 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
+// ---- mbarrier + TMA (cp.async.bulk.tensor) helpers
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int x, int y, int z, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n" ::
+            "r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+        : "memory");
+}
+
 
 // Iterate the cells of the rectangle [r0, r1] x [c0, c1] with NT threads, row-major, full lane
 // utilisation and no per-iteration integer division.
@@ -101,6 +129,10 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
          nc_ > 0 && r <= (R1); r += dr_ + ((c + dc_ > (C1)) ? 1 : 0), c = (c + dc_ > (C1)) ? c + dc_ - nc_ : c + dc_)
 
 struct FusedArgs {
+    CUtensorMap tmE;    // [6][H][W] e planes, box 64 x 72 x 3   (valid when tma)
+    CUtensorMap tmY;    // [B][H][W] brightness, box 64 x 72 x 1
+    CUtensorMap tmD;    // [B][H][W] depth, box 64 x 72 x 1
+    int tma;            // 1: stage e / Y / depth with TMA (needs W % 4 == 0, 16-byte aligned bases)
     const float4* fin;  // fields at launch start (state k or a partial prediction)
     const float4* sk;   // state k (rho^k for the update)
     float4* fout;       // state k+1 (upd) or partial prediction
@@ -308,7 +340,7 @@ __device__ __forceinline__ void transport_passes(const FrameParams& f, int M, fl
 }
 
 template <int K, int NWY, int RULE, bool CLAMP>
-__global__ void __launch_bounds__(32 * NWY, 1) k_fused(const FusedArgs a) {
+__global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ FusedArgs a) {
     using C = Cfg<K, NWY>;
     constexpr int RW = C::RW, RH = C::RH, P = C::P, NT = C::NT;
     extern __shared__ float4 smem4[];
@@ -331,8 +363,30 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const FusedArgs a) {
     const bool edgeR = rmin > 0 || rmax < RH - 1;
     const size_t HW = (size_t)f.H * f.W, plane = (size_t)b * HW;
 
-    // ---------------- prefetch (cp.async): own e1/e2 cells (group 0), Y and depth (group 1)
-    {
+    // ---------------- staging: e1 / e2 planes (transport), Y and depth (update)
+    __shared__ __align__(8) uint64_t bars[3];
+    if (a.tma) {
+        // TMA: one thread issues three bulk tensor copies of the whole region (out-of-range cells
+        // arrive as zeros; the replica cells next to grid edges are fixed up below)
+        if (tid == 0) {
+            mbar_init(&bars[0], 1);
+            mbar_init(&bars[1], 1);
+            mbar_init(&bars[2], 1);
+            asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        }
+        __syncthreads();
+        if (tid == 0) {
+            mbar_expect_tx(&bars[0], 3u * P * 4u);
+            tma_load_3d(Es, &a.tmE, gj0, gi0, 0, &bars[0]);
+            mbar_expect_tx(&bars[1], 3u * P * 4u);
+            tma_load_3d(Es + 3 * P, &a.tmE, gj0, gi0, 3, &bars[1]);
+            if (a.upd) {
+                mbar_expect_tx(&bars[2], 2u * P * 4u);
+                tma_load_3d(Ys, &a.tmY, gj0, gi0, b, &bars[2]);
+                tma_load_3d(Ds, &a.tmD, gj0, gi0, b, &bars[2]);
+            }
+        }
+    } else {
         const bool pair = !edgeC && (f.W & 1) == 0;  // both cells contiguous and 8-byte aligned
 #pragma unroll
         for (int k = 0; k < K; ++k) {
@@ -390,7 +444,29 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const FusedArgs a) {
         s1z[k] = sb.z;
         mx[k] = 0.0f;
     }
-    cp_async_wait<1>();  // own e cells landed (each thread reads only what it copied until the 1st barrier)
+    if (a.tma) {
+        mbar_wait(&bars[0], 0);
+        mbar_wait(&bars[1], 0);
+        if (edgeC || edgeR) {  // replica cells next to grid edges take the edge cell's e (reading 10)
+            __syncthreads();
+            if (cmin > 0 || cmax < RW - 1)
+                for (int t = tid; t < 6 * RH; t += NT) {
+                    float* row = Es + (t / RH) * P + (t % RH) * RW;
+                    if (cmin > 0) row[cmin - 1] = row[cmin];
+                    if (cmax < RW - 1) row[cmax + 1] = row[cmax];
+                }
+            __syncthreads();
+            if (rmin > 0 || rmax < RH - 1)
+                for (int t = tid; t < 6 * RW; t += NT) {
+                    float* col = Es + (t / RW) * P + (t % RW);
+                    if (rmin > 0) col[(rmin - 1) * RW] = col[rmin * RW];
+                    if (rmax < RH - 1) col[(rmax + 1) * RW] = col[rmax * RW];
+                }
+            __syncthreads();
+        }
+    } else {
+        cp_async_wait<1>();  // own e cells landed (each thread reads only what it copied until the 1st barrier)
+    }
 
     transport_passes<K, NWY, RULE, CLAMP>(f, a.M, f0, f1, s0x, s0y, s0z, s1x, s1y, s1z, mx, Es, XR0, lane, wy, cmin,
                                           cmax, rmin, rmax);
@@ -440,7 +516,22 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const FusedArgs a) {
             *reinterpret_cast<float2*>(Fz + ib) = make_float2(f0[k].z, f1[k].z);
             *reinterpret_cast<float2*>(Fw + ib) = make_float2(f0[k].w, f1[k].w);
         }
-        cp_async_wait<0>();
+        if (a.tma) {
+            mbar_wait(&bars[2], 0);
+            if (edgeC || edgeR) {  // out-of-grid cells of Y / depth take their clamped cell's value
+                __syncthreads();
+                for (int t = tid; t < P; t += NT) {
+                    const int r = t / RW, c = t % RW;
+                    const int rc = iclamp(r, rmin, rmax), cc = iclamp(c, cmin, cmax);
+                    if (rc != r || cc != c) {
+                        Ys[t] = Ys[rc * RW + cc];
+                        Ds[t] = Ds[rc * RW + cc];
+                    }
+                }
+            }
+        } else {
+            cp_async_wait<0>();
+        }
         __syncthreads();
         const float qnan = __int_as_float(0x7fffffff);
         const int S = f.S;
@@ -607,6 +698,37 @@ bool prepare_cfg() {
     return true;
 }
 
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+    }
+    return fn;
+}
+
+// 3-D fp32 tensor [d2][H][W], box RW x RH x bz
+bool encode3d(CUtensorMap* m, const float* base, int W, int H, int d2, int RW, int RH, int bz) {
+    EncodeTiledFn fn = encode_fn();
+    if (!fn || (W & 3) || (reinterpret_cast<uintptr_t>(base) & 15)) return false;
+    const cuuint64_t dims[3] = {(cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)d2};
+    const cuuint64_t strides[2] = {(cuuint64_t)W * 4, (cuuint64_t)W * H * 4};
+    const cuuint32_t box[3] = {(cuuint32_t)RW, (cuuint32_t)RH, (cuuint32_t)bz};
+    const cuuint32_t es[3] = {1, 1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides, box, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <int K, int NWY>
 cudaError_t launch_cfg(sf_ctx* c, const float* Y, const float* D) {
     using FC = Cfg<K, NWY>;
@@ -617,6 +739,9 @@ cudaError_t launch_cfg(sf_ctx* c, const float* Y, const float* D) {
     for (int l = 0; l < p.launches; ++l) {
         const bool upd = l == p.launches - 1;
         FusedArgs a;
+        a.tma = getenv("SF_NO_TMA") == nullptr && encode3d(&a.tmE, c->E, f.W, f.H, 6, FC::RW, FC::RH, 3) &&
+                encode3d(&a.tmY, Y, f.W, f.H, f.B, FC::RW, FC::RH, 1) &&
+                encode3d(&a.tmD, D, f.W, f.H, f.B, FC::RW, FC::RH, 1);
         a.fin = src;
         a.sk = c->state[c->cur];
         a.fout = upd ? c->state[1 - c->cur] : bufs[l & 1];
