@@ -159,7 +159,7 @@ struct Cfg {
     // smem floats: E planes 6P | Ys P | Ds/Rs P | XR buffers 2 x 4 XR (>= 2P for HG/HH, and
     // Ys..end >= 3P for the box planes)
     static constexpr int XRF = 2 * 4 * XR > 2 * P ? 2 * 4 * XR : 2 * P;
-    static constexpr size_t SMEM = sizeof(float) * (8 * (size_t)P + XRF);
+    static constexpr size_t SMEM = sizeof(float) * (8 * (size_t)P + XRF) + 64;  // + mbarriers
 };
 
 // The transport: M substeps of a column pass then a row pass on the thread's
@@ -343,7 +343,7 @@ template <int K, int NWY, int RULE, bool CLAMP>
 __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ FusedArgs a) {
     using C = Cfg<K, NWY>;
     constexpr int RW = C::RW, RH = C::RH, P = C::P, NT = C::NT;
-    extern __shared__ float4 smem4[];
+    extern __shared__ __align__(1024) float4 smem4[];  // TMA destinations need 128-byte alignment
     float* const sm = reinterpret_cast<float*>(smem4);
     float* const Es = sm;          // transport: 6 planes e1.xyz, e2.xyz
     float* const Ys = sm + 6 * P;  // Y (replicated clamp)
@@ -364,7 +364,7 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
     const size_t HW = (size_t)f.H * f.W, plane = (size_t)b * HW;
 
     // ---------------- staging: e1 / e2 planes (transport), Y and depth (update)
-    __shared__ __align__(8) uint64_t bars[3];
+    uint64_t* const bars = reinterpret_cast<uint64_t*>(sm + 8 * P + C::XRF);
     if (a.tma) {
         // TMA: one thread issues three bulk tensor copies of the whole region (out-of-range cells
         // arrive as zeros; the replica cells next to grid edges are fixed up below)
@@ -668,7 +668,9 @@ Plan make_plan(const FrameParams& f) {
         p.M[l] = (l < p.launches - 1) ? MMAX : f.N - MMAX * (p.launches - 1);
         const bool upd = l == p.launches - 1;
         int R = upd ? (p.M[l] > 2 ? p.M[l] : 2) + 2 * f.S : p.M[l];
-        p.R[l] = (R + 1) & ~1;  // even: tiles start at even columns (2 cells per lane)
+        // multiple of 4: tile origins are 16-byte aligned columns (TMA needs the innermost start
+        // coordinate x 4 bytes to be a multiple of 16; the lanes own even/odd column pairs)
+        p.R[l] = (R + 3) & ~3;
     }
     return p;
 }
