@@ -51,6 +51,23 @@ def env_rank():
     return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0)))
 
 
+def ncu_traffic(kernel="k_fused"):
+    """DRAM bytes per launch of the dominant kernel from the newest committed ncu --set full
+    summary (profiles/*_ncu_<kernel>.json, written by tools/ncu_summary.py), or None."""
+    import glob
+
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", f"*_ncu_{kernel}.json")), key=os.path.getmtime)
+    for fp in reversed(files):
+        try:
+            caps = json.load(open(fp)).get("captures", [])
+            vals = [c["traffic_bytes_per_launch"] for c in caps if "traffic_bytes_per_launch" in c]
+            if vals:
+                return {"bytes_per_launch": sum(vals) / len(vals), "source": os.path.relpath(fp, ROOT)}
+        except Exception:
+            continue
+    return None
+
+
 def peaks():
     try:
         return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -177,16 +194,17 @@ def run_sf(args):
     B = 1 if cid != 4 else max(1, 64 // world)
     base = sfgen.CONFIGS[2 if cid == 4 else cid]
     H, W = base["H"], base["W"]
-    ring = args.ring
+    # batch steps already read > L2 per step (64 MiB x 2): a short ring of rendered frames
+    ring = args.ring if B == 1 else 8
     # independent sequence(s) per rank (seeds differ); frames of the sequence fill the ring
-    seqs = [sfgen.config_sequence(2 if cid == 4 else cid, frames=ring if B == 1 else 8,
+    seqs = [sfgen.config_sequence(2 if cid == 4 else cid, frames=ring,
                                   seed=(base["seed"] + 1000 * rank + b)) for b in range(B)]
     geom, params = seqs[0].geom, seqs[0].params
     if B == 1:
         Yh, Dh = seqs[0].Y, seqs[0].depth
-    else:  # batch: 8 rendered frames per sequence, cycled through the ring
-        Yh = np.stack([np.stack([s.Y[k % 8] for s in seqs]) for k in range(ring)])
-        Dh = np.stack([np.stack([s.depth[k % 8] for s in seqs]) for k in range(ring)])
+    else:
+        Yh = np.stack([np.stack([s.Y[k] for s in seqs]) for k in range(ring)])
+        Dh = np.stack([np.stack([s.depth[k] for s in seqs]) for k in range(ring)])
     Yd = torch.from_numpy(np.ascontiguousarray(Yh.reshape(ring, B, H, W))).to(dev)
     Dd = torch.from_numpy(np.ascontiguousarray(Dh.reshape(ring, B, H, W))).to(dev)
     frame_bytes = B * H * W * 4
@@ -194,26 +212,41 @@ def run_sf(args):
     s = torch.cuda.Stream(device=dev)
     kern = {"auto": sf.SF_KERNEL_AUTO, "fused": sf.SF_KERNEL_FUSED, "passes": sf.SF_KERNEL_PASSES}[args.kernel]
     m = sf.StructureFlow(geom, params, batch=B, device=local, stream=s, kernel=kern)
+
+    def frame_of(i):
+        """Palindromic replay order 0..R-1, R-1..0: no jump back in time at the wrap (a camera
+        that reverses), while every step still reads a cold frame of a > L2 ring."""
+        j = i % (2 * ring)
+        return j if j < ring else 2 * ring - 1 - j
+
     with torch.cuda.stream(s):
         m.step(Yd[0], Dd[0])  # frame 0: initialisation (not a timed step)
         for k in range(1, ring):  # one real pass over the ring before capture (untimed)
             m.step(Yd[k], Dd[k])
     s.synchronize()
-    # one CUDA graph per ring slot (R even keeps the double-buffer parity)
-    graphs = []
+    # CUDA graphs per (frame, state parity): a captured step reads state[p] and writes
+    # state[1-p]; replays pick the graph of the current parity
+    graphs = [[None, None] for _ in range(ring)]
+    par = 0  # parity relative to the state at capture start
     for k in range(ring):
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g, stream=s):
-            m.step(Yd[k], Dd[k])
-        graphs.append(g)
+        for _ in range(2):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=s):
+                m.step(Yd[k], Dd[k])
+            graphs[k][par] = g
+            par ^= 1
     launches = m.launches_per_step
+    state = {"par": 0, "i": ring}  # the device state sits at parity 0; continue the palindrome
 
-    def replay(i):
-        graphs[i % ring].replay()
+    def replay():
+        k = frame_of(state["i"])
+        graphs[k][state["par"]].replay()
+        state["par"] ^= 1
+        state["i"] += 1
 
     with torch.cuda.stream(s):
         for i in range(args.warmup):
-            replay(i)
+            replay()
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
@@ -226,7 +259,7 @@ def run_sf(args):
     with torch.cuda.stream(s):
         ev[0].record(s)
         for i in range(args.steps):
-            replay(args.warmup + i)
+            replay()
             ev[i + 1].record(s)
     torch.cuda.synchronize(dev)
     if world > 1:
@@ -255,7 +288,9 @@ def run_sf(args):
         dist.barrier()
     t0 = time.perf_counter()
     for i in range(e2e_steps):
-        sf.sf_step_host(m.ctx, Yp[i % ring].data_ptr(), Dp[i % ring].data_ptr(), w_out.data_ptr(), r_out.data_ptr())
+        k = frame_of(state["i"])
+        state["i"] += 1
+        sf.sf_step_host(m.ctx, Yp[k].data_ptr(), Dp[k].data_ptr(), w_out.data_ptr(), r_out.data_ptr())
     e2e_s = torch.tensor([time.perf_counter() - t0], device=dev)
     if world > 1:
         dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
@@ -275,8 +310,11 @@ def run_sf(args):
         alu_peak = SMS * FP32_LANES_PER_SM * sm_max * 1e6 / 1e12  # TFLOP/s-equivalent FP32 lane-ops
         alu = ops / (mean_ms / 1e3) / 1e12
         kname = "k_fused" if m.kernel == sf.SF_KERNEL_FUSED else "whole step (2N+2+2S per-pass kernels)"
+        tr = ncu_traffic() if m.kernel == sf.SF_KERNEL_FUSED else None
         roof = {"bound": "alu", "achieved": alu, "peak": alu_peak, "unit": "TFLOP/s", "frac": alu / alu_peak,
-                "traffic": None, "kernel": kname, "launches_per_step": launches,
+                "traffic": tr["bytes_per_launch"] if tr else None,
+                "traffic_source": (tr["source"] + " (ncu --set full, cache-flushed replay)") if tr else None,
+                "kernel": kname, "launches_per_step": launches,
                 "algo_ops_per_launch": ops / max(1, launches),
                 "peak_source": f"148 SMs x 128 FP32 lanes x {sm_max:.0f} MHz (DESIGN.md section 8)",
                 "hbm_view": {"achieved_gbs": gbs, "peak_gbs": hbm_peak, "frac": gbs / hbm_peak,
@@ -288,7 +326,7 @@ def run_sf(args):
                "config": {"workload": CONFIG_NAMES[cid], "batch_per_gpu": B, "H": H, "W": W, "N": params.N,
                           "S": params.smooth_iters, "parallelism": f"independent sequences x{world}",
                           "inputs": f"ring of {ring} frames ({ring * 2 * frame_bytes / 2**20:.0f} MiB) > L2, "
-                                    "cold reads each step; per-frame CUDA graphs",
+                                    "replayed palindromically, cold reads each step; per-frame CUDA graphs",
                           "kernel": {sf.SF_KERNEL_FUSED: "fused", sf.SF_KERNEL_PASSES: "passes"}.get(m.kernel)},
                "roofline": roof, "gpu_launches": launches * args.steps, "step_ms_median": med_ms,
                "e2e": {"value": e2e_value, "unit": "Hz", "h2d_bytes_per_step": 2 * frame_bytes,
