@@ -34,7 +34,8 @@ import numpy as np  # noqa: E402
 METRIC = "predictor-update Hz at 512x512, 8-px max flow; achieved HBM GB/s vs peak"
 CONFIG_NAMES = {2: "512x512 spherepix (gnomonic 90 deg), max flow 8 px (N=8), S=2, H=1 level",
                 3: "1024x1024 spherepix (gnomonic 90 deg), max flow 16 px (N=16), S=2, H=1 level",
-                4: "64 x 512x512 sequences per job, max flow 8 px (N=8), S=2, H=1 level"}
+                4: "64 x 512x512 sequences per job, max flow 8 px (N=8), S=2, H=1 level",
+                5: "8192x8192 spherepix (gnomonic 90 deg) row-banded over the GPUs, max flow 8 px (N=8), S=2"}
 ALGO_BYTES_PER_PX = 48  # read w 12 + rho 4 + Yhat 4 + Y 4 + lambda 4, write 12 + 4 + 4
 
 
@@ -341,13 +342,110 @@ def run_sf(args):
     return 0
 
 
+def run_banded(args):
+    """configs[4]: one 8192^2 frame per step, row bands over the ranks (strong scaling).  Each
+    rank owns rows [o0, o1) plus halo = max(N,2)+2S rows; per step: NCCL halo exchange
+    (sf_halo_exchange_nccl, 2 x halo rows of state + Yhat), then sf_step on the band."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2406_18031_b200 as sf
+    import sfgen
+
+    rank, world, local = env_rank()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    c = sfgen.CONFIGS[5]
+    H, W = c["H"], c["W"]
+    cfg0 = sf.sf_config_default(H, W)
+    cfg0.max_flow_px = c["max_flow"]
+    cfg0.smooth_iters = 2
+    halo = sf.sf_band_halo(cfg0)
+    e0, o0, o1, e1 = sf.sf_band_partition(H, world, rank, halo)
+    ring = 2  # each frame is 512 MiB of inputs: 2 frames replayed palindromically already exceed L2
+    geom, Yh, Dh, params = sfgen.configs.band_sequence(5, e0, e1, ring)
+    Hb = e1 - e0
+    Yd = torch.from_numpy(Yh.reshape(ring, 1, Hb, W)).to(dev)
+    Dd = torch.from_numpy(Dh.reshape(ring, 1, Hb, W)).to(dev)
+    s = torch.cuda.Stream(device=dev)
+    band = (e0, o0, o1, H) if world > 1 else None
+    m = sf.StructureFlow(geom, params, batch=1, device=local, stream=s, band=band)
+    comm = None
+    if world > 1:
+        uid = torch.zeros(128, dtype=torch.uint8, device=dev)
+        if rank == 0:
+            uid.copy_(torch.frombuffer(bytearray(sf.sf_nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(uid, 0)
+        comm = sf.sf_nccl_comm_init(world, bytes(uid.cpu().numpy()), rank)
+
+    started = [False]
+
+    def step(i):
+        j = i % (2 * ring)
+        k = j if j < ring else 2 * ring - 1 - j
+        if comm is not None and started[0]:
+            sf.sf_halo_exchange_nccl(m.ctx, comm, rank, world)
+        m.step(Yd[k], Dd[k])
+        started[0] = True
+
+    with torch.cuda.stream(s):
+        for i in range(args.warmup + 1):
+            step(i)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    clk, clk_path = (start_clock_sampler(local) if rank == 0 else (None, None))
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(s):
+        ev0.record(s)
+        for i in range(args.steps):
+            step(args.warmup + 1 + i)
+        ev1.record(s)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    clocks = stop_clock_sampler(clk, clk_path) if rank == 0 else None
+    t = torch.tensor([ev0.elapsed_time(ev1)], device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    flags = sf.sf_status_flags(m.ctx)[1]
+    if rank == 0:
+        value = args.steps / (total_ms / 1e3)  # whole 8192^2 frames per second
+        ops = algo_ops_per_px(params.N, params.smooth_iters) * H * W
+        pk = peaks() or {}
+        sm_max = pk.get("sm_max_mhz", 1965.0)
+        alu_peak = world * SMS * FP32_LANES_PER_SM * sm_max * 1e6 / 1e12
+        alu = ops / (total_ms / args.steps / 1e3) / 1e12
+        out = {"metric": METRIC, "value": value, "unit": "Hz", "n_gpus": world, "steps": args.steps,
+               "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+               "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+               "config": {"workload": CONFIG_NAMES[5], "H": H, "W": W, "N": params.N, "S": params.smooth_iters,
+                          "parallelism": f"row bands x{world}, halo {halo} rows, 1 NCCL exchange / frame",
+                          "inputs": f"{ring} frames x {2 * H * W * 4 / 2**20:.0f} MiB, palindromic (> L2)"},
+               "roofline": {"bound": "alu", "achieved": alu, "peak": alu_peak, "unit": "TFLOP/s",
+                            "frac": alu / alu_peak, "traffic": None, "kernel": "k_fused + halo exchange",
+                            "peak_source": f"{world} x 148 SMs x 128 FP32 lanes x {sm_max:.0f} MHz"},
+               "gpu_launches": m.launches_per_step * args.steps, "e2e": None, "device_flags": flags, "clocks": clocks}
+        print(json.dumps(out))
+    if comm is not None:
+        torch.cuda.synchronize(dev)
+        sf.sf_nccl_comm_destroy(comm)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=2000)
     ap.add_argument("--warmup", type=int, default=100)
     ap.add_argument("--impl", choices=["sf", "reference"], default="sf")
-    ap.add_argument("--config", type=int, choices=[2, 3, 4], default=2)
+    ap.add_argument("--config", type=int, choices=[2, 3, 4, 5], default=2)
     ap.add_argument("--kernel", choices=["auto", "fused", "passes"], default="auto")
     ap.add_argument("--ring", type=int, default=96)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -358,6 +456,8 @@ def main():
         args.ring += 1
     if args.impl == "reference":
         return run_reference(args)
+    if args.config == 5:
+        return run_banded(args)
     return run_sf(args)
 
 

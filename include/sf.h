@@ -83,7 +83,16 @@ typedef struct {
     void* stream;                   /* cudaStream_t for all work (cudaStreamLegacy allowed); NULL: the
                                        context creates its own non-blocking stream                     */
     int32_t kernel;                 /* SF_KERNEL_*                                                    */
-    int32_t reserved[7];            /* zero                                                           */
+    /* Banded mode (row-band decomposition of a tall grid over several contexts / GPUs,
+     * DESIGN.md section 10).  All zero: the context is the whole grid.  Otherwise the context
+     * holds rows [band_ext_begin, band_ext_begin + height) of a global grid of global_height
+     * rows and OWNS rows [band_own_begin, band_own_end): the others are halo rows refreshed by
+     * sf_halo_exchange_* before each sf_step (see sf_band_partition). */
+    int32_t band_ext_begin;
+    int32_t band_own_begin;
+    int32_t band_own_end;
+    int32_t global_height;
+    int32_t reserved[3];            /* zero                                                           */
 } sf_config;
 
 /* Fill *cfg with defaults for an H x W grid (batch 1, max flow 1 px, S = 2, sigma = 0.5,
@@ -136,6 +145,34 @@ sf_status sf_set_fields(sf_ctx* ctx, const float* w, const float* rho, const flo
 /* Read (and optionally clear) the sticky device flags; synchronises the stream.  Returns
  * SF_E_STABILITY if SF_FLAG_CFL is set, else SF_OK. */
 sf_status sf_status_flags(sf_ctx* ctx, uint32_t* flags, int32_t clear);
+
+/* ---- banded mode -------------------------------------------------------------------------
+ * Halo rows a band needs so that its owned rows are exact after one sf_step: the transport
+ * moves information N rows per frame (eq:numerical_stability), the update reads +-2 rows of
+ * brightness and +-1 of depth and S box passes reach +-2S: halo = max(N, 2) + 2S. */
+int32_t sf_band_halo(const sf_config* cfg);
+
+/* Even split of global_height rows into nbands bands; band b owns [*own_begin, *own_end) and
+ * its context holds [*ext_begin, *ext_end) (owned rows + `halo` rows each side, clipped to the
+ * grid).  Errors: SF_E_CONFIG (a band thinner than the halo, bad indices). */
+sf_status sf_band_partition(int32_t global_height, int32_t nbands, int32_t band, int32_t halo, int32_t* ext_begin,
+                            int32_t* own_begin, int32_t* own_end, int32_t* ext_end);
+
+/* Refresh this band's halo rows of the state (w, rho, Yhat^k) from the neighbouring bands'
+ * contexts in this process (device-to-device copies on ctx's stream; up / down NULL at the grid
+ * edges).  All bands must share a stream or be ordered by the caller. */
+sf_status sf_halo_exchange_peer(sf_ctx* ctx, const sf_ctx* up, const sf_ctx* down);
+
+/* The same exchange across processes: ncclSend / ncclRecv of the boundary rows with ranks
+ * rank - 1 and rank + 1 (band index == rank) on ctx's stream.  nccl_comm: an ncclComm_t from
+ * sf_nccl_comm_init (or any communicator of the same NCCL library).  Errors: SF_E_NCCL. */
+sf_status sf_halo_exchange_nccl(sf_ctx* ctx, void* nccl_comm, int32_t rank, int32_t nranks);
+
+/* NCCL plumbing (libnccl.so.2 is loaded at first use): rank 0 makes a 128-byte unique id, the
+ * caller broadcasts it (e.g. torch.distributed), every rank creates its communicator. */
+sf_status sf_nccl_unique_id(char id[128]);
+sf_status sf_nccl_comm_init(int32_t nranks, const char id[128], int32_t rank, void** comm);
+void sf_nccl_comm_destroy(void* comm);
 
 /* Kernel strategy actually used by sf_step (SF_KERNEL_FUSED or SF_KERNEL_PASSES). */
 int32_t sf_kernel_in_use(const sf_ctx* ctx);

@@ -24,7 +24,8 @@ SF_ABI_VERSION = 1
 
 EXPORTS = ("sf_config_default", "sf_create", "sf_destroy", "sf_predict", "sf_update", "sf_step", "sf_step_host",
            "sf_get_fields", "sf_set_fields", "sf_status_flags", "sf_kernel_in_use", "sf_launches_per_step",
-           "sf_error_string")
+           "sf_error_string", "sf_band_halo", "sf_band_partition", "sf_halo_exchange_peer", "sf_halo_exchange_nccl",
+           "sf_nccl_unique_id", "sf_nccl_comm_init", "sf_nccl_comm_destroy")
 
 
 class sf_config(C.Structure):
@@ -32,7 +33,9 @@ class sf_config(C.Structure):
                 ("levels", C.c_int32), ("max_flow_px", C.c_float), ("gamma", C.c_float * 5),
                 ("smooth_iters", C.c_int32), ("dominant_rule", C.c_int32), ("source_weight", C.c_float),
                 ("clamp_advection", C.c_int32), ("input_is_inverse_depth", C.c_int32), ("device", C.c_int32),
-                ("stream", C.c_void_p), ("kernel", C.c_int32), ("reserved", C.c_int32 * 7)]
+                ("stream", C.c_void_p), ("kernel", C.c_int32), ("band_ext_begin", C.c_int32),
+                ("band_own_begin", C.c_int32), ("band_own_end", C.c_int32), ("global_height", C.c_int32),
+                ("reserved", C.c_int32 * 3)]
 
 
 class SFError(RuntimeError):
@@ -63,8 +66,19 @@ def _load():
     lib.sf_launches_per_step.argtypes = [P]
     lib.sf_error_string.argtypes = [C.c_int]
     lib.sf_error_string.restype = C.c_char_p
+    lib.sf_band_halo.argtypes = [C.POINTER(sf_config)]
+    I = C.POINTER(C.c_int32)
+    lib.sf_band_partition.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.c_int32, I, I, I, I]
+    lib.sf_halo_exchange_peer.argtypes = [P, P, P]
+    lib.sf_halo_exchange_nccl.argtypes = [P, P, C.c_int32, C.c_int32]
+    lib.sf_nccl_unique_id.argtypes = [C.c_char_p]
+    lib.sf_nccl_comm_init.argtypes = [C.c_int32, C.c_char_p, C.c_int32, C.POINTER(P)]
+    lib.sf_nccl_comm_destroy.argtypes = [P]
+    lib.sf_nccl_comm_destroy.restype = None
     for name in ("sf_create", "sf_predict", "sf_update", "sf_step", "sf_step_host", "sf_get_fields",
-                 "sf_set_fields", "sf_status_flags", "sf_kernel_in_use", "sf_launches_per_step"):
+                 "sf_set_fields", "sf_status_flags", "sf_kernel_in_use", "sf_launches_per_step", "sf_band_halo",
+                 "sf_band_partition", "sf_halo_exchange_peer", "sf_halo_exchange_nccl", "sf_nccl_unique_id",
+                 "sf_nccl_comm_init"):
         getattr(lib, name).restype = C.c_int
     return lib
 
@@ -142,6 +156,41 @@ def sf_launches_per_step(ctx: int) -> int:
     return _lib.sf_launches_per_step(C.c_void_p(ctx))
 
 
+def sf_band_halo(cfg: sf_config) -> int:
+    return _lib.sf_band_halo(C.byref(cfg))
+
+
+def sf_band_partition(global_height: int, nbands: int, band: int, halo: int) -> tuple[int, int, int, int]:
+    """(ext_begin, own_begin, own_end, ext_end) of band `band`."""
+    v = [C.c_int32() for _ in range(4)]
+    _check(_lib.sf_band_partition(global_height, nbands, band, halo, *[C.byref(x) for x in v]), "sf_band_partition")
+    return tuple(x.value for x in v)
+
+
+def sf_halo_exchange_peer(ctx: int, up: int | None, down: int | None) -> None:
+    _check(_lib.sf_halo_exchange_peer(C.c_void_p(ctx), C.c_void_p(up), C.c_void_p(down)), "sf_halo_exchange_peer")
+
+
+def sf_halo_exchange_nccl(ctx: int, comm: int, rank: int, nranks: int) -> None:
+    _check(_lib.sf_halo_exchange_nccl(C.c_void_p(ctx), C.c_void_p(comm), rank, nranks), "sf_halo_exchange_nccl")
+
+
+def sf_nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _check(_lib.sf_nccl_unique_id(buf), "sf_nccl_unique_id")
+    return buf.raw
+
+
+def sf_nccl_comm_init(nranks: int, uid: bytes, rank: int) -> int:
+    h = C.c_void_p()
+    _check(_lib.sf_nccl_comm_init(nranks, C.create_string_buffer(uid, 128), rank, C.byref(h)), "sf_nccl_comm_init")
+    return h.value
+
+
+def sf_nccl_comm_destroy(comm: int) -> None:
+    _lib.sf_nccl_comm_destroy(C.c_void_p(comm))
+
+
 # ----------------------------------------------------------------------------- torch convenience
 class StructureFlow:
     """One libsf context over torch CUDA tensors (marshalling only).
@@ -151,7 +200,10 @@ class StructureFlow:
     clamp_advection, input_is_inverse_depth (e.g. sfgen.Params).
     """
 
-    def __init__(self, geometry, params, batch: int = 1, device: int = 0, stream=None, kernel: int = SF_KERNEL_AUTO):
+    def __init__(self, geometry, params, batch: int = 1, device: int = 0, stream=None, kernel: int = SF_KERNEL_AUTO,
+                 band: tuple | None = None):
+        """band: None, or (ext_begin, own_begin, own_end, global_height) for a row-band context
+        whose geometry holds the global rows [ext_begin, ext_begin + H)."""
         import numpy as np
         import torch
 
@@ -177,6 +229,8 @@ class StructureFlow:
         # pass cudaStreamLegacy (0x1) so libsf orders with torch's work on that stream.
         cfg.stream = self.stream.cuda_stream or 1
         cfg.kernel = kernel
+        if band is not None:
+            cfg.band_ext_begin, cfg.band_own_begin, cfg.band_own_end, cfg.global_height = (int(x) for x in band)
         self.cfg = cfg
         torch.cuda.synchronize(self.device)
         self.ctx = sf_create(cfg, g.data_ptr())

@@ -10,7 +10,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-SOURCES = ["sf_api.cu", "sf_passes.cu", "sf_fused.cu"]
+SOURCES = ["sf_api.cu", "sf_passes.cu", "sf_fused.cu", "sf_band.cu"]
 LIB = os.path.join(HERE, "libsf.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
@@ -19,6 +19,7 @@ FLAGS = [
     # IEEE float32: no fast math, no FTZ, correctly rounded division / sqrt
     "-ftz=false", "-prec-div=true", "-prec-sqrt=true",
     "-I" + os.path.join(ROOT, "include"),
+    "-ldl",
 ]
 
 

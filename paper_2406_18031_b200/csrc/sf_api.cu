@@ -40,6 +40,14 @@ static sf_status validate(const sf_config* c) {
     if (c->dominant_rule != SF_DOM_LARGEST && c->dominant_rule != SF_DOM_PRINTED) return SF_E_CONFIG;
     if (!(c->source_weight >= 0.0f) || !isfinite(c->source_weight)) return SF_E_CONFIG;
     if (c->kernel < SF_KERNEL_AUTO || c->kernel > SF_KERNEL_PASSES) return SF_E_CONFIG;
+    if (c->band_own_end != 0) {  // banded mode
+        const int gh = c->global_height;
+        if (c->band_ext_begin < 0 || c->band_ext_begin > c->band_own_begin || c->band_own_begin >= c->band_own_end ||
+            c->band_own_end > c->band_ext_begin + c->height || c->band_ext_begin + c->height > gh)
+            return SF_E_CONFIG;
+    } else if (c->band_ext_begin != 0 || c->band_own_begin != 0 || (c->global_height != 0 && c->global_height != c->height)) {
+        return SF_E_CONFIG;
+    }
     if (c->levels != 1) return SF_E_UNSUPPORTED;
     return SF_OK;
 }
@@ -84,6 +92,19 @@ extern "C" sf_status sf_create(const sf_config* cfg, const float* geometry, sf_c
         volatile float g45 = cfg->gamma[3] + cfg->gamma[4];  // float32 sum, then IEEE division
         f.kappa = cfg->gamma[3] / g45;
     }
+    if (cfg->band_own_end != 0) {
+        c->ext_begin = cfg->band_ext_begin;
+        c->own_begin = cfg->band_own_begin;
+        c->own_end = cfg->band_own_end;
+        c->global_h = cfg->global_height;
+    } else {
+        c->ext_begin = 0;
+        c->own_begin = 0;
+        c->own_end = f.H;
+        c->global_h = f.H;
+    }
+    f.fr0 = c->own_begin - c->ext_begin;
+    f.fr1 = c->own_end - c->ext_begin;
     if (cfg->stream) {
         c->stream = (cudaStream_t)cfg->stream;
     } else {

@@ -479,7 +479,7 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
 #pragma unroll
         for (int k = 0; k < K; ++k) {
             const int r = r0 + k;
-            if (tcol && r >= R && r < R + TH && r >= rmin && r <= rmax) {
+            if (tcol && r >= R && r < R + TH && r >= rmin && r <= rmax && gi0 + r >= f.fr0 && gi0 + r < f.fr1) {
                 if (CLAMP) {
                     if (mx[k] > U) fl |= SF_FLAG_CLAMPED;
                 } else if (xmul(f.dt, mx[k]) > 1.0f) {
@@ -549,7 +549,7 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
                 HG[idx] = tap_g(x0, x1, x2, x3, x4);
                 HH[idx] = tap_h(x0, x1, x2, x3, x4);
                 if (r >= R && r < R + TH && c >= R && c < R + TW && r >= rmin && r <= rmax && c >= cmin &&
-                    c <= cmax && !isfinite(x2))
+                    c <= cmax && gi0 + r >= f.fr0 && gi0 + r < f.fr1 && !isfinite(x2))
                     fl |= SF_FLAG_NONFINITE;
             }
         }
@@ -592,7 +592,9 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
             Fy[idx] = x[1];
             Fz[idx] = x[2];
             Fw[idx] = rn;
-            if (!(isfinite(x[0]) && isfinite(x[1]) && isfinite(x[2]) && isfinite(rn))) fl |= SF_FLAG_NONFINITE;
+            if (!(isfinite(x[0]) && isfinite(x[1]) && isfinite(x[2]) && isfinite(rn)) && gi0 + r >= f.fr0 &&
+                gi0 + r < f.fr1)
+                fl |= SF_FLAG_NONFINITE;
             if (r >= R && r < R + TH && c >= R && c < R + TW) a.yout[plane + g] = yh;
         }
         // ---- S x 5x5 box (reading 13): horizontal 5-sum -> Tq, vertical 5-sum / 25 -> Fq

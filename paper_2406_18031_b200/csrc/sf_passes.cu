@@ -68,8 +68,9 @@ __global__ void __launch_bounds__(BX* BY) k_pass(const float4* __restrict__ in, 
     o.y = xfma(-f.dt, xfma(uh, fwd ? xsub(c.y, cm.y) : xsub(cp.y, c.y), xmul(c.y, q)), c.y);
     o.z = xfma(-f.dt, xfma(uh, fwd ? xsub(c.z, cm.z) : xsub(cp.z, c.z), xmul(c.z, q)), c.z);
     o.w = xfma(-f.dt, xfma(uh, fwd ? xsub(c.w, cm.w) : xsub(cp.w, c.w), xmul(c.w, q)), c.w);
-    raise_flag(flags, live && clamped, SF_FLAG_CLAMPED);
-    raise_flag(flags, live && cfl, SF_FLAG_CFL);
+    const bool own = live && i >= f.fr0 && i < f.fr1;  // banded mode: owned rows only
+    raise_flag(flags, own && clamped, SF_FLAG_CLAMPED);
+    raise_flag(flags, own && cfl, SF_FLAG_CFL);
     if (live) out[base + g] = o;
 }
 
@@ -87,7 +88,7 @@ __global__ void __launch_bounds__(BX* BY) k_hconv(const float* __restrict__ Y, f
         const size_t p = ((size_t)b * f.H + i) * f.W + j;
         HG[p] = tap_g(x0, x1, x2, x3, x4);
         HH[p] = tap_h(x0, x1, x2, x3, x4);
-        bad = !isfinite(x2);
+        bad = !isfinite(x2) && i >= f.fr0 && i < f.fr1;
     }
     raise_flag(flags, bad, SF_FLAG_NONFINITE);
 }
@@ -173,7 +174,7 @@ __global__ void __launch_bounds__(BX* BY) k_solve(const float* __restrict__ HG, 
         const float rn = xfma(kap, xsub(M.rh, wp.w), wp.w);  // fusion (reading 21)
         out[p] = make_float4(x[0], x[1], x[2], rn);
         yout[p] = M.yh;
-        bad = !(isfinite(x[0]) && isfinite(x[1]) && isfinite(x[2]) && isfinite(rn));
+        bad = !(isfinite(x[0]) && isfinite(x[1]) && isfinite(x[2]) && isfinite(rn)) && i >= f.fr0 && i < f.fr1;
     }
     raise_flag(flags, bad, SF_FLAG_NONFINITE);
 }

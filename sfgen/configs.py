@@ -115,15 +115,18 @@ MAX_NORMAL_RATE = 0.02  # |<s, w_gt>| <= 2 % depth change per frame (time to con
 
 
 def make_scene(name: str, seed: int, geom64: np.ndarray, max_flow: float, frames: int = 1,
-               target: float = 0.9) -> Scene:
+               target: float = 0.9, subsampled: bool = False) -> Scene:
     """Scene with velocities scaled (bisection) so that, over frames 0 and F-1, the peak
     ground-truth tangent flow is target*max_flow pixels, or the peak normal rate
     |<s, w_gt>| is MAX_NORMAL_RATE per frame, whichever binds first."""
     rng = np.random.default_rng(seed)
     base = SCENES[name](rng)
-    # render at reduced resolution for the scale search (flow in px scales with 1/ds)
-    step = max(1, min(geom64.shape[0], geom64.shape[1]) // 128)
-    g = geom64[::step, ::step]
+    # render at reduced resolution for the scale search (per-pixel ds keeps the flow in full-res px)
+    if subsampled:
+        g = geom64
+    else:
+        step = max(1, min(geom64.shape[0], geom64.shape[1]) // 128)
+        g = geom64[::step, ::step]
     def peak(a):
         sc = base.scaled(a)
         r = 0.0
@@ -159,6 +162,26 @@ def make_sequence(H: int, W: int, fov: float, max_flow: float, frames: int, seed
             Ws.append(w)
     return Sequence(geom, np.stack(Ys), np.stack(Ds), np.stack(Ws) if with_gt else None,
                     default_params(geom, max_flow, smooth_iters), sc)
+
+
+def band_sequence(cid: int, r0: int, r1: int, frames: int, seed: int | None = None):
+    """Rows [r0, r1) of config `cid`'s sequence (same scene and speed scale as the whole grid),
+    generated without the whole grid: the 8192^2 row-band config.  Returns (geom, Y, depth, params)."""
+    c = dict(CONFIGS[cid])
+    H, W = c["H"], c["W"]
+    step = max(1, min(H, W) // 128)
+    gsub = _grid.gnomonic_rows(H, W, c["fov"], 0, H, as_f64=True, col_step=step, row_step=step)
+    sc = make_scene(c["scene"], c["seed"] if seed is None else seed, gsub, c["max_flow"], frames, subsampled=True)
+    g64 = _grid.gnomonic_rows(H, W, c["fov"], r0, r1, as_f64=True)
+    Ys, Ds = [], []
+    for k in range(frames):
+        y, d, _ = render(sc, g64[..., 0:3], float(k))
+        Ys.append(y)
+        Ds.append(d)
+    # gains from the centre pixel of the whole grid (default_params reads the centre of the geometry)
+    centre = _grid.gnomonic_rows(H, W, c["fov"], H // 2, H // 2 + 1, col_step=1)[0:1, W // 2:W // 2 + 1]
+    params = default_params(centre, c["max_flow"])
+    return g64.astype(np.float32), np.stack(Ys), np.stack(Ds), params
 
 
 def config_sequence(cid: int, frames: int | None = None, H: int | None = None, W: int | None = None,

@@ -32,19 +32,22 @@ def _tangent_project(s: np.ndarray, x: np.ndarray) -> np.ndarray:
     return x - s * np.sum(s * x, axis=-1, keepdims=True)
 
 
-def directions_gnomonic(H: int, W: int, fov_deg: float) -> np.ndarray:
+def directions_gnomonic(H: int, W: int, fov_deg: float, rows=None, cols=None) -> np.ndarray:
     """Unit directions of a gnomonic patch, square pixels, horizontal FOV = fov_deg.
 
     Pixel (i, j) looks through the image-plane point ((j - (W-1)/2) p, (i - (H-1)/2) p, 1)
     with pitch p = 2 tan(fov/2) / W.  The centre of the patch is the optical axis +z.
+    rows / cols: optional integer index arrays (a sub-grid of the H x W patch).
     """
     if not (0.0 < fov_deg < 180.0):
         raise ValueError("fov_deg must be in (0, 180)")
     if H < 2 or W < 2:
         raise ValueError("grid must be at least 2x2")
     p = 2.0 * np.tan(np.radians(fov_deg) / 2.0) / W
-    x = (np.arange(W, dtype=np.float64) - (W - 1) / 2.0) * p
-    y = (np.arange(H, dtype=np.float64) - (H - 1) / 2.0) * p
+    jj = np.arange(W, dtype=np.float64) if cols is None else np.asarray(cols, dtype=np.float64)
+    ii = np.arange(H, dtype=np.float64) if rows is None else np.asarray(rows, dtype=np.float64)
+    x = (jj - (W - 1) / 2.0) * p
+    y = (ii - (H - 1) / 2.0) * p
     X, Y = np.meshgrid(x, y)
     v = np.stack([X, Y, np.ones_like(X)], axis=-1)
     return _normalize(v)
@@ -77,6 +80,31 @@ def geometry_from_directions(s: np.ndarray) -> np.ndarray:
 def gnomonic(H: int, W: int, fov_deg: float, as_f64: bool = False) -> np.ndarray:
     """GNOMONIC grid geometry [H][W][10], float32 (or the float64 original)."""
     g = geometry_from_directions(directions_gnomonic(H, W, fov_deg))
+    return g if as_f64 else g.astype(np.float32)
+
+
+def gnomonic_rows(H: int, W: int, fov_deg: float, r0: int, r1: int, as_f64: bool = False,
+                  col_step: int = 1, row_step: int = 1) -> np.ndarray:
+    """Rows [r0, r1) (every row_step-th, every col_step-th column) of the H x W GNOMONIC grid,
+    identical to gnomonic(H, W, fov)[r0:r1:row_step, ::col_step] but computed without the whole grid
+    (row bands of the 8192^2 config, subsampled scale searches)."""
+    rows = np.arange(r0, r1, row_step)
+    cols = np.arange(0, W, col_step)
+    s = directions_gnomonic(H, W, fov_deg, rows, cols)
+    # neighbours: (i, j+1) (mirrored (i, j-1) on the last column) and (i+1, j) (mirrored on the last row)
+    cn = np.where(cols < W - 1, cols + 1, cols - 1)
+    rn = np.where(rows < H - 1, rows + 1, rows - 1)
+    sc = directions_gnomonic(H, W, fov_deg, rows, cn)
+    sr = directions_gnomonic(H, W, fov_deg, rn, cols)
+    sign_c = np.where(cols < W - 1, 1.0, -1.0)[None, :, None]
+    sign_r = np.where(rows < H - 1, 1.0, -1.0)[:, None, None]
+    mu1 = sign_c * _tangent_project(s, sc)
+    ds = np.linalg.norm(mu1, axis=-1)
+    b1 = mu1 / ds[..., None]
+    mu2 = sign_r * _tangent_project(s, sr)
+    mu2 = mu2 - b1 * np.sum(mu2 * b1, axis=-1, keepdims=True)
+    b2 = _normalize(mu2)
+    g = np.concatenate([s, b1, b2, ds[..., None]], axis=-1)
     return g if as_f64 else g.astype(np.float32)
 
 

@@ -312,3 +312,104 @@ def test_fused_equals_passes_on_bench_ring():
             for name, x, y in zip(("w", "rho", "yhat"), a, b):
                 assert_parity(y, x, f"{name} step {i}")
             assert sf.sf_status_flags(ms["passes"].ctx)[1] == sf.sf_status_flags(ms["fused"].ctx)[1], i
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+@pytest.mark.parametrize("H,W,nb,N,S", [(150, 61, 3, 8, 2), (200, 64, 4, 5, 1), (97, 128, 2, 16, 2)])
+def test_banded_equals_single_context(kernel, H, W, nb, N, S):
+    """Row bands (config 5 decomposition) on one GPU: nb band contexts with
+    halo = max(N,2)+2S rows, halo exchange by peer copies before every frame, then sf_step on
+    each band: the owned rows are bitwise the single-context result, flags included."""
+    sf = _sf()
+    g = grid.gnomonic(H, W, 80.0)
+    p = Params(max_flow=float(N), gamma=(3e5, 3e6, 1.0, 1.0, 2.0), smooth_iters=S)
+    rng = np.random.default_rng(H + W)
+    ds = g[..., 9][None, ..., None]
+    w = (rng.normal(size=(1, H, W, 3)) * 0.5 * N * ds).astype(np.float32)
+    rho = rng.uniform(0.05, 0.6, (1, H, W)).astype(np.float32)
+    yh = rng.uniform(0.1, 0.9, (1, H, W)).astype(np.float32)
+    Ys = rng.uniform(0.1, 0.9, (3, 1, H, W)).astype(np.float32)
+    Ds = rng.uniform(1.0, 9.0, (3, 1, H, W)).astype(np.float32)
+    stream = torch.cuda.current_stream()
+    full = sf.StructureFlow(g, p, kernel=_kernel_id(kernel), stream=stream)
+    full.set_fields(_dev(w), _dev(rho), _dev(yh))
+    halo = sf.sf_band_halo(full.cfg)
+    assert halo == max(N, 2) + 2 * S
+    bands = []
+    for bi in range(nb):
+        e0, o0, o1, e1 = sf.sf_band_partition(H, nb, bi, halo)
+        m = sf.StructureFlow(g[e0:e1], p, kernel=_kernel_id(kernel), stream=stream, band=(e0, o0, o1, H))
+        m.set_fields(_dev(w[:, e0:e1]), _dev(rho[:, e0:e1]), _dev(yh[:, e0:e1]))
+        bands.append((m, e0, o0, o1, e1))
+    for k in range(3):
+        full.step(_dev(Ys[k]), _dev(Ds[k]))
+        for bi, (m, e0, o0, o1, e1) in enumerate(bands):
+            up = bands[bi - 1][0].ctx if bi > 0 else None
+            dn = bands[bi + 1][0].ctx if bi < nb - 1 else None
+            sf.sf_halo_exchange_peer(m.ctx, up, dn)
+        for m, e0, o0, o1, e1 in bands:
+            m.step(_dev(np.ascontiguousarray(Ys[k][:, e0:e1])), _dev(np.ascontiguousarray(Ds[k][:, e0:e1])))
+    ref = _fields(full)
+    fl = 0
+    for m, e0, o0, o1, e1 in bands:
+        got = _fields(m)
+        for name, x, y in zip(("w", "rho", "yhat"), ref, got):
+            assert_parity(y[:, o0 - e0:o1 - e0], x[:, o0:o1], f"{name} band rows {o0}:{o1}")
+        fl |= sf.sf_status_flags(m.ctx)[1]
+    assert fl == sf.sf_status_flags(full.ctx)[1]
+
+
+def _oracle_crop_step(geom, params, w, rho, yh, Y, D, i, j, rad):
+    """One oracle frame on a (2 rad + 1)^2 crop around (i, j) of a full-size grid, from the given
+    state: the centre is exact when rad >= the dependency radius max(N,2) + 2S + 1 (its value
+    cannot see the crop's artificial replicate border).  Returns (w, rho, yhat) at (i, j)."""
+    H, W = geom.shape[:2]
+    r0, r1 = max(0, i - rad), min(H, i + rad + 1)
+    c0, c1 = max(0, j - rad), min(W, j + rad + 1)
+    o = oracle.Oracle(np.ascontiguousarray(geom[r0:r1, c0:c1]), params, "f32")
+    o.set_state(np.ascontiguousarray(w[r0:r1, c0:c1]), np.ascontiguousarray(rho[r0:r1, c0:c1]),
+                np.ascontiguousarray(yh[r0:r1, c0:c1]))
+    o.step(np.ascontiguousarray(Y[r0:r1, c0:c1]), np.ascontiguousarray(D[r0:r1, c0:c1]))
+    return o.w[i - r0, j - c0], o.rho[i - r0, j - c0], o.yhat[i - r0, j - c0]
+
+
+def test_config5_8192_banded_full_size():
+    """configs[4] at full size on one GPU: 8 row-band contexts (halo exchange by peer copies) vs
+    one 8192 x 8192 context, 2 frames, bitwise on every owned row; and sampled pixels of the
+    second frame against the float32 oracle run on 49 x 49 crops (dependency radius 13)."""
+    sf = _sf()
+    H = W = 8192
+    frames = 2
+    g, Y, D, p = sfgen.configs.band_sequence(5, 0, H, frames)
+    stream = torch.cuda.current_stream()
+    full = sf.StructureFlow(g, p, stream=stream)
+    nb = 8
+    halo = sf.sf_band_halo(full.cfg)
+    bands = []
+    for bi in range(nb):
+        e0, o0, o1, e1 = sf.sf_band_partition(H, nb, bi, halo)
+        bands.append((sf.StructureFlow(g[e0:e1], p, stream=stream, band=(e0, o0, o1, H)), e0, o0, o1, e1))
+    state0 = None
+    for k in range(frames):
+        Yk, Dk = _dev(Y[k]), _dev(D[k])
+        if k == frames - 1:
+            state0 = _fields(full)
+        full.step(Yk, Dk)
+        if k > 0:
+            for bi, (m, *_r) in enumerate(bands):
+                sf.sf_halo_exchange_peer(m.ctx, bands[bi - 1][0].ctx if bi else None,
+                                         bands[bi + 1][0].ctx if bi < nb - 1 else None)
+        for m, e0, o0, o1, e1 in bands:
+            m.step(Yk[e0:e1].contiguous(), Dk[e0:e1].contiguous())
+    ref = _fields(full)
+    for m, e0, o0, o1, e1 in bands:
+        got = _fields(m)
+        for x, y in zip(ref, got):
+            assert np.array_equal(y[:, o0 - e0:o1 - e0], x[:, o0:o1])
+    rng = np.random.default_rng(5)
+    pts = [(0, 0), (H - 1, W - 1), (H // 2, W // 2), (1023, 4000), (1024, 17)] + \
+          [tuple(rng.integers(0, H, 2)) for _ in range(6)]
+    w0, r0, y0 = (x[0] for x in state0)
+    for (i, j) in pts:
+        ow, orho, oy = _oracle_crop_step(g, p, w0, r0, y0, Y[-1], D[-1], int(i), int(j), 24)
+        assert np.array_equal(ref[0][0, i, j], ow) and ref[1][0, i, j] == orho and ref[2][0, i, j] == oy, (i, j)
