@@ -172,16 +172,22 @@ def band_sequence(cid: int, r0: int, r1: int, frames: int, seed: int | None = No
     step = max(1, min(H, W) // 128)
     gsub = _grid.gnomonic_rows(H, W, c["fov"], 0, H, as_f64=True, col_step=step, row_step=step)
     sc = make_scene(c["scene"], c["seed"] if seed is None else seed, gsub, c["max_flow"], frames, subsampled=True)
-    g64 = _grid.gnomonic_rows(H, W, c["fov"], r0, r1, as_f64=True)
-    Ys, Ds = [], []
-    for k in range(frames):
-        y, d, _ = render(sc, g64[..., 0:3], float(k))
-        Ys.append(y)
-        Ds.append(d)
+    # row chunks keep the float64 working set small at 8192^2
+    geom = np.empty((r1 - r0, W, 10), np.float32)
+    Ys = np.empty((frames, r1 - r0, W), np.float32)
+    Ds = np.empty((frames, r1 - r0, W), np.float32)
+    for a in range(r0, r1, 256):
+        b = min(r1, a + 256)
+        g64 = _grid.gnomonic_rows(H, W, c["fov"], a, b, as_f64=True)
+        geom[a - r0:b - r0] = g64
+        for k in range(frames):
+            y, d, _ = render(sc, g64[..., 0:3], float(k))
+            Ys[k, a - r0:b - r0] = y
+            Ds[k, a - r0:b - r0] = d
     # gains from the centre pixel of the whole grid (default_params reads the centre of the geometry)
     centre = _grid.gnomonic_rows(H, W, c["fov"], H // 2, H // 2 + 1, col_step=1)[0:1, W // 2:W // 2 + 1]
     params = default_params(centre, c["max_flow"])
-    return g64.astype(np.float32), np.stack(Ys), np.stack(Ds), params
+    return geom, Ys, Ds, params
 
 
 def config_sequence(cid: int, frames: int | None = None, H: int | None = None, W: int | None = None,
