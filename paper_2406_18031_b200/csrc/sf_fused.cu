@@ -94,6 +94,10 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
+// ---- programmatic dependent launch (griddepcontrol; no-ops without the launch attribute)
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;\n" ::); }
+
 // ---- mbarrier + TMA (cp.async.bulk.tensor) helpers
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
@@ -133,6 +137,7 @@ struct FusedArgs {
     CUtensorMap tmY;    // [B][H][W] brightness, box 64 x 72 x 1
     CUtensorMap tmD;    // [B][H][W] depth, box 64 x 72 x 1
     int tma;            // 1: stage e / Y / depth with TMA (needs W % 4 == 0, 16-byte aligned bases)
+    int dbg_skip;       // timing experiments only (SF_DEBUG_SKIP): 1 = skip transport, 2 = skip update
     const float4* fin;  // fields at launch start (state k or a partial prediction)
     const float4* sk;   // state k (rho^k for the update)
     float4* fout;       // state k+1 (upd) or partial prediction
@@ -375,16 +380,11 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
             asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
         }
         __syncthreads();
-        if (tid == 0) {
+        if (tid == 0) {  // geometry: independent of the previous frame (issued before the PDL wait)
             mbar_expect_tx(&bars[0], 3u * P * 4u);
             tma_load_3d(Es, &a.tmE, gj0, gi0, 0, &bars[0]);
             mbar_expect_tx(&bars[1], 3u * P * 4u);
             tma_load_3d(Es + 3 * P, &a.tmE, gj0, gi0, 3, &bars[1]);
-            if (a.upd) {
-                mbar_expect_tx(&bars[2], 2u * P * 4u);
-                tma_load_3d(Ys, &a.tmY, gj0, gi0, b, &bars[2]);
-                tma_load_3d(Ds, &a.tmD, gj0, gi0, b, &bars[2]);
-            }
         }
     } else {
         const bool pair = !edgeC && (f.W & 1) == 0;  // both cells contiguous and 8-byte aligned
@@ -405,6 +405,7 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
             }
         }
         cp_async_commit();
+        griddep_wait();  // inputs / state of this frame may come from the preceding kernel
         if (a.upd) {
             if (!edgeC && !edgeR && (f.W & 3) == 0 && (gj0 & 3) == 0) {
                 for (int idx = tid; idx < P / 4; idx += NT) {
@@ -433,8 +434,6 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
     for (int k = 0; k < K; ++k) {
         const size_t gr = (size_t)iclamp(gi0 + r0 + k, 0, f.H - 1) * f.W;
         const size_t ga = gr + iclamp(gj0 + c0, 0, f.W - 1), gb = gr + iclamp(gj0 + c0 + 1, 0, f.W - 1);
-        f0[k] = a.fin[plane + ga];
-        f1[k] = a.fin[plane + gb];
         const float4 sa = __ldg(a.G0 + ga), sb = __ldg(a.G0 + gb);
         s0x[k] = sa.x;
         s0y[k] = sa.y;
@@ -444,6 +443,24 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
         s1z[k] = sb.z;
         mx[k] = 0.0f;
     }
+    // ---- programmatic dependent launch: everything above is frame-invariant geometry; the state
+    // and the frame's inputs may be written by the preceding kernel in the stream
+    if (a.tma) {
+        griddep_wait();
+        if (tid == 0 && a.upd) {
+            mbar_expect_tx(&bars[2], 2u * P * 4u);
+            tma_load_3d(Ys, &a.tmY, gj0, gi0, b, &bars[2]);
+            tma_load_3d(Ds, &a.tmD, gj0, gi0, b, &bars[2]);
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        const size_t gr = (size_t)iclamp(gi0 + r0 + k, 0, f.H - 1) * f.W;
+        const size_t ga = gr + iclamp(gj0 + c0, 0, f.W - 1), gb = gr + iclamp(gj0 + c0 + 1, 0, f.W - 1);
+        f0[k] = a.fin[plane + ga];
+        f1[k] = a.fin[plane + gb];
+    }
+    griddep_launch_dependents();  // the next frame's CTAs may start their geometry loads
     if (a.tma) {
         mbar_wait(&bars[0], 0);
         mbar_wait(&bars[1], 0);
@@ -468,6 +485,7 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
         cp_async_wait<1>();  // own e cells landed (each thread reads only what it copied until the 1st barrier)
     }
 
+    if (!(a.dbg_skip & 1))
     transport_passes<K, NWY, RULE, CLAMP>(f, a.M, f0, f1, s0x, s0y, s0z, s1x, s1y, s1z, mx, Es, XR0, lane, wy, cmin,
                                           cmax, rmin, rmax);
     const float U = f.U;
@@ -489,7 +507,7 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
         }
     }
 
-    if (!a.upd) {  // intermediate launch: store the partial prediction of the tile
+    if (!a.upd || (a.dbg_skip & 2)) {  // intermediate launch: store the partial prediction of the tile
 #pragma unroll
         for (int k = 0; k < K; ++k) {
             const int r = r0 + k;
@@ -743,6 +761,10 @@ cudaError_t launch_cfg(sf_ctx* c, const float* Y, const float* D) {
     for (int l = 0; l < p.launches; ++l) {
         const bool upd = l == p.launches - 1;
         FusedArgs a;
+        {
+            const char* dbg = getenv("SF_DEBUG_SKIP");
+            a.dbg_skip = dbg ? atoi(dbg) : 0;
+        }
         a.tma = getenv("SF_NO_TMA") == nullptr && encode3d(&a.tmE, c->E, f.W, f.H, 6, FC::RW, FC::RH, 3) &&
                 encode3d(&a.tmY, Y, f.W, f.H, f.B, FC::RW, FC::RH, 1) &&
                 encode3d(&a.tmD, D, f.W, f.H, f.B, FC::RW, FC::RH, 1);
@@ -765,18 +787,21 @@ cudaError_t launch_cfg(sf_ctx* c, const float* Y, const float* D) {
         a.TW = FC::RW - 2 * a.R;
         a.TH = FC::RH - 2 * a.R;
         const dim3 grid((f.W + a.TW - 1) / a.TW, (f.H + a.TH - 1) / a.TH, f.B);
-        if (f.rule == SF_DOM_PRINTED) {
-            if (f.clamp)
-                k_fused<K, NWY, SF_DOM_PRINTED, true><<<grid, FC::NT, FC::SMEM, c->stream>>>(a);
-            else
-                k_fused<K, NWY, SF_DOM_PRINTED, false><<<grid, FC::NT, FC::SMEM, c->stream>>>(a);
-        } else {
-            if (f.clamp)
-                k_fused<K, NWY, SF_DOM_LARGEST, true><<<grid, FC::NT, FC::SMEM, c->stream>>>(a);
-            else
-                k_fused<K, NWY, SF_DOM_LARGEST, false><<<grid, FC::NT, FC::SMEM, c->stream>>>(a);
-        }
-        cudaError_t e = cudaGetLastError();
+        void (*kern)(FusedArgs) = f.rule == SF_DOM_PRINTED
+                                      ? (f.clamp ? k_fused<K, NWY, SF_DOM_PRINTED, true> : k_fused<K, NWY, SF_DOM_PRINTED, false>)
+                                      : (f.clamp ? k_fused<K, NWY, SF_DOM_LARGEST, true> : k_fused<K, NWY, SF_DOM_LARGEST, false>);
+        cudaLaunchConfig_t lc = {};
+        lc.gridDim = grid;
+        lc.blockDim = dim3(FC::NT);
+        lc.dynamicSmemBytes = FC::SMEM;
+        lc.stream = c->stream;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL
+        at[0].val.programmaticStreamSerializationAllowed = getenv("SF_NO_PDL") ? 0 : 1;
+        lc.attrs = at;
+        lc.numAttrs = 1;
+        cudaError_t e = cudaLaunchKernelEx(&lc, kern, a);
+        if (e == cudaSuccess) e = cudaGetLastError();
         if (e != cudaSuccess) return e;
         src = a.fout;
     }
