@@ -9,8 +9,8 @@ N > 1 (torchrun, one process per GPU): each rank runs its own independent sequen
 data-path collective ("weak" scaling; value = frames of all ranks / max-over-ranks time).
 
 Inputs: a ring of R distinct frames resident in HBM (R x 2 MiB > the 126 MB L2), so each
-step reads cold brightness/depth; steps are replayed from per-frame CUDA graphs captured on
-the context stream.  Timing: CUDA events on that stream, barrier + synchronize on both
+step reads cold brightness/depth; steps are replayed from CUDA graphs of 8 consecutive steps
+captured on the context stream.  Timing: CUDA events on that stream, barrier + synchronize on both
 sides, max over ranks.  --impl reference times the float32 CPU oracle (the only other
 place this file runs oracle/), see DESIGN.md section 9.
 """
@@ -225,29 +225,40 @@ def run_sf(args):
         for k in range(1, ring):  # one real pass over the ring before capture (untimed)
             m.step(Yd[k], Dd[k])
     s.synchronize()
-    # CUDA graphs per (frame, state parity): a captured step reads state[p] and writes
-    # state[1-p]; replays pick the graph of the current parity
-    graphs = [[None, None] for _ in range(ring)]
-    par = 0  # parity relative to the state at capture start
-    for k in range(ring):
-        for _ in range(2):
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g, stream=s):
+    # CUDA graphs of CHUNK consecutive steps of the palindrome (an even count, so a chunk starts
+    # and ends at the same state parity); the cycle of 2R steps is split into 2R / CHUNK graphs
+    # replayed in order.  Steps beyond a multiple of CHUNK are direct sf_step calls.
+    CHUNK = 8
+    cycle = 2 * ring
+    pos0 = ring  # palindrome position after the untimed pass over the ring
+    chunks = []
+    for c in range(cycle // CHUNK):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            for t in range(CHUNK):
+                k = frame_of(pos0 + c * CHUNK + t)
                 m.step(Yd[k], Dd[k])
-            graphs[k][par] = g
-            par ^= 1
+        chunks.append(g)
     launches = m.launches_per_step
-    state = {"par": 0, "i": ring}  # the device state sits at parity 0; continue the palindrome
+    state = {"i": pos0}
 
-    def replay():
-        k = frame_of(state["i"])
-        graphs[k][state["par"]].replay()
-        state["par"] ^= 1
-        state["i"] += 1
+    def run_steps(n):
+        """n steps continuing the palindrome: whole chunks as graph replays, the rest direct."""
+        while n > 0:
+            off = state["i"] - pos0
+            if n >= CHUNK and off % CHUNK == 0:
+                chunks[(off // CHUNK) % len(chunks)].replay()
+                state["i"] += CHUNK
+                n -= CHUNK
+            else:
+                k = frame_of(state["i"])
+                m.step(Yd[k], Dd[k])
+                state["i"] += 1
+                n -= 1
 
+    args.warmup += (-args.warmup) % CHUNK  # end the warm-up on a chunk boundary (reported as run)
     with torch.cuda.stream(s):
-        for i in range(args.warmup):
-            replay()
+        run_steps(args.warmup)
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
@@ -256,19 +267,22 @@ def run_sf(args):
     if rank == 0:
         clk, clk_path = start_clock_sampler(local)
         time.sleep(0.3)
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    nchunk = args.steps // CHUNK
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(nchunk + 2)]
     with torch.cuda.stream(s):
         ev[0].record(s)
-        for i in range(args.steps):
-            replay()
+        for i in range(nchunk):
+            run_steps(CHUNK)
             ev[i + 1].record(s)
+        run_steps(args.steps - nchunk * CHUNK)
+        ev[-1].record(s)
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
     clocks = stop_clock_sampler(clk, clk_path) if rank == 0 else None
     total_ms = ev[0].elapsed_time(ev[-1])
-    step_ms = [ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps)]
+    step_ms = [ev[i].elapsed_time(ev[i + 1]) / CHUNK for i in range(nchunk)] or [total_ms / args.steps]
     t = torch.tensor([total_ms], device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -327,7 +341,7 @@ def run_sf(args):
                "config": {"workload": CONFIG_NAMES[cid], "batch_per_gpu": B, "H": H, "W": W, "N": params.N,
                           "S": params.smooth_iters, "parallelism": f"independent sequences x{world}",
                           "inputs": f"ring of {ring} frames ({ring * 2 * frame_bytes / 2**20:.0f} MiB) > L2, "
-                                    "replayed palindromically, cold reads each step; per-frame CUDA graphs",
+                                    "replayed palindromically, cold reads each step; CUDA graphs of 8 steps",
                           "kernel": {sf.SF_KERNEL_FUSED: "fused", sf.SF_KERNEL_PASSES: "passes"}.get(m.kernel)},
                "roofline": roof, "gpu_launches": launches * args.steps, "step_ms_median": med_ms,
                "e2e": {"value": e2e_value, "unit": "Hz", "h2d_bytes_per_step": 2 * frame_bytes,

@@ -137,7 +137,8 @@ struct FusedArgs {
     CUtensorMap tmY;    // [B][H][W] brightness, box 64 x 72 x 1
     CUtensorMap tmD;    // [B][H][W] depth, box 64 x 72 x 1
     int tma;            // 1: stage e / Y / depth with TMA (needs W % 4 == 0, 16-byte aligned bases)
-    int dbg_skip;       // timing experiments only (SF_DEBUG_SKIP): 1 = skip transport, 2 = skip update
+    int dbg_skip;       // timing experiments only (SF_DEBUG_SKIP): 1 = skip transport, 2 = skip update,
+                        // 4 = no e TMA, 8 = no Y/depth TMA, 16 = no field / s loads, 32 = exit at entry
     const float4* fin;  // fields at launch start (state k or a partial prediction)
     const float4* sk;   // state k (rho^k for the update)
     float4* fout;       // state k+1 (upd) or partial prediction
@@ -368,6 +369,7 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
     const bool edgeR = rmin > 0 || rmax < RH - 1;
     const size_t HW = (size_t)f.H * f.W, plane = (size_t)b * HW;
 
+    if (a.dbg_skip & 32) return;
     // ---------------- staging: e1 / e2 planes (transport), Y and depth (update)
     uint64_t* const bars = reinterpret_cast<uint64_t*>(sm + 8 * P + C::XRF);
     if (a.tma) {
@@ -380,7 +382,7 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
             asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
         }
         __syncthreads();
-        if (tid == 0) {  // geometry: independent of the previous frame (issued before the PDL wait)
+        if (tid == 0 && !(a.dbg_skip & 4)) {  // geometry: independent of the previous frame
             mbar_expect_tx(&bars[0], 3u * P * 4u);
             tma_load_3d(Es, &a.tmE, gj0, gi0, 0, &bars[0]);
             mbar_expect_tx(&bars[1], 3u * P * 4u);
@@ -434,7 +436,8 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
     for (int k = 0; k < K; ++k) {
         const size_t gr = (size_t)iclamp(gi0 + r0 + k, 0, f.H - 1) * f.W;
         const size_t ga = gr + iclamp(gj0 + c0, 0, f.W - 1), gb = gr + iclamp(gj0 + c0 + 1, 0, f.W - 1);
-        const float4 sa = __ldg(a.G0 + ga), sb = __ldg(a.G0 + gb);
+        const float4 sa = (a.dbg_skip & 16) ? make_float4(0, 0, 1, 0) : __ldg(a.G0 + ga);
+        const float4 sb = (a.dbg_skip & 16) ? make_float4(0, 0, 1, 0) : __ldg(a.G0 + gb);
         s0x[k] = sa.x;
         s0y[k] = sa.y;
         s0z[k] = sa.z;
@@ -447,7 +450,7 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
     // and the frame's inputs may be written by the preceding kernel in the stream
     if (a.tma) {
         griddep_wait();
-        if (tid == 0 && a.upd) {
+        if (tid == 0 && a.upd && !(a.dbg_skip & 8)) {
             mbar_expect_tx(&bars[2], 2u * P * 4u);
             tma_load_3d(Ys, &a.tmY, gj0, gi0, b, &bars[2]);
             tma_load_3d(Ds, &a.tmD, gj0, gi0, b, &bars[2]);
@@ -457,11 +460,11 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
     for (int k = 0; k < K; ++k) {
         const size_t gr = (size_t)iclamp(gi0 + r0 + k, 0, f.H - 1) * f.W;
         const size_t ga = gr + iclamp(gj0 + c0, 0, f.W - 1), gb = gr + iclamp(gj0 + c0 + 1, 0, f.W - 1);
-        f0[k] = a.fin[plane + ga];
-        f1[k] = a.fin[plane + gb];
+        f0[k] = (a.dbg_skip & 16) ? make_float4(0, 0, 0, 0.5f) : a.fin[plane + ga];
+        f1[k] = (a.dbg_skip & 16) ? make_float4(0, 0, 0, 0.5f) : a.fin[plane + gb];
     }
     griddep_launch_dependents();  // the next frame's CTAs may start their geometry loads
-    if (a.tma) {
+    if (a.tma && !(a.dbg_skip & 4)) {
         mbar_wait(&bars[0], 0);
         mbar_wait(&bars[1], 0);
         if (edgeC || edgeR) {  // replica cells next to grid edges take the edge cell's e (reading 10)
@@ -534,7 +537,7 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
             *reinterpret_cast<float2*>(Fz + ib) = make_float2(f0[k].z, f1[k].z);
             *reinterpret_cast<float2*>(Fw + ib) = make_float2(f0[k].w, f1[k].w);
         }
-        if (a.tma) {
+        if (a.tma && !(a.dbg_skip & 8)) {
             mbar_wait(&bars[2], 0);
             if (edgeC || edgeR) {  // out-of-grid cells of Y / depth take their clamped cell's value
                 __syncthreads();
