@@ -138,7 +138,8 @@ struct FusedArgs {
     CUtensorMap tmD;    // [B][H][W] depth, box 64 x 72 x 1
     int tma;            // 1: stage e / Y / depth with TMA (needs W % 4 == 0, 16-byte aligned bases)
     int dbg_skip;       // timing experiments only (SF_DEBUG_SKIP): 1 = skip transport, 2 = skip update,
-                        // 4 = no e TMA, 8 = no Y/depth TMA, 16 = no field / s loads, 32 = exit at entry
+                        // 4 = no e TMA, 8 = no Y/depth TMA, 16 = no field / s loads, 32 = exit at entry,
+                        // 64 = no column passes, 128 = no row passes
     const float4* fin;  // fields at launch start (state k or a partial prediction)
     const float4* sk;   // state k (rho^k for the update)
     float4* fout;       // state k+1 (upd) or partial prediction
@@ -180,7 +181,7 @@ __device__ __forceinline__ void transport_passes(const FrameParams& f, int M, fl
                                                  const float (&s0x)[K], const float (&s0y)[K], const float (&s0z)[K],
                                                  const float (&s1x)[K], const float (&s1y)[K], const float (&s1z)[K],
                                                  float (&mx)[K], const float* Es, float4* XR0, int lane, int wy,
-                                                 int cmin, int cmax, int rmin, int rmax) {
+                                                 int cmin, int cmax, int rmin, int rmax, int dbg) {
     using C = Cfg<K, NWY>;
     constexpr int RW = C::RW, RH = C::RH, P = C::P;
     const int c0 = 2 * lane, r0 = K * wy;
@@ -196,6 +197,7 @@ __device__ __forceinline__ void transport_passes(const FrameParams& f, int M, fl
 
     for (int n = 0; n < M; ++n) {
         // ================= column pass (beta_1): registers + shuffles only
+        if (!(dbg & 64))
 #pragma unroll
         for (int k = 0; k < K; ++k) {
             const int ib = (r0 + k) * RW + c0;
@@ -269,7 +271,7 @@ __device__ __forceinline__ void transport_passes(const FrameParams& f, int M, fl
             }
         }
         // ================= row pass (beta_2, reading 3)
-        {
+        if (!(dbg & 128)) {
             float4* const XR = XR0 + (n & 1) * C::XR;
             XR[(wy * 2 + 0) * RW + c0] = f0[0];
             XR[(wy * 2 + 0) * RW + c0 + 1] = f1[0];
@@ -284,6 +286,44 @@ __device__ __forceinline__ void transport_passes(const FrameParams& f, int M, fl
                 const float2 ez = *reinterpret_cast<const float2*>(Es + 5 * P + ib);
                 v0[k] = dot3s(ex.x, ey.x, ez.x, f0[k]);
                 v1[k] = dot3s(ex.y, ey.y, ez.y, f1[k]);
+            }
+            // one row of the row pass for both cells: neighbours (vm, fm) above and (vp, fp) below
+            auto row_update = [&](int k, float vm0, float vm1, const float4& fm0, const float4& fm1, float vp0,
+                                  float vp1, const float4& fp0, const float4& fp1, float4& m0, float4& m1) {
+                float vh0 = dominant(vm0, vp0, RULE);
+                float vh1 = dominant(vm1, vp1, RULE);
+                mx[k] = fmaxf(mx[k], fmaxf(fabsf(vh0), in1 ? fabsf(vh1) : 0.0f));
+                if (CLAMP) {
+                    vh0 = fminf(fmaxf(vh0, -U), U);
+                    vh1 = fminf(fmaxf(vh1, -U), U);
+                }
+                const float4 fu0 = sel4(vh0 > 0.0f, fm0, fp0);
+                const float4 fu1 = sel4(vh1 > 0.0f, fm1, fp1);
+                const float q0 = xmul(f.sigma, dot3s(s0x[k], s0y[k], s0z[k], f0[k]));
+                const float q1 = xmul(f.sigma, dot3s(s1x[k], s1y[k], s1z[k], f1[k]));
+                m0 = transport(f0[k], fu0, fabsf(vh0), q0, ndt);
+                m1 = transport(f1[k], fu1, fabsf(vh1), q1, ndt);
+            };
+            // interior rows 1..K-2 need no exchanged value: compute them before the barrier (new
+            // values written back one row late so rows k-1, k, k+1 are pre-pass; the pre-pass rows 1
+            // and K-2 that the run ends need are kept aside)
+            const float4 o10 = f0[1], o11 = f1[1], oK0 = f0[K - 2], oK1 = f1[K - 2];
+            {
+                float4 n0, n1;
+#pragma unroll
+                for (int k = 1; k <= K - 2; ++k) {
+                    float4 m0, m1;
+                    row_update(k, v0[k - 1], v1[k - 1], f0[k - 1], f1[k - 1], v0[k + 1], v1[k + 1], f0[k + 1],
+                               f1[k + 1], m0, m1);
+                    if (k > 1) {
+                        f0[k - 1] = n0;
+                        f1[k - 1] = n1;
+                    }
+                    n0 = m0;
+                    n1 = m1;
+                }
+                f0[K - 2] = n0;
+                f1[K - 2] = n1;
             }
             __syncthreads();
             float4 t0 = f0[0], t1 = f1[0], b0 = f0[K - 1], b1 = f1[K - 1];
@@ -309,36 +349,15 @@ __device__ __forceinline__ void transport_passes(const FrameParams& f, int M, fl
                 vb0 = dot3s(ex.x, ey.x, ez.x, b0);
                 vb1 = dot3s(ex.y, ey.y, ez.y, b1);
             }
-            // new values are written back one row late, so rows k-1, k, k+1 are all pre-pass here
-            float4 n0 = f0[0], n1 = f1[0];
-#pragma unroll
-            for (int k = 0; k < K; ++k) {
-                const float vm0 = (k > 0) ? v0[k - 1] : vt0, vm1 = (k > 0) ? v1[k - 1] : vt1;
-                const float vp0 = (k < K - 1) ? v0[k + 1] : vb0, vp1 = (k < K - 1) ? v1[k + 1] : vb1;
-                const float4 fm0 = (k > 0) ? f0[k - 1] : t0, fm1 = (k > 0) ? f1[k - 1] : t1;
-                const float4 fp0 = (k < K - 1) ? f0[k + 1] : b0, fp1 = (k < K - 1) ? f1[k + 1] : b1;
-                float vh0 = dominant(vm0, vp0, RULE);
-                float vh1 = dominant(vm1, vp1, RULE);
-                mx[k] = fmaxf(mx[k], fmaxf(fabsf(vh0), in1 ? fabsf(vh1) : 0.0f));
-                if (CLAMP) {
-                    vh0 = fminf(fmaxf(vh0, -U), U);
-                    vh1 = fminf(fmaxf(vh1, -U), U);
-                }
-                const float4 fu0 = sel4(vh0 > 0.0f, fm0, fp0);
-                const float4 fu1 = sel4(vh1 > 0.0f, fm1, fp1);
-                const float q0 = xmul(f.sigma, dot3s(s0x[k], s0y[k], s0z[k], f0[k]));
-                const float q1 = xmul(f.sigma, dot3s(s1x[k], s1y[k], s1z[k], f1[k]));
-                const float4 m0 = transport(f0[k], fu0, fabsf(vh0), q0, ndt);
-                const float4 m1 = transport(f1[k], fu1, fabsf(vh1), q1, ndt);
-                if (k > 0) {
-                    f0[k - 1] = n0;
-                    f1[k - 1] = n1;
-                }
-                n0 = m0;
-                n1 = m1;
+            {
+                float4 m0, m1, q0, q1;
+                row_update(0, vt0, vt1, t0, t1, v0[1], v1[1], o10, o11, m0, m1);
+                row_update(K - 1, v0[K - 2], v1[K - 2], oK0, oK1, vb0, vb1, b0, b1, q0, q1);
+                f0[0] = m0;
+                f1[0] = m1;
+                f0[K - 1] = q0;
+                f1[K - 1] = q1;
             }
-            f0[K - 1] = n0;
-            f1[K - 1] = n1;
         }
         // (row passes keep column replicas valid; the next column pass keeps row replicas as
         //  they are and they are refreshed again before the next row pass)
@@ -490,7 +509,7 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
 
     if (!(a.dbg_skip & 1))
     transport_passes<K, NWY, RULE, CLAMP>(f, a.M, f0, f1, s0x, s0y, s0z, s1x, s1y, s1z, mx, Es, XR0, lane, wy, cmin,
-                                          cmax, rmin, rmax);
+                                          cmax, rmin, rmax, a.dbg_skip);
     const float U = f.U;
 
     // ---------------- flags from tile cells (exact at every pass); |u_hat| before the clamp
