@@ -641,43 +641,65 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
         float* const Tx = Ys;
         float* const Ty = Ds;
         float* const Tz = HG;
+        // Two adjacent cells per thread (8-byte shared loads).  In edge CTAs the out-of-grid cells of
+        // the w planes are first set to their clamped in-grid cell (replicate border, reading 10),
+        // so both passes read plain neighbours.
         const bool edge = edgeC || edgeR;
         for (int it = 0; it < S; ++it) {
             // output of this pass: tile + 2(S-1-it); its horizontal sums are needed 2 rows further
             const int m = 2 * (S - 1 - it);
             const int or0 = max(R - m, rmin), or1 = min(R + TH + m - 1, rmax);
-            const int oc0 = max(R - m, cmin), oc1 = min(R + TW + m - 1, cmax);
-            const int hr0 = max(or0 - 2, rmin), hr1 = min(or1 + 2, rmax);
+            const int oc0 = max(R - m, cmin);  // even
+            int oc1 = min(R + TW + m - 1, cmax);
+            if ((oc1 - oc0 + 1) & 1) ++oc1;    // whole pairs (the extra column is a replica)
+            const int hr0 = or0 - 2, hr1 = or1 + 2;
             __syncthreads();
+            if (edge) {
 #pragma unroll 1
-            SF_FOR_RECT(r, c, hr0, hr1, oc0, oc1, NT, tid) {
-                const int idx = r * RW + c;
-                int j0 = idx - 2, j1 = idx - 1, j3 = idx + 1, j4 = idx + 2;
-                if (edge) {
-                    const int rb = r * RW;
-                    j0 = rb + max(c - 2, cmin);
-                    j1 = rb + max(c - 1, cmin);
-                    j3 = rb + min(c + 1, cmax);
-                    j4 = rb + min(c + 2, cmax);
+                SF_FOR_RECT(r, c, hr0, hr1, oc0 - 2, oc1 + 2, NT, tid) {
+                    const int rc = iclamp(r, rmin, rmax), cc = iclamp(c, cmin, cmax);
+                    if (rc != r || cc != c) {
+                        const int src = rc * RW + cc, dst = r * RW + c;
+                        Fx[dst] = Fx[src];
+                        Fy[dst] = Fy[src];
+                        Fz[dst] = Fz[src];
+                    }
                 }
-                Tx[idx] = xadd(xadd(xadd(xadd(Fx[j0], Fx[j1]), Fx[idx]), Fx[j3]), Fx[j4]);
-                Ty[idx] = xadd(xadd(xadd(xadd(Fy[j0], Fy[j1]), Fy[idx]), Fy[j3]), Fy[j4]);
-                Tz[idx] = xadd(xadd(xadd(xadd(Fz[j0], Fz[j1]), Fz[idx]), Fz[j3]), Fz[j4]);
+                __syncthreads();
+            }
+            const int np = (oc1 - oc0 + 1) / 2;
+#pragma unroll 1
+            SF_FOR_RECT(r, pc, hr0, hr1, 0, np - 1, NT, tid) {
+                const int idx = r * RW + oc0 + 2 * pc;
+                const float* Pl[3] = {Fx, Fy, Fz};
+                float* Tl[3] = {Tx, Ty, Tz};
+#pragma unroll
+                for (int q = 0; q < 3; ++q) {
+                    const float2 x0 = *reinterpret_cast<const float2*>(Pl[q] + idx - 2);
+                    const float2 x1 = *reinterpret_cast<const float2*>(Pl[q] + idx);
+                    const float2 x2 = *reinterpret_cast<const float2*>(Pl[q] + idx + 2);
+                    *reinterpret_cast<float2*>(Tl[q] + idx) =
+                        make_float2(xadd(xadd(xadd(xadd(x0.x, x0.y), x1.x), x1.y), x2.x),
+                                    xadd(xadd(xadd(xadd(x0.y, x1.x), x1.y), x2.x), x2.y));
+                }
             }
             __syncthreads();
 #pragma unroll 1
-            SF_FOR_RECT(r, c, or0, or1, oc0, oc1, NT, tid) {
-                const int idx = r * RW + c;
-                int i0 = idx - 2 * RW, i1 = idx - RW, i3 = idx + RW, i4 = idx + 2 * RW;
-                if (edge) {
-                    i0 = max(r - 2, rmin) * RW + c;
-                    i1 = max(r - 1, rmin) * RW + c;
-                    i3 = min(r + 1, rmax) * RW + c;
-                    i4 = min(r + 2, rmax) * RW + c;
+            SF_FOR_RECT(r, pc, or0, or1, 0, np - 1, NT, tid) {
+                const int idx = r * RW + oc0 + 2 * pc;
+                const float* Tl[3] = {Tx, Ty, Tz};
+                float* Pl[3] = {Fx, Fy, Fz};
+#pragma unroll
+                for (int q = 0; q < 3; ++q) {
+                    const float2 y0 = *reinterpret_cast<const float2*>(Tl[q] + idx - 2 * RW);
+                    const float2 y1 = *reinterpret_cast<const float2*>(Tl[q] + idx - RW);
+                    const float2 y2 = *reinterpret_cast<const float2*>(Tl[q] + idx);
+                    const float2 y3 = *reinterpret_cast<const float2*>(Tl[q] + idx + RW);
+                    const float2 y4 = *reinterpret_cast<const float2*>(Tl[q] + idx + 2 * RW);
+                    *reinterpret_cast<float2*>(Pl[q] + idx) =
+                        make_float2(__fdiv_rn(xadd(xadd(xadd(xadd(y0.x, y1.x), y2.x), y3.x), y4.x), 25.0f),
+                                    __fdiv_rn(xadd(xadd(xadd(xadd(y0.y, y1.y), y2.y), y3.y), y4.y), 25.0f));
                 }
-                Fx[idx] = __fdiv_rn(xadd(xadd(xadd(xadd(Tx[i0], Tx[i1]), Tx[idx]), Tx[i3]), Tx[i4]), 25.0f);
-                Fy[idx] = __fdiv_rn(xadd(xadd(xadd(xadd(Ty[i0], Ty[i1]), Ty[idx]), Ty[i3]), Ty[i4]), 25.0f);
-                Fz[idx] = __fdiv_rn(xadd(xadd(xadd(xadd(Tz[i0], Tz[i1]), Tz[idx]), Tz[i3]), Tz[i4]), 25.0f);
             }
         }
         __syncthreads();
