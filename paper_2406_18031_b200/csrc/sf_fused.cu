@@ -22,6 +22,7 @@
 //     the 3x3 LDL^T solve and S box passes on shared planes, then fuses rho and stores.
 // The transport update of the 4 fields uses paired f32x2 ops (FADD2/FMUL2/FFMA2).
 #include <cuda.h>
+#include <stdio.h>
 #include <stdlib.h>
 
 #include "sf_internal.cuh"
@@ -139,7 +140,7 @@ struct FusedArgs {
     int tma;            // 1: stage e / Y / depth with TMA (needs W % 4 == 0, 16-byte aligned bases)
     int dbg_skip;       // timing experiments only (SF_DEBUG_SKIP): 1 = skip transport, 2 = skip update,
                         // 4 = no e TMA, 8 = no Y/depth TMA, 16 = no field / s loads, 32 = exit at entry,
-                        // 64 = no column passes, 128 = no row passes
+                        // 64 = no column passes, 128 = no row passes, 256 = print phase clocks of CTA (6,5)
     const float4* fin;  // fields at launch start (state k or a partial prediction)
     const float4* sk;   // state k (rho^k for the update)
     float4* fout;       // state k+1 (upd) or partial prediction
@@ -165,7 +166,7 @@ struct Cfg {
     static constexpr int XR = NWY * 2 * RW;  // float4 slots of one row-exchange buffer
     // smem floats: E planes 6P | Ys P | Ds/Rs P | XR buffers 2 x 4 XR (>= 2P for HG/HH, and
     // Ys..end >= 3P for the box planes)
-    static constexpr int XRF = 2 * 4 * XR > 2 * P ? 2 * 4 * XR : 2 * P;
+    static constexpr int XRF = 2 * 4 * XR > 4 * P ? 2 * 4 * XR : 4 * P;  // row buffers | HG HH Fy Fz
     static constexpr size_t SMEM = sizeof(float) * (8 * (size_t)P + XRF) + 64;  // + mbarriers
 };
 
@@ -389,6 +390,11 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
     const size_t HW = (size_t)f.H * f.W, plane = (size_t)b * HW;
 
     if (a.dbg_skip & 32) return;
+    long long T_[10];
+    int nT_ = 0;
+    const bool tim = (a.dbg_skip & 256) && blockIdx.x == 6 && blockIdx.y == 5 && blockIdx.z == 0;
+#define SF_TICK() do { if (tim) { __syncthreads(); if (tid == 0) T_[nT_] = clock64(); ++nT_; } } while (0)
+    SF_TICK();
     // ---------------- staging: e1 / e2 planes (transport), Y and depth (update)
     uint64_t* const bars = reinterpret_cast<uint64_t*>(sm + 8 * P + C::XRF);
     if (a.tma) {
@@ -483,6 +489,7 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
         f1[k] = (a.dbg_skip & 16) ? make_float4(0, 0, 0, 0.5f) : a.fin[plane + gb];
     }
     griddep_launch_dependents();  // the next frame's CTAs may start their geometry loads
+    SF_TICK();
     if (a.tma && !(a.dbg_skip & 4)) {
         mbar_wait(&bars[0], 0);
         mbar_wait(&bars[1], 0);
@@ -529,6 +536,7 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
         }
     }
 
+    SF_TICK();
     if (!a.upd || (a.dbg_skip & 2)) {  // intermediate launch: store the partial prediction of the tile
 #pragma unroll
         for (int k = 0; k < K; ++k) {
@@ -541,21 +549,13 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
         }
     } else {
         // =========================== update (U1-U5) on shared planes, compact runtime loops
-        float* const Fx = sm;  // w^{k+}, rho^{k+} -> w_LS, rho^{k+1} (in place)
-        float* const Fy = sm + P;
-        float* const Fz = sm + 2 * P;
-        float* const Fw = sm + 3 * P;
-        float* const HG = sm + 4 * P;
-        float* const HH = sm + 5 * P;
-        __syncthreads();  // e planes and row buffers are dead from here on
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-            const int ib = (r0 + k) * RW + c0;
-            *reinterpret_cast<float2*>(Fx + ib) = make_float2(f0[k].x, f1[k].x);
-            *reinterpret_cast<float2*>(Fy + ib) = make_float2(f0[k].y, f1[k].y);
-            *reinterpret_cast<float2*>(Fz + ib) = make_float2(f0[k].z, f1[k].z);
-            *reinterpret_cast<float2*>(Fw + ib) = make_float2(f0[k].w, f1[k].w);
-        }
+        // planes: E (e1, e2) stay until the solve; HG, HH, Fy, Fz take the row-buffer region; Fx takes
+        // Y's plane once the brightness taps are done; rhohat replaces depth and lives to the end
+        float* const HG = Xb;
+        float* const HH = Xb + P;
+        float* const Fx = Ys;  // w^{k+} -> w_LS -> smoothed w (in place)
+        float* const Fy = Xb + 2 * P;
+        float* const Fz = Xb + 3 * P;
         if (a.tma && !(a.dbg_skip & 8)) {
             mbar_wait(&bars[2], 0);
             if (edgeC || edgeR) {  // out-of-grid cells of Y / depth take their clamped cell's value
@@ -572,15 +572,16 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
         } else {
             cp_async_wait<0>();
         }
-        __syncthreads();
+        __syncthreads();  // Y / depth complete; row buffers dead
         const float qnan = __int_as_float(0x7fffffff);
+        SF_TICK();
         const int S = f.S;
         // solve region = tile + 2S (clipped to the grid); models needed on it +-2 rows, +-1 cols
         const int rlo = max(R - 2 * S, rmin), rhi = min(R + TH + 2 * S - 1, rmax);
         const int clo = max(R - 2 * S, cmin), chi = min(R + TW + 2 * S - 1, cmax);
         {
             // rhohat plane + horizontal brightness taps on the solve region +-2 rows, +-1 cols
-#pragma unroll 1
+#pragma unroll 2
             SF_FOR_RECT(r, c, rlo - 2, rhi + 2, clo - 1, chi + 1, NT, tid) {
                 const int idx = r * RW + c;
                 const float d = Ds[idx];
@@ -593,9 +594,18 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
                     fl |= SF_FLAG_NONFINITE;
             }
         }
+        __syncthreads();  // Y plane dead: w^{k+} goes to the F planes
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const int ib = (r0 + k) * RW + c0;
+            *reinterpret_cast<float2*>(Fx + ib) = make_float2(f0[k].x, f1[k].x);
+            *reinterpret_cast<float2*>(Fy + ib) = make_float2(f0[k].y, f1[k].y);
+            *reinterpret_cast<float2*>(Fz + ib) = make_float2(f0[k].z, f1[k].z);
+        }
         __syncthreads();
+        SF_TICK();
 #pragma unroll 2
-        SF_FOR_RECT(r, c, rlo, rhi, clo, chi, NT, tid) {  // per-pixel LS (eq:LS_update) + fusion, solve region
+        SF_FOR_RECT(r, c, rlo, rhi, clo, chi, NT, tid) {  // per-pixel LS (eq:LS_update), solve region
             const int idx = r * RW + c;
             const float g0 = HG[idx - 2 * RW], g1 = HG[idx - RW], g2 = HG[idx], g3 = HG[idx + RW], g4 = HG[idx + 2 * RW];
             const float h0 = HH[idx - 2 * RW], h1 = HH[idx - RW], h2 = HH[idx], h3 = HH[idx + RW], h4 = HH[idx + 2 * RW];
@@ -609,9 +619,10 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
             const float br2 = pick_side(rh, vc, ru, vu, rd, vd);  // eq:dominant_b2
             const size_t g = (size_t)(gi0 + r) * f.W + (gj0 + c);
             const float4 s4 = __ldg(a.G0 + g);
-            const float4 e1 = __ldg(a.G1 + g), e2 = __ldg(a.G2 + g);
             const float d2 = s4.w;
-            const float e1a[3] = {e1.x, e1.y, e1.z}, e2a[3] = {e2.x, e2.y, e2.z}, sa[3] = {s4.x, s4.y, s4.z};
+            const float e1a[3] = {Es[idx], Es[P + idx], Es[2 * P + idx]};
+            const float e2a[3] = {Es[3 * P + idx], Es[4 * P + idx], Es[5 * P + idx]};
+            const float sa[3] = {s4.x, s4.y, s4.z};
             float gh[3], m[3];
             const float d2r = xmul(d2, rh);
 #pragma unroll
@@ -620,30 +631,26 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
                 const float dr = xmul(d2, xfma(e2a[q], br2, xmul(e1a[q], br1)));
                 m[q] = xfma(d2r, sa[q], dr);
             }
-            const float cY = xmul(d2, xsub(yh, a.yin[plane + g]));  // eq:img_cost_top
-            const float cr = xmul(d2, xsub(rh, a.sk[plane + g].w));  // eq:invdepth_cost_top
+            const float cY = xmul(d2, xsub(yh, __ldg(a.yin + plane + g)));    // eq:img_cost_top
+            const float cr = xmul(d2, xsub(rh, __ldg(&a.sk[plane + g].w)));  // eq:invdepth_cost_top
             const float wp[3] = {Fx[idx], Fy[idx], Fz[idx]};
-            const float rp = Fw[idx];
             float x[3];
             ls_solve3(gh, m, cY, cr, wp, f.g1, vc ? f.g2 : 0.0f, f.g3, x);
-            const float kap = vc ? f.kappa : 0.0f;
-            const float rn = xfma(kap, xsub(rh, rp), rp);  // fusion
             Fx[idx] = x[0];
             Fy[idx] = x[1];
             Fz[idx] = x[2];
-            Fw[idx] = rn;
-            if (!(isfinite(x[0]) && isfinite(x[1]) && isfinite(x[2]) && isfinite(rn)) && gi0 + r >= f.fr0 &&
-                gi0 + r < f.fr1)
+            if (!(isfinite(x[0]) && isfinite(x[1]) && isfinite(x[2])) && gi0 + r >= f.fr0 && gi0 + r < f.fr1)
                 fl |= SF_FLAG_NONFINITE;
             if (r >= R && r < R + TH && c >= R && c < R + TW) a.yout[plane + g] = yh;
         }
         // ---- S x 5x5 box (reading 13): horizontal 5-sum -> Tq, vertical 5-sum / 25 -> Fq
-        float* const Tx = Ys;
-        float* const Ty = Ds;
-        float* const Tz = HG;
+        float* const Tx = Es;  // e planes are dead after the solve
+        float* const Ty = Es + P;
+        float* const Tz = Es + 2 * P;
         // Two adjacent cells per thread (8-byte shared loads).  In edge CTAs the out-of-grid cells of
         // the w planes are first set to their clamped in-grid cell (replicate border, reading 10),
         // so both passes read plain neighbours.
+        SF_TICK();
         const bool edge = edgeC || edgeR;
         for (int it = 0; it < S; ++it) {
             // output of this pass: tile + 2(S-1-it); its horizontal sums are needed 2 rows further
@@ -703,15 +710,37 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
             }
         }
         __syncthreads();
-        // ---- store the tile: (w^{k+1}, rho^{k+1}), coalesced along rows
-        const int tr0 = max(R, rmin), tr1 = min(R + TH - 1, rmax);
-        const int tc0 = max(R, cmin), tc1 = min(R + TW - 1, cmax);
-#pragma unroll 1
-        SF_FOR_RECT(r, c, tr0, tr1, tc0, tc1, NT, tid) {
-            const int idx = r * RW + c;
-            a.fout[plane + (size_t)(gi0 + r) * f.W + (gj0 + c)] = make_float4(Fx[idx], Fy[idx], Fz[idx], Fw[idx]);
+        SF_TICK();
+        // ---- rho fusion by the threads that hold rho^{k+} in registers, and the store of
+        // the tile (w^{k+1}, rho^{k+1}): two adjacent cells per thread per row, coalesced
+        const float kap = f.kappa;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const int r = r0 + k;
+            if (r >= R && r < R + TH && r >= rmin && r <= rmax && c0 >= R && c0 < R + TW && c0 >= cmin &&
+                c0 <= cmax) {
+                const int idx = r * RW + c0;
+                const float2 wx = *reinterpret_cast<const float2*>(Fx + idx);
+                const float2 wy2 = *reinterpret_cast<const float2*>(Fy + idx);
+                const float2 wz = *reinterpret_cast<const float2*>(Fz + idx);
+                const float2 rh2 = *reinterpret_cast<const float2*>(Ds + idx);
+                const bool v0 = !isnan(rh2.x), v1 = !isnan(rh2.y);
+                const float rn0 = xfma(v0 ? kap : 0.0f, xsub(v0 ? rh2.x : 0.0f, f0[k].w), f0[k].w);
+                const float rn1 = xfma(v1 ? kap : 0.0f, xsub(v1 ? rh2.y : 0.0f, f1[k].w), f1[k].w);
+                if (!(isfinite(rn0) && isfinite(rn1)) && gi0 + r >= f.fr0 && gi0 + r < f.fr1) fl |= SF_FLAG_NONFINITE;
+                const size_t g = plane + (size_t)(gi0 + r) * f.W + (gj0 + c0);
+                a.fout[g] = make_float4(wx.x, wy2.x, wz.x, rn0);
+                if (c0 + 1 <= cmax) a.fout[g + 1] = make_float4(wx.y, wy2.y, wz.y, rn1);
+            }
         }
     }
+    SF_TICK();
+    if (tim && tid == 0) {
+        printf("SFTIME");
+        for (int i = 1; i < nT_; ++i) printf(" %lld", T_[i] - T_[i - 1]);
+        printf("\n");
+    }
+#undef SF_TICK
     const unsigned any = __reduce_or_sync(FULL, fl);
     if (lane == 0 && any) atomicOr(a.flags, any);
 }
