@@ -704,8 +704,8 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
                     const float2 y3 = *reinterpret_cast<const float2*>(Tl[q] + idx + RW);
                     const float2 y4 = *reinterpret_cast<const float2*>(Tl[q] + idx + 2 * RW);
                     *reinterpret_cast<float2*>(Pl[q] + idx) =
-                        make_float2(__fdiv_rn(xadd(xadd(xadd(xadd(y0.x, y1.x), y2.x), y3.x), y4.x), 25.0f),
-                                    __fdiv_rn(xadd(xadd(xadd(xadd(y0.y, y1.y), y2.y), y3.y), y4.y), 25.0f));
+                        make_float2(div25(xadd(xadd(xadd(xadd(y0.x, y1.x), y2.x), y3.x), y4.x)),
+                                    div25(xadd(xadd(xadd(xadd(y0.y, y1.y), y2.y), y3.y), y4.y)));
                 }
             }
         }

@@ -211,9 +211,9 @@ __global__ void __launch_bounds__(BX* BY) k_box_v(const float4* __restrict__ in,
         a.y = xadd(a.y, v.y);
         a.z = xadd(a.z, v.z);
     }
-    a.x = __fdiv_rn(a.x, 25.0f);
-    a.y = __fdiv_rn(a.y, 25.0f);
-    a.z = __fdiv_rn(a.z, 25.0f);
+    a.x = div25(a.x);
+    a.y = div25(a.y);
+    a.z = div25(a.z);
     a.w = pl[(size_t)i * f.W + j].w;
     out[((size_t)b * f.H + i) * f.W + j] = a;
 }
