@@ -39,6 +39,13 @@ __device__ __forceinline__ float2 sub2(float2 a, float2 b) {
         : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
     return d;
 }
+__device__ __forceinline__ float2 add2(float2 a, float2 b) {
+    float2 d;
+    asm("{.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+        "add.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;}"
+        : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+    return d;
+}
 __device__ __forceinline__ float2 mul2(float2 a, float2 b) {
     float2 d;
     asm("{.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
@@ -140,7 +147,8 @@ struct FusedArgs {
     int tma;            // 1: stage e / Y / depth with TMA (needs W % 4 == 0, 16-byte aligned bases)
     int dbg_skip;       // timing experiments only (SF_DEBUG_SKIP): 1 = skip transport, 2 = skip update,
                         // 4 = no e TMA, 8 = no Y/depth TMA, 16 = no field / s loads, 32 = exit at entry,
-                        // 64 = no column passes, 128 = no row passes, 256 = print phase clocks of CTA (6,5)
+                        // 64 = no column passes, 128 = no row passes, 256 = print phase clocks of CTA (6,5),
+                        // 512 = no box passes, 1024 = no solve
     const float4* fin;  // fields at launch start (state k or a partial prediction)
     const float4* sk;   // state k (rho^k for the update)
     float4* fout;       // state k+1 (upd) or partial prediction
@@ -390,7 +398,7 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
     const size_t HW = (size_t)f.H * f.W, plane = (size_t)b * HW;
 
     if (a.dbg_skip & 32) return;
-    long long T_[10];
+    long long T_[16];
     int nT_ = 0;
     const bool tim = (a.dbg_skip & 256) && blockIdx.x == 6 && blockIdx.y == 5 && blockIdx.z == 0;
 #define SF_TICK() do { if (tim) { __syncthreads(); if (tid == 0) T_[nT_] = clock64(); ++nT_; } } while (0)
@@ -605,7 +613,7 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
         __syncthreads();
         SF_TICK();
 #pragma unroll 2
-        SF_FOR_RECT(r, c, rlo, rhi, clo, chi, NT, tid) {  // per-pixel LS (eq:LS_update), solve region
+        SF_FOR_RECT(r, c, rlo, rhi, clo, (a.dbg_skip & 1024) ? clo - 1 : chi, NT, tid) {  // per-pixel LS, solve region
             const int idx = r * RW + c;
             const float g0 = HG[idx - 2 * RW], g1 = HG[idx - RW], g2 = HG[idx], g3 = HG[idx + RW], g4 = HG[idx + 2 * RW];
             const float h0 = HH[idx - 2 * RW], h1 = HH[idx - RW], h2 = HH[idx], h3 = HH[idx + RW], h4 = HH[idx + 2 * RW];
@@ -643,72 +651,107 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
                 fl |= SF_FLAG_NONFINITE;
             if (r >= R && r < R + TH && c >= R && c < R + TW) a.yout[plane + g] = yh;
         }
-        // ---- S x 5x5 box (reading 13): horizontal 5-sum -> Tq, vertical 5-sum / 25 -> Fq
-        float* const Tx = Es;  // e planes are dead after the solve
-        float* const Ty = Es + P;
-        float* const Tz = Es + 2 * P;
-        // Two adjacent cells per thread (8-byte shared loads).  In edge CTAs the out-of-grid cells of
-        // the w planes are first set to their clamped in-grid cell (replicate border, reading 10),
-        // so both passes read plain neighbours.
+        // ---- S x 5x5 box (reading 13) as a register-tiled 2-D stencil: one work item = one
+        // component of a 4 x 4 output block, read as an 8 x 8 window (8-byte shared loads) ->
+        // horizontal 5-sums of 8 rows -> vertical 5-sums -> / 25, both passes in registers; the
+        // passes ping-pong between the F planes and the e planes (dead after the solve).  In edge
+        // CTAs the out-of-grid cells of the input planes are first set to their clamped in-grid cell
+        // (replicate border, reading 10).
         SF_TICK();
         const bool edge = edgeC || edgeR;
-        for (int it = 0; it < S; ++it) {
-            // output of this pass: tile + 2(S-1-it); its horizontal sums are needed 2 rows further
-            const int m = 2 * (S - 1 - it);
+        float* src[3] = {Fx, Fy, Fz};
+        float* dst[3] = {Es, Es + P, Es + 2 * P};
+        for (int it = 0; it < ((a.dbg_skip & 512) ? 0 : S); ++it) {
+            const int m = 2 * (S - 1 - it);  // output of this pass: tile + 2(S-1-it), in the grid
             const int or0 = max(R - m, rmin), or1 = min(R + TH + m - 1, rmax);
-            const int oc0 = max(R - m, cmin);  // even
-            int oc1 = min(R + TW + m - 1, cmax);
-            if ((oc1 - oc0 + 1) & 1) ++oc1;    // whole pairs (the extra column is a replica)
-            const int hr0 = or0 - 2, hr1 = or1 + 2;
+            const int oc0 = max(R - m, cmin), oc1 = min(R + TW + m - 1, cmax);
+            const int bc0 = ((oc0 - 2) & ~3) + 2;  // block windows (c-2 .. c+5) start 16-byte aligned
+            const int nbc = (oc1 - bc0) / 4 + 1, nbr = (or1 - or0) / 4 + 1;
             __syncthreads();
             if (edge) {
 #pragma unroll 1
-                SF_FOR_RECT(r, c, hr0, hr1, oc0 - 2, oc1 + 2, NT, tid) {
+                SF_FOR_RECT(r, c, max(or0 - 2, 0), min(or0 + 4 * nbr + 1, RH - 1), max(bc0 - 2, 0),
+                            min(bc0 + 4 * nbc + 1, RW - 1), NT, tid) {
                     const int rc = iclamp(r, rmin, rmax), cc = iclamp(c, cmin, cmax);
                     if (rc != r || cc != c) {
-                        const int src = rc * RW + cc, dst = r * RW + c;
-                        Fx[dst] = Fx[src];
-                        Fy[dst] = Fy[src];
-                        Fz[dst] = Fz[src];
+                        const int from = rc * RW + cc, to = r * RW + c;
+                        src[0][to] = src[0][from];
+                        src[1][to] = src[1][from];
+                        src[2][to] = src[2][from];
                     }
                 }
                 __syncthreads();
             }
-            const int np = (oc1 - oc0 + 1) / 2;
+            SF_TICK();
+            const int items = 3 * nbc * nbr;
 #pragma unroll 1
-            SF_FOR_RECT(r, pc, hr0, hr1, 0, np - 1, NT, tid) {
-                const int idx = r * RW + oc0 + 2 * pc;
-                const float* Pl[3] = {Fx, Fy, Fz};
-                float* Tl[3] = {Tx, Ty, Tz};
+            for (int t = tid; t < items; t += NT) {
+                // Item order (bank-conflict free 16-byte shared accesses): plane-major, then strips of
+                // 8 block columns, row-major inside a strip, so the 8 lanes of a quarter warp read 8
+                // distinct 16-byte bank groups.
+                const int nb = nbr * nbc, q = t / nb, u = t - q * nb;
+                const int nfull = nbc >> 3, ufull = nbr * 8 * nfull;
+                int br, bc;
+                if (u < ufull) {
+                    const int s8 = u / (8 * nbr), v = u - s8 * 8 * nbr;
+                    br = v >> 3;
+                    bc = 8 * s8 + (v & 7);
+                } else {
+                    const int wl = nbc - 8 * nfull, v = u - ufull;
+                    br = v / wl;
+                    bc = 8 * nfull + (v - br * wl);
+                }
+                const int r = or0 + 4 * br, c = bc0 + 4 * bc;
+                const float* in = q == 0 ? src[0] : (q == 1 ? src[1] : src[2]);
+                float* out = q == 0 ? dst[0] : (q == 1 ? dst[1] : dst[2]);
+                // Window columns c-2 .. c+5 stay inside the plane row (c - 2 >= bc0 - 2 >= 0) or
+                // run at most one cell into the next row (harmless: it only feeds unstored columns);
+                // window rows are clamped (rows outside [or0-2, or1+2] only feed unstored rows).
+                float2 h[8][2];  // horizontal 5-sums, column pairs (0,1) (2,3)
 #pragma unroll
-                for (int q = 0; q < 3; ++q) {
-                    const float2 x0 = *reinterpret_cast<const float2*>(Pl[q] + idx - 2);
-                    const float2 x1 = *reinterpret_cast<const float2*>(Pl[q] + idx);
-                    const float2 x2 = *reinterpret_cast<const float2*>(Pl[q] + idx + 2);
-                    *reinterpret_cast<float2*>(Tl[q] + idx) =
-                        make_float2(xadd(xadd(xadd(xadd(x0.x, x0.y), x1.x), x1.y), x2.x),
-                                    xadd(xadd(xadd(xadd(x0.y, x1.x), x1.y), x2.x), x2.y));
+                for (int i = 0; i < 8; ++i) {
+                    const float* row = in + iclamp(r - 2 + i, 0, RH - 1) * RW + c - 2;
+                    const float4 xa = *reinterpret_cast<const float4*>(row);
+                    const float4 xb = *reinterpret_cast<const float4*>(row + 4);
+                    const float x[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
+                    float hs[4];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+                        hs[j] = xadd(xadd(xadd(xadd(x[j], x[j + 1]), x[j + 2]), x[j + 3]), x[j + 4]);
+                    h[i][0] = make_float2(hs[0], hs[1]);
+                    h[i][1] = make_float2(hs[2], hs[3]);
+                }
+                // vertical 5-sums (paired columns) and x / 25 (div25, paired): q = x RN(1/25),
+                // q1 = fma(fma(-q, 25, x), RN(1/25), q); non-finite sums take q (= the IEEE quotient)
+                const float2 y25 = make_float2(0.04f, 0.04f), m25 = make_float2(-25.0f, -25.0f);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    float o[4];
+#pragma unroll
+                    for (int jp = 0; jp < 2; ++jp) {
+                        const float2 v =
+                            add2(add2(add2(add2(h[i][jp], h[i + 1][jp]), h[i + 2][jp]), h[i + 3][jp]), h[i + 4][jp]);
+                        const float2 q = mul2(v, y25);
+                        const float2 q1 = fma2(fma2(q, m25, v), y25, q);
+                        o[2 * jp] = isfinite(v.x) ? q1.x : q.x;
+                        o[2 * jp + 1] = isfinite(v.y) ? q1.y : q.y;
+                    }
+                    if (r + i <= or1) {
+                        *reinterpret_cast<float2*>(out + (r + i) * RW + c) = make_float2(o[0], o[1]);
+                        *reinterpret_cast<float2*>(out + (r + i) * RW + c + 2) = make_float2(o[2], o[3]);
+                    }
                 }
             }
-            __syncthreads();
-#pragma unroll 1
-            SF_FOR_RECT(r, pc, or0, or1, 0, np - 1, NT, tid) {
-                const int idx = r * RW + oc0 + 2 * pc;
-                const float* Tl[3] = {Tx, Ty, Tz};
-                float* Pl[3] = {Fx, Fy, Fz};
 #pragma unroll
-                for (int q = 0; q < 3; ++q) {
-                    const float2 y0 = *reinterpret_cast<const float2*>(Tl[q] + idx - 2 * RW);
-                    const float2 y1 = *reinterpret_cast<const float2*>(Tl[q] + idx - RW);
-                    const float2 y2 = *reinterpret_cast<const float2*>(Tl[q] + idx);
-                    const float2 y3 = *reinterpret_cast<const float2*>(Tl[q] + idx + RW);
-                    const float2 y4 = *reinterpret_cast<const float2*>(Tl[q] + idx + 2 * RW);
-                    *reinterpret_cast<float2*>(Pl[q] + idx) =
-                        make_float2(div25(xadd(xadd(xadd(xadd(y0.x, y1.x), y2.x), y3.x), y4.x)),
-                                    div25(xadd(xadd(xadd(xadd(y0.y, y1.y), y2.y), y3.y), y4.y)));
-                }
+            for (int qq = 0; qq < 3; ++qq) {  // this pass's output is the next pass's input
+                float* tmp = src[qq];
+                src[qq] = dst[qq];
+                dst[qq] = tmp;
             }
         }
+        float* const Wx = src[0];
+        float* const Wy = src[1];
+        float* const Wz = src[2];
         __syncthreads();
         SF_TICK();
         // ---- rho fusion by the threads that hold rho^{k+} in registers, and the store of
@@ -720,9 +763,9 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
             if (r >= R && r < R + TH && r >= rmin && r <= rmax && c0 >= R && c0 < R + TW && c0 >= cmin &&
                 c0 <= cmax) {
                 const int idx = r * RW + c0;
-                const float2 wx = *reinterpret_cast<const float2*>(Fx + idx);
-                const float2 wy2 = *reinterpret_cast<const float2*>(Fy + idx);
-                const float2 wz = *reinterpret_cast<const float2*>(Fz + idx);
+                const float2 wx = *reinterpret_cast<const float2*>(Wx + idx);
+                const float2 wy2 = *reinterpret_cast<const float2*>(Wy + idx);
+                const float2 wz = *reinterpret_cast<const float2*>(Wz + idx);
                 const float2 rh2 = *reinterpret_cast<const float2*>(Ds + idx);
                 const bool v0 = !isnan(rh2.x), v1 = !isnan(rh2.y);
                 const float rn0 = xfma(v0 ? kap : 0.0f, xsub(v0 ? rh2.x : 0.0f, f0[k].w), f0[k].w);
