@@ -20,7 +20,7 @@
 //     depth land while the transport runs; cp.async fallback when W % 4 != 0), and
 //     while the transport runs; the update computes the brightness / inverse-depth models,
 //     the 3x3 LDL^T solve and S box passes on shared planes, then fuses rho and stores.
-// The transport update of the 4 fields uses paired f32x2 ops (FADD2/FMUL2/FFMA2).
+// The per-cell arithmetic of the transport runs on cell pairs as f32x2 ops (FADD2/FMUL2/FFMA2).
 #include <cuda.h>
 #include <stdio.h>
 #include <stdlib.h>
@@ -59,31 +59,6 @@ __device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
         "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;}"
         : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
     return d;
-}
-
-// f* = fma(-dt, fma(|u_hat|, f - f_up, f q), f)  -- equal (up to the sign of a zero) to
-// the literal fma(-dt, fma(u_hat, D, f q), f) with D the upwind difference,
-// because |u_hat| (f - f_up) and u_hat D are the same exact product.
-__device__ __forceinline__ float4 transport(float4 v, float4 fu, float a, float q, float ndt) {
-    const float2 A = make_float2(a, a), Q = make_float2(q, q), T = make_float2(ndt, ndt);
-    const float2 v01 = make_float2(v.x, v.y), v23 = make_float2(v.z, v.w);
-    const float2 d01 = sub2(v01, make_float2(fu.x, fu.y)), d23 = sub2(v23, make_float2(fu.z, fu.w));
-    const float2 t01 = fma2(A, d01, mul2(v01, Q)), t23 = fma2(A, d23, mul2(v23, Q));
-    const float2 o01 = fma2(T, t01, v01), o23 = fma2(T, t23, v23);
-    return make_float4(o01.x, o01.y, o23.x, o23.y);
-}
-
-__device__ __forceinline__ float dot3s(float ax, float ay, float az, float4 x) {
-    return xfma(az, x.z, xfma(ay, x.y, xmul(ax, x.x)));
-}
-__device__ __forceinline__ float4 sel4(bool p, float4 a, float4 b) { return p ? a : b; }
-__device__ __forceinline__ float4 shfl_up4(float4 v) {
-    return make_float4(__shfl_up_sync(FULL, v.x, 1), __shfl_up_sync(FULL, v.y, 1), __shfl_up_sync(FULL, v.z, 1),
-                       __shfl_up_sync(FULL, v.w, 1));
-}
-__device__ __forceinline__ float4 shfl_dn4(float4 v) {
-    return make_float4(__shfl_down_sync(FULL, v.x, 1), __shfl_down_sync(FULL, v.y, 1), __shfl_down_sync(FULL, v.z, 1),
-                       __shfl_down_sync(FULL, v.w, 1));
 }
 
 __device__ __forceinline__ void cp_async4(float* sdst, const float* gsrc) {
@@ -178,23 +153,40 @@ struct Cfg {
     static constexpr size_t SMEM = sizeof(float) * (8 * (size_t)P + XRF) + 64;  // + mbarriers
 };
 
+// Cell-paired helpers: every float2 holds one quantity of the thread's two cells (cell 0, cell 1),
+// so the per-cell arithmetic runs as f32x2 ops with no operand regrouping.
+// dot2 = fma(az, z, fma(ay, y, ax x)) per cell (the order of xdot3).
+__device__ __forceinline__ float2 dot2(float2 ax, float2 ay, float2 az, float2 x, float2 y, float2 z) {
+    return fma2(az, z, fma2(ay, y, mul2(ax, x)));
+}
+// f* = fma(-dt, fma(|u_hat|, f - f_up, f q), f) per cell -- equal (up to the sign of a zero) to the
+// literal fma(-dt, fma(u_hat, D, f q), f) with D the upwind difference, because
+// |u_hat| (f - f_up) and u_hat D are the same exact product.
+__device__ __forceinline__ float2 tr2(float2 v, float2 fu, float2 A, float2 Q, float2 T) {
+    return fma2(T, fma2(A, sub2(v, fu), mul2(v, Q)), v);
+}
+__device__ __forceinline__ float2 sel2(bool p0, bool p1, float2 a, float2 b) {
+    return make_float2(p0 ? a.x : b.x, p1 ? a.y : b.y);
+}
+
 // The transport: M substeps of a column pass then a row pass on the thread's
-// 2 x K cells.  Grid borders (replicate clamp, reading 10) are handled by REPLICA cells: the
-// out-of-grid cell next to a grid edge is kept equal to the edge cell (loaded that way, and
+// 2 x K cells, held cell-paired: W[0..2][k] = w (x, y, z), W[3][k] = rho, each a float2 over the
+// thread's two columns.  Grid borders (replicate clamp, reading 10) are handled by REPLICA cells:
+// the out-of-grid cell next to a grid edge is kept equal to the edge cell (loaded that way, and
 // refreshed after each pass that changed the edge), so the neighbour read of the edge cell
 // returns its own value and the pass bodies carry no boundary logic.  A grid edge on the
 // region border itself needs no replica: it lies R cells from the tile, outside the tile's
 // dependency cone, like any cut edge.
 template <int K, int NWY, int RULE, bool CLAMP>
-__device__ __forceinline__ void transport_passes(const FrameParams& f, int M, float4 (&f0)[K], float4 (&f1)[K],
-                                                 const float (&s0x)[K], const float (&s0y)[K], const float (&s0z)[K],
-                                                 const float (&s1x)[K], const float (&s1y)[K], const float (&s1z)[K],
-                                                 float (&mx)[K], const float* Es, float4* XR0, int lane, int wy,
-                                                 int cmin, int cmax, int rmin, int rmax, int dbg) {
+__device__ __forceinline__ void transport_passes(const FrameParams& f, int M, float2 (&W)[4][K], const float2 (&SX)[K],
+                                                 const float2 (&SY)[K], const float2 (&SZ)[K], float (&mx)[K],
+                                                 const float* Es, float2* XB0, int lane, int wy, int cmin, int cmax,
+                                                 int rmin, int rmax, int dbg) {
     using C = Cfg<K, NWY>;
-    constexpr int RW = C::RW, RH = C::RH, P = C::P;
+    constexpr int RW = C::RW, P = C::P, RH = C::RH;
     const int c0 = 2 * lane, r0 = K * wy;
-    const float ndt = -f.dt, U = f.U;
+    const float U = f.U;
+    const float2 T2 = make_float2(-f.dt, -f.dt), SG = make_float2(f.sigma, f.sigma);
     const int srcL = lane - 1, srcR = lane + 1;
     // replica bookkeeping (block-uniform except for the lane / k tests)
     const bool repL = cmin > 0, repR = cmax < RW - 1, repT = rmin > 0, repB = rmax < RH - 1;
@@ -203,6 +195,18 @@ __device__ __forceinline__ void transport_passes(const FrameParams& f, int M, fl
     const bool rOdd = (cmax & 1) != 0;                         // replica is cell 0 of laneR (else its cell 1)
     const bool in1 = c0 + 1 <= cmax;                           // cell 1 inside the grid (for the flag max)
     const int keT = rmin - r0, keB = rmax - r0;                // edge rows in this thread's run
+
+    // dominant flow of both cells -> flag max, clamp, (|u_hat0|, |u_hat1|)
+    auto flow = [&](int k, float uh0, float uh1, bool& p0, bool& p1) -> float2 {
+        mx[k] = fmaxf(mx[k], fmaxf(fabsf(uh0), in1 ? fabsf(uh1) : 0.0f));
+        if (CLAMP) {
+            uh0 = fminf(fmaxf(uh0, -U), U);
+            uh1 = fminf(fmaxf(uh1, -U), U);
+        }
+        p0 = uh0 > 0.0f;
+        p1 = uh1 > 0.0f;
+        return make_float2(fabsf(uh0), fabsf(uh1));
+    };
 
     for (int n = 0; n < M; ++n) {
         // ================= column pass (beta_1): registers + shuffles only
@@ -213,53 +217,47 @@ __device__ __forceinline__ void transport_passes(const FrameParams& f, int M, fl
             const float2 ex = *reinterpret_cast<const float2*>(Es + ib);
             const float2 ey = *reinterpret_cast<const float2*>(Es + P + ib);
             const float2 ez = *reinterpret_cast<const float2*>(Es + 2 * P + ib);
-            const float u0 = dot3s(ex.x, ey.x, ez.x, f0[k]);
-            const float u1 = dot3s(ex.y, ey.y, ez.y, f1[k]);
-            const float uL = __shfl_up_sync(FULL, u1, 1);    // lane-1's cell 1 = left of cell 0
-            const float uR = __shfl_down_sync(FULL, u0, 1);  // lane+1's cell 0 = right of cell 1
-            float uh0 = dominant(uL, u1, RULE);
-            float uh1 = dominant(u0, uR, RULE);
-            mx[k] = fmaxf(mx[k], fmaxf(fabsf(uh0), in1 ? fabsf(uh1) : 0.0f));
-            if (CLAMP) {
-                uh0 = fminf(fmaxf(uh0, -U), U);
-                uh1 = fminf(fmaxf(uh1, -U), U);
-            }
+            const float2 u = dot2(ex, ey, ez, W[0][k], W[1][k], W[2][k]);
+            const float uL = __shfl_up_sync(FULL, u.y, 1);    // lane-1's cell 1 = left of cell 0
+            const float uR = __shfl_down_sync(FULL, u.x, 1);  // lane+1's cell 0 = right of cell 1
+            bool p0, p1;
+            const float2 A = flow(k, dominant(uL, u.y, RULE), dominant(u.x, uR, RULE), p0, p1);
             // upwind value by per-lane source: cell 0 takes lane-1's cell 1 (u_hat > 0) or its own
             // cell 1; cell 1 takes its own cell 0 (u_hat > 0) or lane+1's cell 0
-            const int s0 = uh0 > 0.0f ? srcL : lane, s1 = uh1 > 0.0f ? lane : srcR;
-            float4 fu0, fu1;
-            fu0.x = __shfl_sync(FULL, f1[k].x, s0);
-            fu0.y = __shfl_sync(FULL, f1[k].y, s0);
-            fu0.z = __shfl_sync(FULL, f1[k].z, s0);
-            fu0.w = __shfl_sync(FULL, f1[k].w, s0);
-            fu1.x = __shfl_sync(FULL, f0[k].x, s1);
-            fu1.y = __shfl_sync(FULL, f0[k].y, s1);
-            fu1.z = __shfl_sync(FULL, f0[k].z, s1);
-            fu1.w = __shfl_sync(FULL, f0[k].w, s1);
-            const float q0 = xmul(f.sigma, dot3s(s0x[k], s0y[k], s0z[k], f0[k]));
-            const float q1 = xmul(f.sigma, dot3s(s1x[k], s1y[k], s1z[k], f1[k]));
-            f0[k] = transport(f0[k], fu0, fabsf(uh0), q0, ndt);
-            f1[k] = transport(f1[k], fu1, fabsf(uh1), q1, ndt);
+            const int s0 = p0 ? srcL : lane, s1 = p1 ? lane : srcR;
+            const float2 q = mul2(SG, dot2(SX[k], SY[k], SZ[k], W[0][k], W[1][k], W[2][k]));
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const float2 fu = make_float2(__shfl_sync(FULL, W[c][k].y, s0), __shfl_sync(FULL, W[c][k].x, s1));
+                W[c][k] = tr2(W[c][k], fu, A, q, T2);
+            }
         }
         // column replicas <- their edge cells
         if (repL) {
+            const bool me = lane == laneL;
 #pragma unroll
-            for (int k = 0; k < K; ++k) {
-                const float4 e = shfl_dn4(f0[k]);
-                if (lane == laneL) f1[k] = e;
-            }
+            for (int k = 0; k < K; ++k)
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    const float e = __shfl_down_sync(FULL, W[c][k].x, 1);
+                    W[c][k].y = me ? e : W[c][k].y;
+                }
         }
         if (repR) {
+            const bool me = lane == laneR;
             if (rOdd) {
 #pragma unroll
-                for (int k = 0; k < K; ++k) {
-                    const float4 e = shfl_up4(f1[k]);
-                    if (lane == laneR) f0[k] = e;
-                }
+                for (int k = 0; k < K; ++k)
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        const float e = __shfl_up_sync(FULL, W[c][k].y, 1);
+                        W[c][k].x = me ? e : W[c][k].x;
+                    }
             } else {
 #pragma unroll
                 for (int k = 0; k < K; ++k)
-                    if (lane == laneR) f1[k] = f0[k];
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) W[c][k].y = me ? W[c][k].x : W[c][k].y;
             }
         }
         // row replicas inside this thread's run <- their edge rows (before the row pass reads)
@@ -267,106 +265,92 @@ __device__ __forceinline__ void transport_passes(const FrameParams& f, int M, fl
 #pragma unroll
             for (int k = 0; k < K - 1; ++k) {
                 const bool p = (keT - 1 - k) == 0;
-                f0[k] = sel4(p, f0[k + 1], f0[k]);
-                f1[k] = sel4(p, f1[k + 1], f1[k]);
+#pragma unroll
+                for (int c = 0; c < 4; ++c) W[c][k] = sel2(p, p, W[c][k + 1], W[c][k]);
             }
         }
         if (repB && keB >= 0 && keB <= K - 2) {
 #pragma unroll
             for (int k = K - 1; k >= 1; --k) {
                 const bool p = (keB + 1 - k) == 0;
-                f0[k] = sel4(p, f0[k - 1], f0[k]);
-                f1[k] = sel4(p, f1[k - 1], f1[k]);
+#pragma unroll
+                for (int c = 0; c < 4; ++c) W[c][k] = sel2(p, p, W[c][k - 1], W[c][k]);
             }
         }
         // ================= row pass (beta_2, reading 3)
         if (!(dbg & 128)) {
-            float4* const XR = XR0 + (n & 1) * C::XR;
-            XR[(wy * 2 + 0) * RW + c0] = f0[0];
-            XR[(wy * 2 + 0) * RW + c0 + 1] = f1[0];
-            XR[(wy * 2 + 1) * RW + c0] = f0[K - 1];
-            XR[(wy * 2 + 1) * RW + c0 + 1] = f1[K - 1];
-            float v0[K], v1[K];
+            // run-end rows to the exchange buffer: [comp][warp][end][lane] float2
+            float2* const XB = XB0 + (n & 1) * C::XR;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                XB[((c * NWY + wy) * 2 + 0) * 32 + lane] = W[c][0];
+                XB[((c * NWY + wy) * 2 + 1) * 32 + lane] = W[c][K - 1];
+            }
+            float2 v[K];
 #pragma unroll
             for (int k = 0; k < K; ++k) {
                 const int ib = (r0 + k) * RW + c0;
-                const float2 ex = *reinterpret_cast<const float2*>(Es + 3 * P + ib);
-                const float2 ey = *reinterpret_cast<const float2*>(Es + 4 * P + ib);
-                const float2 ez = *reinterpret_cast<const float2*>(Es + 5 * P + ib);
-                v0[k] = dot3s(ex.x, ey.x, ez.x, f0[k]);
-                v1[k] = dot3s(ex.y, ey.y, ez.y, f1[k]);
+                v[k] = dot2(*reinterpret_cast<const float2*>(Es + 3 * P + ib),
+                            *reinterpret_cast<const float2*>(Es + 4 * P + ib),
+                            *reinterpret_cast<const float2*>(Es + 5 * P + ib), W[0][k], W[1][k], W[2][k]);
             }
-            // one row of the row pass for both cells: neighbours (vm, fm) above and (vp, fp) below
-            auto row_update = [&](int k, float vm0, float vm1, const float4& fm0, const float4& fm1, float vp0,
-                                  float vp1, const float4& fp0, const float4& fp1, float4& m0, float4& m1) {
-                float vh0 = dominant(vm0, vp0, RULE);
-                float vh1 = dominant(vm1, vp1, RULE);
-                mx[k] = fmaxf(mx[k], fmaxf(fabsf(vh0), in1 ? fabsf(vh1) : 0.0f));
-                if (CLAMP) {
-                    vh0 = fminf(fmaxf(vh0, -U), U);
-                    vh1 = fminf(fmaxf(vh1, -U), U);
-                }
-                const float4 fu0 = sel4(vh0 > 0.0f, fm0, fp0);
-                const float4 fu1 = sel4(vh1 > 0.0f, fm1, fp1);
-                const float q0 = xmul(f.sigma, dot3s(s0x[k], s0y[k], s0z[k], f0[k]));
-                const float q1 = xmul(f.sigma, dot3s(s1x[k], s1y[k], s1z[k], f1[k]));
-                m0 = transport(f0[k], fu0, fabsf(vh0), q0, ndt);
-                m1 = transport(f1[k], fu1, fabsf(vh1), q1, ndt);
-            };
-            // interior rows 1..K-2 need no exchanged value: compute them before the barrier (new
-            // values written back one row late so rows k-1, k, k+1 are pre-pass; the pre-pass rows 1
-            // and K-2 that the run ends need are kept aside)
-            const float4 o10 = f0[1], o11 = f1[1], oK0 = f0[K - 2], oK1 = f1[K - 2];
-            {
-                float4 n0, n1;
+            // row k in place from its upwind values fu (selected from the pre-pass rows k-1 / k+1)
+            auto row_update = [&](int k, float2 vm, float2 vp, const float2 (&fm)[4], const float2 (&fp)[4]) {
+                bool p0, p1;
+                const float2 A = flow(k, dominant(vm.x, vp.x, RULE), dominant(vm.y, vp.y, RULE), p0, p1);
+                const float2 q = mul2(SG, dot2(SX[k], SY[k], SZ[k], W[0][k], W[1][k], W[2][k]));
 #pragma unroll
-                for (int k = 1; k <= K - 2; ++k) {
-                    float4 m0, m1;
-                    row_update(k, v0[k - 1], v1[k - 1], f0[k - 1], f1[k - 1], v0[k + 1], v1[k + 1], f0[k + 1],
-                               f1[k + 1], m0, m1);
-                    if (k > 1) {
-                        f0[k - 1] = n0;
-                        f1[k - 1] = n1;
-                    }
-                    n0 = m0;
-                    n1 = m1;
+                for (int c = 0; c < 4; ++c) W[c][k] = tr2(W[c][k], sel2(p0, p1, fm[c], fp[c]), A, q, T2);
+            };
+            // pre-pass rows 1 and K-2 are kept for the run ends; the interior rows 1..K-2 need no
+            // exchanged value and are updated before the barrier, in place, in increasing k: row
+            // k's neighbours are the pre-pass row k-1 (kept one step) and row k+1 (not yet updated)
+            float2 o1[4], oK[4], prev[4];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                o1[c] = W[c][1];
+                oK[c] = W[c][K - 2];
+                prev[c] = W[c][0];
+            }
+#pragma unroll
+            for (int k = 1; k <= K - 2; ++k) {
+                float2 cur[4], nxt[4];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    cur[c] = W[c][k];
+                    nxt[c] = W[c][k + 1];
                 }
-                f0[K - 2] = n0;
-                f1[K - 2] = n1;
+                row_update(k, v[k - 1], v[k + 1], prev, nxt);
+#pragma unroll
+                for (int c = 0; c < 4; ++c) prev[c] = cur[c];
             }
             __syncthreads();
-            float4 t0 = f0[0], t1 = f1[0], b0 = f0[K - 1], b1 = f1[K - 1];
-            float vt0 = v0[0], vt1 = v1[0], vb0 = v0[K - 1], vb1 = v1[K - 1];
+            float2 t[4], bb[4];
+            float2 vt = v[0], vb = v[K - 1];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                t[c] = W[c][0];
+                bb[c] = W[c][K - 1];
+            }
             // neighbour run ends; at an edge row on a run boundary the replica is the row itself
             if (wy > 0 && !(repT && keT == 0)) {
-                t0 = XR[((wy - 1) * 2 + 1) * RW + c0];
-                t1 = XR[((wy - 1) * 2 + 1) * RW + c0 + 1];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) t[c] = XB[((c * NWY + wy - 1) * 2 + 1) * 32 + lane];
                 const int ib = (r0 - 1) * RW + c0;
-                const float2 ex = *reinterpret_cast<const float2*>(Es + 3 * P + ib);
-                const float2 ey = *reinterpret_cast<const float2*>(Es + 4 * P + ib);
-                const float2 ez = *reinterpret_cast<const float2*>(Es + 5 * P + ib);
-                vt0 = dot3s(ex.x, ey.x, ez.x, t0);
-                vt1 = dot3s(ex.y, ey.y, ez.y, t1);
+                vt = dot2(*reinterpret_cast<const float2*>(Es + 3 * P + ib),
+                          *reinterpret_cast<const float2*>(Es + 4 * P + ib),
+                          *reinterpret_cast<const float2*>(Es + 5 * P + ib), t[0], t[1], t[2]);
             }
             if (wy < NWY - 1 && !(repB && keB == K - 1)) {
-                b0 = XR[((wy + 1) * 2 + 0) * RW + c0];
-                b1 = XR[((wy + 1) * 2 + 0) * RW + c0 + 1];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) bb[c] = XB[((c * NWY + wy + 1) * 2 + 0) * 32 + lane];
                 const int ib = (r0 + K) * RW + c0;
-                const float2 ex = *reinterpret_cast<const float2*>(Es + 3 * P + ib);
-                const float2 ey = *reinterpret_cast<const float2*>(Es + 4 * P + ib);
-                const float2 ez = *reinterpret_cast<const float2*>(Es + 5 * P + ib);
-                vb0 = dot3s(ex.x, ey.x, ez.x, b0);
-                vb1 = dot3s(ex.y, ey.y, ez.y, b1);
+                vb = dot2(*reinterpret_cast<const float2*>(Es + 3 * P + ib),
+                          *reinterpret_cast<const float2*>(Es + 4 * P + ib),
+                          *reinterpret_cast<const float2*>(Es + 5 * P + ib), bb[0], bb[1], bb[2]);
             }
-            {
-                float4 m0, m1, q0, q1;
-                row_update(0, vt0, vt1, t0, t1, v0[1], v1[1], o10, o11, m0, m1);
-                row_update(K - 1, v0[K - 2], v1[K - 2], oK0, oK1, vb0, vb1, b0, b1, q0, q1);
-                f0[0] = m0;
-                f1[0] = m1;
-                f0[K - 1] = q0;
-                f1[K - 1] = q1;
-            }
+            row_update(0, vt, v[1], t, o1);
+            row_update(K - 1, v[K - 2], vb, oK, bb);
         }
         // (row passes keep column replicas valid; the next column pass keeps row replicas as
         //  they are and they are refreshed again before the next row pass)
@@ -383,7 +367,7 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
     float* const Ys = sm + 6 * P;  // Y (replicated clamp)
     float* const Ds = sm + 7 * P;  // depth -> rhohat (NaN = invalid)
     float* const Xb = sm + 8 * P;  // transport: 2 row-exchange buffers
-    float4* const XR0 = reinterpret_cast<float4*>(Xb);
+    float2* const XB0 = reinterpret_cast<float2*>(Xb);
 
     const FrameParams& f = a.f;
     const int tid = threadIdx.x, lane = tid & 31, wy = tid >> 5;
@@ -400,7 +384,9 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
     if (a.dbg_skip & 32) return;
     long long T_[16];
     int nT_ = 0;
-    const bool tim = (a.dbg_skip & 256) && blockIdx.x == 6 && blockIdx.y == 5 && blockIdx.z == 0;
+    const bool tim = (a.dbg_skip & 256) && blockIdx.z == 0 &&
+                     ((blockIdx.x == 6 && blockIdx.y == 5) || (blockIdx.x == 0 && blockIdx.y == 0) ||
+                      (blockIdx.x == 0 && blockIdx.y == 5) || (blockIdx.x == gridDim.x - 1 && blockIdx.y == gridDim.y - 1));
 #define SF_TICK() do { if (tim) { __syncthreads(); if (tid == 0) T_[nT_] = clock64(); ++nT_; } } while (0)
     SF_TICK();
     // ---------------- staging: e1 / e2 planes (transport), Y and depth (update)
@@ -462,8 +448,8 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
     }
 
     // ---------------- own fields and directions -> registers
-    float4 f0[K], f1[K];
-    float s0x[K], s0y[K], s0z[K], s1x[K], s1y[K], s1z[K];
+    float2 W[4][K];  // cell-paired fields: w.x, w.y, w.z, rho
+    float2 SX[K], SY[K], SZ[K];
     float mx[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) {
@@ -471,12 +457,9 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
         const size_t ga = gr + iclamp(gj0 + c0, 0, f.W - 1), gb = gr + iclamp(gj0 + c0 + 1, 0, f.W - 1);
         const float4 sa = (a.dbg_skip & 16) ? make_float4(0, 0, 1, 0) : __ldg(a.G0 + ga);
         const float4 sb = (a.dbg_skip & 16) ? make_float4(0, 0, 1, 0) : __ldg(a.G0 + gb);
-        s0x[k] = sa.x;
-        s0y[k] = sa.y;
-        s0z[k] = sa.z;
-        s1x[k] = sb.x;
-        s1y[k] = sb.y;
-        s1z[k] = sb.z;
+        SX[k] = make_float2(sa.x, sb.x);
+        SY[k] = make_float2(sa.y, sb.y);
+        SZ[k] = make_float2(sa.z, sb.z);
         mx[k] = 0.0f;
     }
     // ---- programmatic dependent launch: everything above is frame-invariant geometry; the state
@@ -493,8 +476,12 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
     for (int k = 0; k < K; ++k) {
         const size_t gr = (size_t)iclamp(gi0 + r0 + k, 0, f.H - 1) * f.W;
         const size_t ga = gr + iclamp(gj0 + c0, 0, f.W - 1), gb = gr + iclamp(gj0 + c0 + 1, 0, f.W - 1);
-        f0[k] = (a.dbg_skip & 16) ? make_float4(0, 0, 0, 0.5f) : a.fin[plane + ga];
-        f1[k] = (a.dbg_skip & 16) ? make_float4(0, 0, 0, 0.5f) : a.fin[plane + gb];
+        const float4 fa = (a.dbg_skip & 16) ? make_float4(0, 0, 0, 0.5f) : a.fin[plane + ga];
+        const float4 fb = (a.dbg_skip & 16) ? make_float4(0, 0, 0, 0.5f) : a.fin[plane + gb];
+        W[0][k] = make_float2(fa.x, fb.x);
+        W[1][k] = make_float2(fa.y, fb.y);
+        W[2][k] = make_float2(fa.z, fb.z);
+        W[3][k] = make_float2(fa.w, fb.w);
     }
     griddep_launch_dependents();  // the next frame's CTAs may start their geometry loads
     SF_TICK();
@@ -523,7 +510,7 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
     }
 
     if (!(a.dbg_skip & 1))
-    transport_passes<K, NWY, RULE, CLAMP>(f, a.M, f0, f1, s0x, s0y, s0z, s1x, s1y, s1z, mx, Es, XR0, lane, wy, cmin,
+    transport_passes<K, NWY, RULE, CLAMP>(f, a.M, W, SX, SY, SZ, mx, Es, XB0, lane, wy, cmin,
                                           cmax, rmin, rmax, a.dbg_skip);
     const float U = f.U;
 
@@ -551,8 +538,10 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
             const int r = r0 + k;
             if (r >= R && r < R + TH && r >= rmin && r <= rmax) {
                 const size_t g = plane + (size_t)(gi0 + r) * f.W + (gj0 + c0);
-                if (c0 >= R && c0 < R + TW && c0 >= cmin && c0 <= cmax) a.fout[g] = f0[k];
-                if (c0 + 1 >= R && c0 + 1 < R + TW && c0 + 1 >= cmin && c0 + 1 <= cmax) a.fout[g + 1] = f1[k];
+                if (c0 >= R && c0 < R + TW && c0 >= cmin && c0 <= cmax)
+                    a.fout[g] = make_float4(W[0][k].x, W[1][k].x, W[2][k].x, W[3][k].x);
+                if (c0 + 1 >= R && c0 + 1 < R + TW && c0 + 1 >= cmin && c0 + 1 <= cmax)
+                    a.fout[g + 1] = make_float4(W[0][k].y, W[1][k].y, W[2][k].y, W[3][k].y);
             }
         }
     } else {
@@ -606,14 +595,38 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
 #pragma unroll
         for (int k = 0; k < K; ++k) {
             const int ib = (r0 + k) * RW + c0;
-            *reinterpret_cast<float2*>(Fx + ib) = make_float2(f0[k].x, f1[k].x);
-            *reinterpret_cast<float2*>(Fy + ib) = make_float2(f0[k].y, f1[k].y);
-            *reinterpret_cast<float2*>(Fz + ib) = make_float2(f0[k].z, f1[k].z);
+            *reinterpret_cast<float2*>(Fx + ib) = W[0][k];
+            *reinterpret_cast<float2*>(Fy + ib) = W[1][k];
+            *reinterpret_cast<float2*>(Fz + ib) = W[2][k];
         }
         __syncthreads();
         SF_TICK();
-#pragma unroll 2
-        SF_FOR_RECT(r, c, rlo, rhi, clo, (a.dbg_skip & 1024) ? clo - 1 : chi, NT, tid) {  // per-pixel LS, solve region
+        // per-pixel LS on the solve region; the cell's global inputs (s, 1/ds^2, Y, rho^k) are
+        // fetched one cell ahead (L2 latency hidden behind the previous cell's solve)
+        {
+            const int nc = ((a.dbg_skip & 1024) ? clo - 1 : chi) - clo + 1, dr = NT / nc, dc = NT % nc;
+            int rn = rlo + tid / nc, cn = clo + tid % nc;
+            float4 s4n = make_float4(0.f, 0.f, 0.f, 0.f);
+            float yn = 0.f, skn = 0.f;
+            if (nc > 0 && rn <= rhi) {
+                const size_t g = (size_t)(gi0 + rn) * f.W + (gj0 + cn);
+                s4n = __ldg(a.G0 + g);
+                yn = __ldg(a.yin + plane + g);
+                skn = __ldg(&a.sk[plane + g].w);
+            }
+#pragma unroll 1
+            while (nc > 0 && rn <= rhi) {
+            const int r = rn, c = cn;
+            const float4 s4 = s4n;
+            const float ycur = yn, skcur = skn;
+            rn += dr + ((cn + dc > chi) ? 1 : 0);
+            cn = (cn + dc > chi) ? cn + dc - nc : cn + dc;
+            if (rn <= rhi) {
+                const size_t gq = (size_t)(gi0 + rn) * f.W + (gj0 + cn);
+                s4n = __ldg(a.G0 + gq);
+                yn = __ldg(a.yin + plane + gq);
+                skn = __ldg(&a.sk[plane + gq].w);
+            }
             const int idx = r * RW + c;
             const float g0 = HG[idx - 2 * RW], g1 = HG[idx - RW], g2 = HG[idx], g3 = HG[idx + RW], g4 = HG[idx + 2 * RW];
             const float h0 = HH[idx - 2 * RW], h1 = HH[idx - RW], h2 = HH[idx], h3 = HH[idx + RW], h4 = HH[idx + 2 * RW];
@@ -626,7 +639,6 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
             const float br1 = pick_side(rh, vc, rl, vl, rr, vr);  // eq:dominant_b1
             const float br2 = pick_side(rh, vc, ru, vu, rd, vd);  // eq:dominant_b2
             const size_t g = (size_t)(gi0 + r) * f.W + (gj0 + c);
-            const float4 s4 = __ldg(a.G0 + g);
             const float d2 = s4.w;
             const float e1a[3] = {Es[idx], Es[P + idx], Es[2 * P + idx]};
             const float e2a[3] = {Es[3 * P + idx], Es[4 * P + idx], Es[5 * P + idx]};
@@ -639,8 +651,8 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
                 const float dr = xmul(d2, xfma(e2a[q], br2, xmul(e1a[q], br1)));
                 m[q] = xfma(d2r, sa[q], dr);
             }
-            const float cY = xmul(d2, xsub(yh, __ldg(a.yin + plane + g)));    // eq:img_cost_top
-            const float cr = xmul(d2, xsub(rh, __ldg(&a.sk[plane + g].w)));  // eq:invdepth_cost_top
+            const float cY = xmul(d2, xsub(yh, ycur));   // eq:img_cost_top
+            const float cr = xmul(d2, xsub(rh, skcur));  // eq:invdepth_cost_top
             const float wp[3] = {Fx[idx], Fy[idx], Fz[idx]};
             float x[3];
             ls_solve3(gh, m, cY, cr, wp, f.g1, vc ? f.g2 : 0.0f, f.g3, x);
@@ -650,6 +662,7 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
             if (!(isfinite(x[0]) && isfinite(x[1]) && isfinite(x[2])) && gi0 + r >= f.fr0 && gi0 + r < f.fr1)
                 fl |= SF_FLAG_NONFINITE;
             if (r >= R && r < R + TH && c >= R && c < R + TW) a.yout[plane + g] = yh;
+            }
         }
         // ---- S x 5x5 box (reading 13) as a register-tiled 2-D stencil: one work item = one
         // component of a 4 x 4 output block, read as an 8 x 8 window (8-byte shared loads) ->
@@ -768,8 +781,8 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
                 const float2 wz = *reinterpret_cast<const float2*>(Wz + idx);
                 const float2 rh2 = *reinterpret_cast<const float2*>(Ds + idx);
                 const bool v0 = !isnan(rh2.x), v1 = !isnan(rh2.y);
-                const float rn0 = xfma(v0 ? kap : 0.0f, xsub(v0 ? rh2.x : 0.0f, f0[k].w), f0[k].w);
-                const float rn1 = xfma(v1 ? kap : 0.0f, xsub(v1 ? rh2.y : 0.0f, f1[k].w), f1[k].w);
+                const float rn0 = xfma(v0 ? kap : 0.0f, xsub(v0 ? rh2.x : 0.0f, W[3][k].x), W[3][k].x);
+                const float rn1 = xfma(v1 ? kap : 0.0f, xsub(v1 ? rh2.y : 0.0f, W[3][k].y), W[3][k].y);
                 if (!(isfinite(rn0) && isfinite(rn1)) && gi0 + r >= f.fr0 && gi0 + r < f.fr1) fl |= SF_FLAG_NONFINITE;
                 const size_t g = plane + (size_t)(gi0 + r) * f.W + (gj0 + c0);
                 a.fout[g] = make_float4(wx.x, wy2.x, wz.x, rn0);
@@ -779,9 +792,11 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
     }
     SF_TICK();
     if (tim && tid == 0) {
-        printf("SFTIME");
-        for (int i = 1; i < nT_; ++i) printf(" %lld", T_[i] - T_[i - 1]);
-        printf("\n");
+        long long d[12];
+        for (int i = 0; i < 12; ++i) d[i] = (i + 1 < nT_) ? T_[i + 1] - T_[i] : 0;
+        printf("SFTIME %2d,%2d: %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld tot=%lld\n", blockIdx.x,
+               blockIdx.y, d[0], d[1], d[2], d[3], d[4], d[5], d[6], d[7], d[8], d[9], d[10], d[11],
+               T_[nT_ - 1] - T_[0]);
     }
 #undef SF_TICK
     const unsigned any = __reduce_or_sync(FULL, fl);
