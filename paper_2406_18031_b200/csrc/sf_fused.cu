@@ -115,6 +115,32 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
              c = (C0) + (tid) % nc_;                                                             \
          nc_ > 0 && r <= (R1); r += dr_ + ((c + dc_ > (C1)) ? 1 : 0), c = (c + dc_ > (C1)) ? c + dc_ - nc_ : c + dc_)
 
+// Replicate-border fill (reading 10) of the out-of-grid cells of the rectangle [ra, rb] x [ca, cb]
+// of NP shared planes: each takes the value of its clamped in-grid cell.  Only the out-of-grid
+// bands are visited (top and bottom rows with corners, then left and right columns).
+template <int NP, int RW, int RH, int NT>
+__device__ __forceinline__ void edge_fill(float* p0, float* p1, float* p2, int ra, int rb, int ca, int cb, int rmin,
+                                          int rmax, int cmin, int cmax, int tid) {
+    ra = max(ra, 0);
+    rb = min(rb, RH - 1);
+    ca = max(ca, 0);
+    cb = min(cb, RW - 1);
+    auto cp = [&](int r, int c) {
+        const int from = iclamp(r, rmin, rmax) * RW + iclamp(c, cmin, cmax), to = r * RW + c;
+        p0[to] = p0[from];
+        p1[to] = p1[from];
+        if (NP > 2) p2[to] = p2[from];
+    };
+#pragma unroll 1
+    SF_FOR_RECT(r, c, ra, min(rb, rmin - 1), ca, cb, NT, tid) cp(r, c);
+#pragma unroll 1
+    SF_FOR_RECT(r, c, max(ra, rmax + 1), rb, ca, cb, NT, tid) cp(r, c);
+#pragma unroll 1
+    SF_FOR_RECT(r, c, max(ra, rmin), min(rb, rmax), ca, min(cb, cmin - 1), NT, tid) cp(r, c);
+#pragma unroll 1
+    SF_FOR_RECT(r, c, max(ra, rmin), min(rb, rmax), max(ca, cmax + 1), cb, NT, tid) cp(r, c);
+}
+
 struct FusedArgs {
     CUtensorMap tmE;    // [6][H][W] e planes, box 64 x 72 x 3   (valid when tma)
     CUtensorMap tmY;    // [B][H][W] brightness, box 64 x 72 x 1
@@ -553,18 +579,15 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
         float* const Fx = Ys;  // w^{k+} -> w_LS -> smoothed w (in place)
         float* const Fy = Xb + 2 * P;
         float* const Fz = Xb + 3 * P;
+        const int S = f.S;
+        // solve region = tile + 2S (clipped to the grid); models needed on it +-2 rows, +-1 cols
+        const int rlo = max(R - 2 * S, rmin), rhi = min(R + TH + 2 * S - 1, rmax);
+        const int clo = max(R - 2 * S, cmin), chi = min(R + TW + 2 * S - 1, cmax);
         if (a.tma && !(a.dbg_skip & 8)) {
             mbar_wait(&bars[2], 0);
-            if (edgeC || edgeR) {  // out-of-grid cells of Y / depth take their clamped cell's value
+            if (edgeC || edgeR) {  // out-of-grid cells of Y / depth read below take their clamped cell's value
                 __syncthreads();
-                for (int t = tid; t < P; t += NT) {
-                    const int r = t / RW, c = t % RW;
-                    const int rc = iclamp(r, rmin, rmax), cc = iclamp(c, cmin, cmax);
-                    if (rc != r || cc != c) {
-                        Ys[t] = Ys[rc * RW + cc];
-                        Ds[t] = Ds[rc * RW + cc];
-                    }
-                }
+                edge_fill<2, RW, RH, NT>(Ys, Ds, nullptr, rlo - 2, rhi + 2, clo - 3, chi + 3, rmin, rmax, cmin, cmax, tid);
             }
         } else {
             cp_async_wait<0>();
@@ -572,10 +595,6 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
         __syncthreads();  // Y / depth complete; row buffers dead
         const float qnan = __int_as_float(0x7fffffff);
         SF_TICK();
-        const int S = f.S;
-        // solve region = tile + 2S (clipped to the grid); models needed on it +-2 rows, +-1 cols
-        const int rlo = max(R - 2 * S, rmin), rhi = min(R + TH + 2 * S - 1, rmax);
-        const int clo = max(R - 2 * S, cmin), chi = min(R + TW + 2 * S - 1, cmax);
         {
             // rhohat plane + horizontal brightness taps on the solve region +-2 rows, +-1 cols
 #pragma unroll 2
@@ -616,52 +635,52 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
             }
 #pragma unroll 1
             while (nc > 0 && rn <= rhi) {
-            const int r = rn, c = cn;
-            const float4 s4 = s4n;
-            const float ycur = yn, skcur = skn;
-            rn += dr + ((cn + dc > chi) ? 1 : 0);
-            cn = (cn + dc > chi) ? cn + dc - nc : cn + dc;
-            if (rn <= rhi) {
-                const size_t gq = (size_t)(gi0 + rn) * f.W + (gj0 + cn);
-                s4n = __ldg(a.G0 + gq);
-                yn = __ldg(a.yin + plane + gq);
-                skn = __ldg(&a.sk[plane + gq].w);
-            }
-            const int idx = r * RW + c;
-            const float g0 = HG[idx - 2 * RW], g1 = HG[idx - RW], g2 = HG[idx], g3 = HG[idx + RW], g4 = HG[idx + 2 * RW];
-            const float h0 = HH[idx - 2 * RW], h1 = HH[idx - RW], h2 = HH[idx], h3 = HH[idx + RW], h4 = HH[idx + 2 * RW];
-            const float yh = tap_g(g0, g1, g2, g3, g4);  // Yhat^{k+1}
-            const float be1 = tap_g(h0, h1, h2, h3, h4);
-            const float be2 = tap_h(g0, g1, g2, g3, g4);
-            const float rc = Ds[idx], rl = Ds[idx - 1], rr = Ds[idx + 1], ru = Ds[idx - RW], rd = Ds[idx + RW];
-            const bool vc = !isnan(rc), vl = !isnan(rl), vr = !isnan(rr), vu = !isnan(ru), vd = !isnan(rd);
-            const float rh = vc ? rc : 0.0f;
-            const float br1 = pick_side(rh, vc, rl, vl, rr, vr);  // eq:dominant_b1
-            const float br2 = pick_side(rh, vc, ru, vu, rd, vd);  // eq:dominant_b2
-            const size_t g = (size_t)(gi0 + r) * f.W + (gj0 + c);
-            const float d2 = s4.w;
-            const float e1a[3] = {Es[idx], Es[P + idx], Es[2 * P + idx]};
-            const float e2a[3] = {Es[3 * P + idx], Es[4 * P + idx], Es[5 * P + idx]};
-            const float sa[3] = {s4.x, s4.y, s4.z};
-            float gh[3], m[3];
-            const float d2r = xmul(d2, rh);
-#pragma unroll
-            for (int q = 0; q < 3; ++q) {
-                gh[q] = xmul(d2, xfma(e2a[q], be2, xmul(e1a[q], be1)));
-                const float dr = xmul(d2, xfma(e2a[q], br2, xmul(e1a[q], br1)));
-                m[q] = xfma(d2r, sa[q], dr);
-            }
-            const float cY = xmul(d2, xsub(yh, ycur));   // eq:img_cost_top
-            const float cr = xmul(d2, xsub(rh, skcur));  // eq:invdepth_cost_top
-            const float wp[3] = {Fx[idx], Fy[idx], Fz[idx]};
-            float x[3];
-            ls_solve3(gh, m, cY, cr, wp, f.g1, vc ? f.g2 : 0.0f, f.g3, x);
-            Fx[idx] = x[0];
-            Fy[idx] = x[1];
-            Fz[idx] = x[2];
-            if (!(isfinite(x[0]) && isfinite(x[1]) && isfinite(x[2])) && gi0 + r >= f.fr0 && gi0 + r < f.fr1)
-                fl |= SF_FLAG_NONFINITE;
-            if (r >= R && r < R + TH && c >= R && c < R + TW) a.yout[plane + g] = yh;
+                const int r = rn, c = cn;
+                const float4 s4 = s4n;
+                const float ycur = yn, skcur = skn;
+                rn += dr + ((cn + dc > chi) ? 1 : 0);
+                cn = (cn + dc > chi) ? cn + dc - nc : cn + dc;
+                if (rn <= rhi) {
+                    const size_t gq = (size_t)(gi0 + rn) * f.W + (gj0 + cn);
+                    s4n = __ldg(a.G0 + gq);
+                    yn = __ldg(a.yin + plane + gq);
+                    skn = __ldg(&a.sk[plane + gq].w);
+                }
+                const int idx = r * RW + c;
+                const float g0 = HG[idx - 2 * RW], g1 = HG[idx - RW], g2 = HG[idx], g3 = HG[idx + RW], g4 = HG[idx + 2 * RW];
+                const float h0 = HH[idx - 2 * RW], h1 = HH[idx - RW], h2 = HH[idx], h3 = HH[idx + RW], h4 = HH[idx + 2 * RW];
+                const float yh = tap_g(g0, g1, g2, g3, g4);  // Yhat^{k+1}
+                const float be1 = tap_g(h0, h1, h2, h3, h4);
+                const float be2 = tap_h(g0, g1, g2, g3, g4);
+                const float rc = Ds[idx], rl = Ds[idx - 1], rr = Ds[idx + 1], ru = Ds[idx - RW], rd = Ds[idx + RW];
+                const bool vc = !isnan(rc), vl = !isnan(rl), vr = !isnan(rr), vu = !isnan(ru), vd = !isnan(rd);
+                const float rh = vc ? rc : 0.0f;
+                const float br1 = pick_side(rh, vc, rl, vl, rr, vr);  // eq:dominant_b1
+                const float br2 = pick_side(rh, vc, ru, vu, rd, vd);  // eq:dominant_b2
+                const size_t g = (size_t)(gi0 + r) * f.W + (gj0 + c);
+                const float d2 = s4.w;
+                const float e1a[3] = {Es[idx], Es[P + idx], Es[2 * P + idx]};
+                const float e2a[3] = {Es[3 * P + idx], Es[4 * P + idx], Es[5 * P + idx]};
+                const float sa[3] = {s4.x, s4.y, s4.z};
+                float gh[3], m[3];
+                const float d2r = xmul(d2, rh);
+    #pragma unroll
+                for (int q = 0; q < 3; ++q) {
+                    gh[q] = xmul(d2, xfma(e2a[q], be2, xmul(e1a[q], be1)));
+                    const float dr = xmul(d2, xfma(e2a[q], br2, xmul(e1a[q], br1)));
+                    m[q] = xfma(d2r, sa[q], dr);
+                }
+                const float cY = xmul(d2, xsub(yh, ycur));   // eq:img_cost_top
+                const float cr = xmul(d2, xsub(rh, skcur));  // eq:invdepth_cost_top
+                const float wp[3] = {Fx[idx], Fy[idx], Fz[idx]};
+                float x[3];
+                ls_solve3(gh, m, cY, cr, wp, f.g1, vc ? f.g2 : 0.0f, f.g3, x);
+                Fx[idx] = x[0];
+                Fy[idx] = x[1];
+                Fz[idx] = x[2];
+                if (!(isfinite(x[0]) && isfinite(x[1]) && isfinite(x[2])) && gi0 + r >= f.fr0 && gi0 + r < f.fr1)
+                    fl |= SF_FLAG_NONFINITE;
+                if (r >= R && r < R + TH && c >= R && c < R + TW) a.yout[plane + g] = yh;
             }
         }
         // ---- S x 5x5 box (reading 13) as a register-tiled 2-D stencil: one work item = one
@@ -678,21 +697,11 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
             const int m = 2 * (S - 1 - it);  // output of this pass: tile + 2(S-1-it), in the grid
             const int or0 = max(R - m, rmin), or1 = min(R + TH + m - 1, rmax);
             const int oc0 = max(R - m, cmin), oc1 = min(R + TW + m - 1, cmax);
-            const int bc0 = ((oc0 - 2) & ~3) + 2;  // block windows (c-2 .. c+5) start 16-byte aligned
+            const int bc0 = oc0 & ~3;  // 16-byte aligned output blocks
             const int nbc = (oc1 - bc0) / 4 + 1, nbr = (or1 - or0) / 4 + 1;
             __syncthreads();
             if (edge) {
-#pragma unroll 1
-                SF_FOR_RECT(r, c, max(or0 - 2, 0), min(or0 + 4 * nbr + 1, RH - 1), max(bc0 - 2, 0),
-                            min(bc0 + 4 * nbc + 1, RW - 1), NT, tid) {
-                    const int rc = iclamp(r, rmin, rmax), cc = iclamp(c, cmin, cmax);
-                    if (rc != r || cc != c) {
-                        const int from = rc * RW + cc, to = r * RW + c;
-                        src[0][to] = src[0][from];
-                        src[1][to] = src[1][from];
-                        src[2][to] = src[2][from];
-                    }
-                }
+                edge_fill<3, RW, RH, NT>(src[0], src[1], src[2], or0 - 2, or1 + 2, oc0 - 2, oc1 + 2, rmin, rmax, cmin, cmax, tid);
                 __syncthreads();
             }
             SF_TICK();
@@ -717,16 +726,17 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
                 const int r = or0 + 4 * br, c = bc0 + 4 * bc;
                 const float* in = q == 0 ? src[0] : (q == 1 ? src[1] : src[2]);
                 float* out = q == 0 ? dst[0] : (q == 1 ? dst[1] : dst[2]);
-                // Window columns c-2 .. c+5 stay inside the plane row (c - 2 >= bc0 - 2 >= 0) or
+                // Window columns c-2 .. c+5 stay inside the plane row (c - 2 >= bc0 - 2 >= 2) or
                 // run at most one cell into the next row (harmless: it only feeds unstored columns);
                 // window rows are clamped (rows outside [or0-2, or1+2] only feed unstored rows).
                 float2 h[8][2];  // horizontal 5-sums, column pairs (0,1) (2,3)
 #pragma unroll
                 for (int i = 0; i < 8; ++i) {
                     const float* row = in + iclamp(r - 2 + i, 0, RH - 1) * RW + c - 2;
-                    const float4 xa = *reinterpret_cast<const float4*>(row);
-                    const float4 xb = *reinterpret_cast<const float4*>(row + 4);
-                    const float x[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
+                    const float2 xa = *reinterpret_cast<const float2*>(row);
+                    const float4 xb = *reinterpret_cast<const float4*>(row + 2);
+                    const float2 xc = *reinterpret_cast<const float2*>(row + 6);
+                    const float x[8] = {xa.x, xa.y, xb.x, xb.y, xb.z, xb.w, xc.x, xc.y};
                     float hs[4];
 #pragma unroll
                     for (int j = 0; j < 4; ++j)
@@ -749,10 +759,8 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
                         o[2 * jp] = isfinite(v.x) ? q1.x : q.x;
                         o[2 * jp + 1] = isfinite(v.y) ? q1.y : q.y;
                     }
-                    if (r + i <= or1) {
-                        *reinterpret_cast<float2*>(out + (r + i) * RW + c) = make_float2(o[0], o[1]);
-                        *reinterpret_cast<float2*>(out + (r + i) * RW + c + 2) = make_float2(o[2], o[3]);
-                    }
+                    if (r + i <= or1)
+                        *reinterpret_cast<float4*>(out + (r + i) * RW + c) = make_float4(o[0], o[1], o[2], o[3]);
                 }
             }
 #pragma unroll
