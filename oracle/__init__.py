@@ -170,6 +170,40 @@ def ls_solve(g, m, cY, cr, wp, gam, precision="f32"):
     return out
 
 
+def flow_px(geom, w, precision="f32"):
+    """Tangent flow [H][W][2] and normal flow [H][W] of w [H][W][3], in pixels (eq:tangent_flow,
+    eq:normal_flow; reading 23)."""
+    geom = np.ascontiguousarray(geom, np.float32)
+    H, W, _ = geom.shape
+    dt = np.float32 if precision == "f32" else np.float64
+    lib = _lib(precision)
+    geo = np.empty((H, W, 10), dt)
+    lib.or_geometry(H, W, _ptr(geom), _ptr(geo))
+    w = np.ascontiguousarray(w, dt)
+    t = np.empty((H, W, 2), dt)
+    nrm = np.empty((H, W), dt)
+    lib.or_flow_px(C.c_long(H * W), _ptr(geom), _ptr(geo), _ptr(w), _ptr(t), _ptr(nrm))
+    return t, nrm
+
+
+def evaluate(geom, w_gt, w, precision="f32"):
+    """Per-pixel RMSE (px/frame) and AAE (cosine and degrees) of w against w_gt, and their means
+    over the pixels (eq:RMSE_vel and the AAE of P:L726-734; reading 22)."""
+    geom = np.ascontiguousarray(geom, np.float32)
+    H, W, _ = geom.shape
+    dt = np.float32 if precision == "f32" else np.float64
+    w_gt = np.ascontiguousarray(w_gt, dt)
+    w = np.ascontiguousarray(w, dt)
+    rmse = np.empty((H, W), dt)
+    cos = np.empty((H, W), np.float64)
+    deg = np.empty((H, W), np.float64)
+    sums = np.zeros(2, np.float64)
+    _lib(precision).or_eval(C.c_long(H * W), _ptr(geom), _ptr(w_gt), _ptr(w), _ptr(rmse), _ptr(cos), _ptr(deg),
+                            _ptr(sums))
+    return {"rmse": rmse, "aae_cos": cos, "aae_deg": deg, "mean_rmse": sums[0] / (H * W),
+            "mean_aae_deg": sums[1] / (H * W)}
+
+
 def run_sequence(geom, params, Y, depth, precision="f32", frames=None):
     """Run the filter over a sequence; returns the Oracle (final state) and the per-frame flags."""
     o = Oracle(geom, params, precision)

@@ -454,3 +454,72 @@ unsigned or_step(const or_params* P, const real* geo, const float* Y, const floa
 }
 
 int or_real_bytes(void) { return (int)sizeof(real); }
+
+/* ------------------------------------------------------------------ evaluation outputs (NEXT #3)
+ * Tangent flow (eq:tangent_flow, L736-743) and normal flow (eq:normal_flow, L744-747), in pixels:
+ *   sw = <s, w>;  t = P(s) w = w - s sw  (eq:tmatrix L124-128):  t_a = fma(-s_a, sw, w_a)
+ *   w_perp = B^T P(s) w / ds, evaluated as (e1 . t, e2 . t) with the filter's e_k = b_k / ds
+ *            (reading 23: B^T/ds is the same linear map the filter uses for the optical flow,
+ *             eq:oflow_numeric L639-642, reading 5)
+ *   w_par  = sw / ds
+ * g10 supplies the raw pixel separation ds (Spherepix input, L437); geo the filter's (s, e1, e2).
+ */
+void or_flow_px(long n, const float* g10, const real* geo, const real* w, real* tangent, real* normal)
+{
+    for (long p = 0; p < n; ++p) {
+        const real* g = geo + 10 * p;
+        const real* wp = w + 3 * p;
+        const real ds = R(g10[10 * p + 9]);
+        const real sw = dot3(g, wp);
+        real t[3];
+        for (int a = 0; a < 3; ++a) t[a] = FMA(-g[a], sw, wp[a]);
+        if (tangent) {
+            tangent[2 * p] = dot3(g + 3, t);
+            tangent[2 * p + 1] = dot3(g + 6, t);
+        }
+        if (normal) normal[p] = sw / ds;
+    }
+}
+
+/* RMSE (eq:RMSE_vel, L727-730) and AAE (L731-734) of w against the ground truth w_gt, per pixel:
+ *   d_a = (w_gt_a - w_a) / ds;   rmse = sqrt(fma(d_z, d_z, fma(d_y, d_y, d_x d_x)))   [px/frame, real]
+ *   AAE in double (an evaluation metric, not a filter decision; float32 would floor it at ~0.02 deg):
+ *   a = w_gt / ds, b = w / ds (px/frame, reading 22: Barron's homogeneous form, squared norms)
+ *   c = (1 + a.b) / (sqrt(1 + a.a) sqrt(1 + b.b)), clamped to [-1, 1];  aae = acos(c) * 180/pi
+ * (dot products in dot3 order, explicit fma; every double op IEEE-rounded).  sums[0] += rmse and
+ * sums[1] += aae over the n pixels, in pixel order, in double.
+ */
+static inline double ddot3(const double* a, const double* x) { return fma(a[2], x[2], fma(a[1], x[1], a[0] * x[0])); }
+
+void or_eval(long n, const float* g10, const real* wgt, const real* w, real* rmse, double* aae_cos, double* aae_deg,
+             double* sums)
+{
+    double s0 = 0.0, s1 = 0.0;
+    for (long p = 0; p < n; ++p) {
+        const real ds = R(g10[10 * p + 9]);
+        real d[3];
+        double a[3], b[3];
+        for (int k = 0; k < 3; ++k) {
+            d[k] = (wgt[3 * p + k] - w[3 * p + k]) / ds;
+            a[k] = (double)wgt[3 * p + k] / (double)g10[10 * p + 9];
+            b[k] = (double)w[3 * p + k] / (double)g10[10 * p + 9];
+        }
+#ifdef OR_F32
+        const real e = sqrtf(dot3(d, d));
+#else
+        const real e = sqrt(dot3(d, d));
+#endif
+        double c = (1.0 + ddot3(a, b)) / (sqrt(1.0 + ddot3(a, a)) * sqrt(1.0 + ddot3(b, b)));
+        c = fmin(fmax(c, -1.0), 1.0);
+        const double ang = acos(c) * (180.0 / 3.14159265358979323846);
+        if (rmse) rmse[p] = e;
+        if (aae_cos) aae_cos[p] = c;
+        if (aae_deg) aae_deg[p] = ang;
+        s0 += (double)e;
+        s1 += ang;
+    }
+    if (sums) {
+        sums[0] += s0;
+        sums[1] += s1;
+    }
+}
