@@ -146,6 +146,23 @@ sf_status sf_set_fields(sf_ctx* ctx, const float* w, const float* rho, const flo
  * SF_E_STABILITY if SF_FLAG_CFL is set, else SF_OK. */
 sf_status sf_status_flags(sf_ctx* ctx, uint32_t* flags, int32_t clear);
 
+/* ---- evaluation outputs ----------------------------------------------
+ * Tangent and normal flow of the current state w^k in pixels per frame: tangent [B][H][W][2] =
+ * B^T P(s) w / ds (eq:tangent_flow), evaluated as (e1 . t, e2 . t) with
+ * t = w - s <s,w> and the filter's e_k = b_k / ds (DESIGN reading 23); normal [B][H][W] =
+ * <s,w> / ds (eq:normal_flow).  Device pointers, either may be NULL; asynchronous
+ * on the context stream.  Errors: SF_E_DATA (ctx NULL), SF_E_STATE (fresh context). */
+sf_status sf_flow_px(sf_ctx* ctx, float* tangent, float* normal);
+
+/* Accuracy of the current state against a ground truth w_gt ([B][H][W][3] float32, device):
+ * per-pixel RMSE = || (w_gt - w) / ds || in px/frame (eq:RMSE_vel; float32
+ * [B][H][W]) and AAE in degrees (P:L731-734 with DESIGN reading 22: Barron's homogeneous form
+ * with squared norms on w/ds; computed in double, [B][H][W]); either raster may be NULL.
+ * mean_rmse / mean_aae: HOST double [B] (may be NULL) receive each batch member's mean over
+ * its owned rows (all rows unless banded); when either is given the call synchronises the
+ * stream.  Errors: SF_E_DATA (ctx or w_gt NULL), SF_E_STATE (fresh context), SF_E_CUDA. */
+sf_status sf_eval(sf_ctx* ctx, const float* w_gt, float* rmse, double* aae_deg, double* mean_rmse, double* mean_aae);
+
 /* ---- banded mode -------------------------------------------------------------------------
  * Halo rows a band needs so that its owned rows are exact after one sf_step: the transport
  * moves information N rows per frame (eq:numerical_stability), the update reads +-2 rows of

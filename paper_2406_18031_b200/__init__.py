@@ -25,7 +25,7 @@ SF_ABI_VERSION = 1
 EXPORTS = ("sf_config_default", "sf_create", "sf_destroy", "sf_predict", "sf_update", "sf_step", "sf_step_host",
            "sf_get_fields", "sf_set_fields", "sf_status_flags", "sf_kernel_in_use", "sf_launches_per_step",
            "sf_error_string", "sf_band_halo", "sf_band_partition", "sf_halo_exchange_peer", "sf_halo_exchange_nccl",
-           "sf_nccl_unique_id", "sf_nccl_comm_init", "sf_nccl_comm_destroy")
+           "sf_nccl_unique_id", "sf_nccl_comm_init", "sf_nccl_comm_destroy", "sf_flow_px", "sf_eval")
 
 
 class sf_config(C.Structure):
@@ -75,10 +75,12 @@ def _load():
     lib.sf_nccl_comm_init.argtypes = [C.c_int32, C.c_char_p, C.c_int32, C.POINTER(P)]
     lib.sf_nccl_comm_destroy.argtypes = [P]
     lib.sf_nccl_comm_destroy.restype = None
+    lib.sf_flow_px.argtypes = [P, P, P]
+    lib.sf_eval.argtypes = [P, P, P, P, P, P]
     for name in ("sf_create", "sf_predict", "sf_update", "sf_step", "sf_step_host", "sf_get_fields",
                  "sf_set_fields", "sf_status_flags", "sf_kernel_in_use", "sf_launches_per_step", "sf_band_halo",
                  "sf_band_partition", "sf_halo_exchange_peer", "sf_halo_exchange_nccl", "sf_nccl_unique_id",
-                 "sf_nccl_comm_init"):
+                 "sf_nccl_comm_init", "sf_flow_px", "sf_eval"):
         getattr(lib, name).restype = C.c_int
     return lib
 
@@ -132,6 +134,16 @@ def sf_step_host(ctx: int, Y_ptr: int, depth_ptr: int, w_ptr: int | None, rho_pt
 def sf_get_fields(ctx: int, which: int, w_ptr: int | None, rho_ptr: int | None, yhat_ptr: int | None) -> None:
     _check(_lib.sf_get_fields(C.c_void_p(ctx), which, C.c_void_p(w_ptr), C.c_void_p(rho_ptr), C.c_void_p(yhat_ptr)),
            "sf_get_fields")
+
+
+def sf_flow_px(ctx: int, tangent_ptr: int | None, normal_ptr: int | None) -> None:
+    _check(_lib.sf_flow_px(C.c_void_p(ctx), C.c_void_p(tangent_ptr), C.c_void_p(normal_ptr)), "sf_flow_px")
+
+
+def sf_eval(ctx: int, wgt_ptr: int, rmse_ptr: int | None, aae_ptr: int | None, mean_rmse_ptr: int | None,
+            mean_aae_ptr: int | None) -> None:
+    _check(_lib.sf_eval(C.c_void_p(ctx), C.c_void_p(wgt_ptr), C.c_void_p(rmse_ptr), C.c_void_p(aae_ptr),
+                        C.c_void_p(mean_rmse_ptr), C.c_void_p(mean_aae_ptr)), "sf_eval")
 
 
 def sf_set_fields(ctx: int, w_ptr: int, rho_ptr: int, yhat_ptr: int | None) -> None:
@@ -263,6 +275,26 @@ class StructureFlow:
         yhat = t.empty((self.B, self.H, self.W), dtype=t.float32, device=self.device) if which == SF_FIELDS_STATE else None
         sf_get_fields(self.ctx, which, w.data_ptr(), rho.data_ptr(), yhat.data_ptr() if yhat is not None else None)
         return w, rho, yhat
+
+    def flow_px(self):
+        """(tangent [B][H][W][2], normal [B][H][W]) of the current state in pixels (sf_flow_px)."""
+        t = self.torch
+        tg = t.empty((self.B, self.H, self.W, 2), dtype=t.float32, device=self.device)
+        nm = t.empty((self.B, self.H, self.W), dtype=t.float32, device=self.device)
+        sf_flow_px(self.ctx, tg.data_ptr(), nm.data_ptr())
+        return tg, nm
+
+    def evaluate(self, w_gt, rasters: bool = True):
+        """RMSE (px/frame) and AAE (degrees) against w_gt (device [B][H][W][3]) -> dict with the
+        per-pixel rasters (if asked) and the per-batch-member means (sf_eval)."""
+        t = self.torch
+        rm = t.empty((self.B, self.H, self.W), dtype=t.float32, device=self.device) if rasters else None
+        aa = t.empty((self.B, self.H, self.W), dtype=t.float64, device=self.device) if rasters else None
+        mr = (C.c_double * self.B)()
+        ma = (C.c_double * self.B)()
+        sf_eval(self.ctx, self._in3(w_gt), rm.data_ptr() if rasters else None, aa.data_ptr() if rasters else None,
+                C.addressof(mr), C.addressof(ma))
+        return {"rmse": rm, "aae_deg": aa, "mean_rmse": list(mr), "mean_aae_deg": list(ma)}
 
     def set_fields(self, w, rho, yhat=None):
         sf_set_fields(self.ctx, self._in3(w), self._in(rho), self._in(yhat) if yhat is not None else None)

@@ -6,12 +6,6 @@
 
 #include "sf_internal.cuh"
 
-#define SF_TRY(x)                                  \
-    do {                                           \
-        cudaError_t e_ = (x);                      \
-        if (e_ != cudaSuccess) return SF_E_CUDA;   \
-    } while (0)
-
 extern "C" void sf_config_default(sf_config* cfg, int32_t height, int32_t width) {
     memset(cfg, 0, sizeof(*cfg));
     cfg->abi_version = SF_ABI_VERSION;
@@ -55,7 +49,7 @@ static sf_status validate(const sf_config* c) {
 static void free_ctx(sf_ctx* c) {
     if (!c) return;
     void* ptrs[] = {c->G0, c->G1, c->G2, c->E, c->state[0], c->state[1], c->pred, c->tmp, c->tmp2,
-                    c->yhat[0], c->yhat[1], c->HG, c->HH, c->flags, c->hY, c->hD, c->hw, c->hr};
+                    c->yhat[0], c->yhat[1], c->HG, c->HH, c->flags, c->hY, c->hD, c->hw, c->hr, c->eval_part};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);

@@ -18,7 +18,7 @@ __global__ void k_geometry(const float* __restrict__ g10, float4* G0, float4* G1
     const float* g = g10 + 10 * (size_t)p;
     const float ds = g[9];
     G0[p] = make_float4(g[0], g[1], g[2], xmul(ds, ds));
-    const float4 e1 = make_float4(__fdiv_rn(g[3], ds), __fdiv_rn(g[4], ds), __fdiv_rn(g[5], ds), 0.0f);
+    const float4 e1 = make_float4(__fdiv_rn(g[3], ds), __fdiv_rn(g[4], ds), __fdiv_rn(g[5], ds), ds);
     const float4 e2 = make_float4(__fdiv_rn(g[6], ds), __fdiv_rn(g[7], ds), __fdiv_rn(g[8], ds), 0.0f);
     G1[p] = e1;
     G2[p] = e2;
