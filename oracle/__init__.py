@@ -39,7 +39,7 @@ def _lib(prec: str):
         if not os.path.exists(path) or os.path.getmtime(path) < os.path.getmtime(_build.SRC):
             _build.build()
         lib = C.CDLL(path)
-        for name in ("or_predict", "or_update", "or_step"):
+        for name in ("or_predict", "or_update", "or_step", "or_pyr_step_flat", "or_predict_low"):
             getattr(lib, name).restype = C.c_uint
         _LIBS[prec] = lib
     return _LIBS[prec]
@@ -202,6 +202,117 @@ def evaluate(geom, w_gt, w, precision="f32"):
                             _ptr(sums))
     return {"rmse": rmse, "aae_cos": cos, "aae_deg": deg, "mean_rmse": sums[0] / (H * W),
             "mean_aae_deg": sums[1] / (H * W)}
+
+
+def pyramid_params(params, geom1, geom2, smooth_top: int = 4):
+    """Per-level parameters of the H = 2 filter (DESIGN reading 29): the bottom level keeps
+    `params`; the top level has max_flow / 2 (flows halve on the half grid), its own substep
+    count ceil(max_flow / 2), smooth_top box iterations (Table 3: [2, 4]) and gains gamma1,2
+    scaled by (ds1 / ds2)^2 (centre pixel separations; gains scale as ds^-2, reading 11)."""
+    import copy
+    top = copy.copy(params)
+    top.max_flow = float(np.float32(params.max_flow) * np.float32(0.5))
+    top.smooth_iters = smooth_top
+    H1, W1 = geom1.shape[:2]
+    H2, W2 = geom2.shape[:2]
+    r = float(geom1[H1 // 2, W1 // 2, 9]) / float(geom2[H2 // 2, W2 // 2, 9])
+    r2 = r * r
+    g = list(params.gamma)
+    top.gamma = (float(np.float32(g[0] * r2)), float(np.float32(g[1] * r2)), g[2], g[3], g[4])
+    return top
+
+
+class PyramidOracle:
+    """H = 2 filter (or_pyr_step): top level = an H = 1 state on geom2, bottom level state
+    F [H][W][8] = (w, dw, rho, Yhat).  Output flow/inverse depth: w = F[..., 0:3], rho = F[..., 6]."""
+
+    def __init__(self, geom1, geom2, params, precision="f32", smooth_top: int = 4):
+        self.prec = precision
+        self.dtype = np.float32 if precision == "f32" else np.float64
+        self.lib = _lib(precision)
+        self.geom1 = np.ascontiguousarray(geom1, np.float32)
+        self.geom2 = np.ascontiguousarray(geom2, np.float32)
+        self.H, self.W = self.geom1.shape[:2]
+        self.Hc, self.Wc = self.geom2.shape[:2]
+        assert (self.Hc, self.Wc) == (self.H // 2, self.W // 2) and self.H % 2 == 0 and self.W % 2 == 0
+        self.params_low = params
+        self.params_top = pyramid_params(params, self.geom1, self.geom2, smooth_top)
+        self.Plow = make_params(self.H, self.W, self.params_low)
+        self.Ptop = make_params(self.Hc, self.Wc, self.params_top)
+        self.geo1 = np.empty((self.H, self.W, 10), self.dtype)
+        self.geo2 = np.empty((self.Hc, self.Wc, 10), self.dtype)
+        self.lib.or_geometry(self.H, self.W, _ptr(self.geom1), _ptr(self.geo1))
+        self.lib.or_geometry(self.Hc, self.Wc, _ptr(self.geom2), _ptr(self.geo2))
+        self.w2 = np.zeros((self.Hc, self.Wc, 3), self.dtype)
+        self.rho2 = np.zeros((self.Hc, self.Wc), self.dtype)
+        self.yhat2 = np.zeros((self.Hc, self.Wc), self.dtype)
+        self.F = np.zeros((self.H, self.W, 8), self.dtype)
+        self.initialized = False
+        self.flags = 0
+
+    def step(self, Y, depth):
+        Y = np.ascontiguousarray(Y, np.float32)
+        depth = np.ascontiguousarray(depth, np.float32)
+        self.Y2 = np.empty((self.Hc, self.Wc), np.float32)
+        self.D2 = np.empty((self.Hc, self.Wc), np.float32)
+        f = self.lib.or_pyr_step_flat(C.byref(self.Ptop), C.byref(self.Plow), _ptr(self.geo2), _ptr(self.geo1),
+                                      _ptr(self.w2), _ptr(self.rho2), _ptr(self.yhat2), _ptr(self.F), _ptr(Y),
+                                      _ptr(depth), _ptr(self.Y2), _ptr(self.D2),
+                                      C.c_int(0 if self.initialized else 1))
+        self.initialized = True
+        self.flags |= f
+        return f
+
+    @property
+    def w(self):
+        return self.F[..., 0:3]
+
+    @property
+    def rho(self):
+        return self.F[..., 6]
+
+    @property
+    def dw(self):
+        return self.F[..., 3:6]
+
+    @property
+    def yhat(self):
+        return self.F[..., 7]
+
+
+def predict_low(geom, params, F, precision="f32"):
+    """Bottom-level prediction alone: N substeps transporting F [H][W][8] = (w, dw, rho, Yhat) by w."""
+    dt = np.float32 if precision == "f32" else np.float64
+    geom = np.ascontiguousarray(geom, np.float32)
+    H, W, _ = geom.shape
+    lib = _lib(precision)
+    geo = np.empty((H, W, 10), dt)
+    lib.or_geometry(H, W, _ptr(geom), _ptr(geo))
+    F = np.ascontiguousarray(F, dt).copy()
+    P = make_params(H, W, params)
+    f = lib.or_predict_low(C.byref(P), _ptr(geo), _ptr(F))
+    return F, f
+
+
+def down2(Y, depth, is_inverse=False):
+    """2 x 2 mean pyramid step of brightness and depth (reading 24)."""
+    Y = np.ascontiguousarray(Y, np.float32)
+    depth = np.ascontiguousarray(depth, np.float32)
+    H, W = Y.shape
+    Y2 = np.empty((H // 2, W // 2), np.float32)
+    D2 = np.empty((H // 2, W // 2), np.float32)
+    _lib("f32").or_down2(H, W, _ptr(Y), _ptr(depth), C.c_int(int(is_inverse)), _ptr(Y2), _ptr(D2))
+    return Y2, D2
+
+
+def up2(X, precision="f32"):
+    """Bilinear 2x up-sampling of a [Hc][Wc][3] field (reading 25)."""
+    dt = np.float32 if precision == "f32" else np.float64
+    X = np.ascontiguousarray(X, dt)
+    Hc, Wc, _ = X.shape
+    out = np.empty((2 * Hc, 2 * Wc, 3), dt)
+    _lib(precision).or_up2(Hc, Wc, _ptr(X), _ptr(out))
+    return out
 
 
 def run_sequence(geom, params, Y, depth, precision="f32", frames=None):

@@ -523,3 +523,225 @@ void or_eval(long n, const float* g10, const real* wgt, const real* w, real* rms
         sums[1] += s1;
     }
 }
+
+/* ================================================================== H = 2 pyramid (NEXT #1)
+ * Two levels (L358-404, Fig. 3): the top level h = 2 runs the H = 1 filter above on the
+ * half-resolution grid with down-sampled measurements; the bottom level h = 1 keeps the
+ * increment state (dw, rho) (L362-366), transports (w, dw, rho, Y) by the reconstructed flow w
+ * (L525-536, eq:hflow_propagation_low .. eq:img_propagation_low; numerical scheme L662-683),
+ * updates dw by the increment LS (eq:cost_bottom, L592-607) and reconstructs
+ * w = up(w^2) + dw (eq:hflow_reconstruction, L368-372).  Readings 24-30:
+ *   24  down-sampling (unspecified): 2x2 mean, Y2 = ((Y00 + Y01) + (Y10 + Y11)) * 0.25;
+ *       depth likewise when all four samples are valid, else invalid (NaN).
+ *   25  up-sampling: bilinear at the fine pixel centres (coarse coordinate (i - 1/2)/2), weights
+ *       (3/4, 1/4), replicate border: h_r = fma(wc1, X[r][c1], X[r][c0] * wc0) per coarse row r,
+ *       then up = fma(wr1, h_r1, h_r0 * wr0).
+ *   26  the bottom level transports rho by the reconstructed flow w^h (L531 prints w^H).
+ *   27  the bottom-level dilation terms use sigma <s, w> like the top level (reading 2); Y has
+ *       none (eq:img_propagation_low).
+ *   28  the bottom update uses rho^{k+} and Yhat^{k+} (the transported fields) as printed
+ *       (L597-600), the prior dw^{k+} (L601), then S_1 box iterations on dw and the rho fusion.
+ *   29  per-level parameters: N_1 = ceil(max_flow), N_2 = ceil(max_flow / 2) (flows halve on the
+ *       half grid), smoothing [S_1, S_2] = [2, 4] (Table 3 caption, L803-811).
+ *   30  first frame: top level as H = 1; bottom dw = 0, rho = rhohat, Yhat = Yhat(Y), w = up(0) + 0.
+ * Bottom-level state per pixel: F[8] = (w.x, w.y, w.z, dw.x, dw.y, dw.z, rho, Yhat).
+ */
+void or_down2(int H, int W, const float* Y, const float* depth, int is_inverse, float* Y2, float* D2)
+{
+    const int Hc = H / 2, Wc = W / 2;
+    for (int I = 0; I < Hc; ++I)
+        for (int J = 0; J < Wc; ++J) {
+            const long a = (long)(2 * I) * W + 2 * J, b = a + W;
+            const long o = (long)I * Wc + J;
+            if (Y2) Y2[o] = ((Y[a] + Y[a + 1]) + (Y[b] + Y[b + 1])) * 0.25f;
+            if (D2) {
+                const float d[4] = {depth[a], depth[a + 1], depth[b], depth[b + 1]};
+                int ok = 1;
+                for (int k = 0; k < 4; ++k)
+                    ok &= is_inverse ? (isfinite(d[k]) && d[k] >= 0.0f) : (isfinite(d[k]) && d[k] > 0.0f);
+                D2[o] = ok ? ((d[0] + d[1]) + (d[2] + d[3])) * 0.25f : NAN;
+            }
+        }
+}
+
+/* Bilinear 2x up-sampling of a coarse [Hc][Wc][3] field to [2Hc][2Wc][3] (reading 25). */
+void or_up2(int Hc, int Wc, const real* X, real* out)
+{
+    const int H = 2 * Hc, W = 2 * Wc;
+    for (int i = 0; i < H; ++i) {
+        const int I = i >> 1;
+        const int r0 = (i & 1) ? I : clampi(I - 1, 0, Hc - 1), r1 = (i & 1) ? clampi(I + 1, 0, Hc - 1) : I;
+        const real wr0 = (i & 1) ? R(0.75) : R(0.25), wr1 = (i & 1) ? R(0.25) : R(0.75);
+        for (int j = 0; j < W; ++j) {
+            const int J = j >> 1;
+            const int c0 = (j & 1) ? J : clampi(J - 1, 0, Wc - 1), c1 = (j & 1) ? clampi(J + 1, 0, Wc - 1) : J;
+            const real wc0 = (j & 1) ? R(0.75) : R(0.25), wc1 = (j & 1) ? R(0.25) : R(0.75);
+            for (int a = 0; a < 3; ++a) {
+                const real h0 = FMA(wc1, X[3 * ((long)r0 * Wc + c1) + a], X[3 * ((long)r0 * Wc + c0) + a] * wc0);
+                const real h1 = FMA(wc1, X[3 * ((long)r1 * Wc + c1) + a], X[3 * ((long)r1 * Wc + c0) + a] * wc0);
+                out[3 * ((long)i * W + j) + a] = FMA(wr1, h1, h0 * wr0);
+            }
+        }
+    }
+}
+
+/* One bottom-level transport pass (axis as in pass()): the dominant flow from the reconstructed
+ * w, then for c = 0..6 f* = fma(-dt, fma(u_hat, D, f * (sigma <s,w>)), f) and for Yhat (c = 7)
+ * f* = fma(-dt, u_hat * D, f). */
+static unsigned pass_low(const or_params* P, const real* geo, int axis, const real* F, real* Fo, real* u)
+{
+    const int H = P->H, W = P->W;
+    const real U = R(P->max_flow), sigma = R(P->sigma), dt = R(1) / R(P->N);
+    unsigned flags = 0;
+    for (long p = 0; p < (long)H * W; ++p) u[p] = dot3(geo + 10 * p + 3 + 3 * axis, F + 8 * p);
+    for (int i = 0; i < H; ++i)
+        for (int j = 0; j < W; ++j) {
+            const long p = (long)i * W + j;
+            long pm, pp;
+            if (axis == 0) {
+                pm = (long)i * W + clampi(j - 1, 0, W - 1);
+                pp = (long)i * W + clampi(j + 1, 0, W - 1);
+            } else {
+                pm = (long)clampi(i - 1, 0, H - 1) * W + j;
+                pp = (long)clampi(i + 1, 0, H - 1) * W + j;
+            }
+            const real um = u[pm], up = u[pp];
+            real uh;
+            if (P->dominant_rule == OR_DOM_PRINTED)
+                uh = (FABS(up) - FABS(um) > R(0)) ? um : up;
+            else
+                uh = (FABS(um) > FABS(up)) ? um : up;
+            if (P->clamp_advection) {
+                if (FABS(uh) > U) flags |= OR_FLAG_CLAMPED;
+                uh = FMIN(FMAX(uh, -U), U);
+            } else if (dt * FABS(uh) > R(1)) {
+                flags |= OR_FLAG_CFL;
+            }
+            const real q = sigma * dot3(geo + 10 * p, F + 8 * p);
+            for (int c = 0; c < 8; ++c) {
+                const real f = F[8 * p + c];
+                const real D = (uh > R(0)) ? (f - F[8 * pm + c]) : (F[8 * pp + c] - f);
+                Fo[8 * p + c] = (c < 7) ? FMA(-dt, FMA(uh, D, f * q), f) : FMA(-dt, uh * D, f);
+            }
+        }
+    return flags;
+}
+
+/* The two-level filter state. */
+typedef struct {
+    or_params top, low;          /* per-level parameters (reading 29) */
+    const real* geo2;            /* [Hc][Wc][10] working geometry of the top level */
+    const real* geo1;            /* [H][W][10] of the bottom level */
+    real *w2, *rho2, *yhat2;     /* top level state */
+    real* F;                     /* bottom level [H][W][8] */
+} or_pyr;
+
+/* One frame of the H = 2 filter (init != 0: first frame).  Y, depth: [H][W] full resolution.
+ * scratch: Y2, D2 [Hc][Wc] float.  Returns the flags of both levels. */
+unsigned or_pyr_step(const or_pyr* S, const float* Y, const float* depth, float* Y2, float* D2, int init)
+{
+    const or_params* P = &S->low;
+    const int H = P->H, W = P->W, Hc = S->top.H, Wc = S->top.W;
+    const long n = (long)H * W;
+    unsigned flags = 0;
+    or_down2(H, W, Y, depth, P->input_is_inverse_depth, Y2, D2);
+    flags |= or_step(&S->top, S->geo2, Y2, D2, S->w2, S->rho2, S->yhat2, init, NULL, NULL);
+
+    real* yh1 = malloc(sizeof(real) * n);
+    real* b1 = malloc(sizeof(real) * n);
+    real* b2 = malloc(sizeof(real) * n);
+    real* ghat = malloc(sizeof(real) * 3 * n);
+    real* rh = malloc(sizeof(real) * n);
+    real* br1 = malloc(sizeof(real) * n);
+    real* br2 = malloc(sizeof(real) * n);
+    real* drho = malloc(sizeof(real) * 3 * n);
+    unsigned char* valid = malloc(n);
+    real* up = malloc(sizeof(real) * 3 * n);
+    real* F = S->F;
+    for (long p = 0; p < n; ++p)
+        if (!isfinite(Y[p])) flags |= OR_FLAG_NONFINITE;
+    or_brightness_model(H, W, Y, S->geo1, yh1, b1, b2, ghat);
+    or_invdepth_model(H, W, depth, P->input_is_inverse_depth, S->geo1, rh, valid, br1, br2, drho);
+    if (init) {
+        for (long p = 0; p < n; ++p) {
+            for (int c = 3; c < 6; ++c) F[8 * p + c] = R(0);
+            F[8 * p + 6] = rh[p];
+            F[8 * p + 7] = yh1[p];
+        }
+    } else {
+        /* prediction [P_[]] (L525-536): N_1 substeps, column pass then row pass */
+        real* F2 = malloc(sizeof(real) * 8 * n);
+        real* u = malloc(sizeof(real) * n);
+        for (int s = 0; s < P->N; ++s) {
+            flags |= pass_low(P, S->geo1, 0, F, F2, u);
+            flags |= pass_low(P, S->geo1, 1, F2, F, u);
+        }
+        free(F2);
+        free(u);
+        /* update [dU] (L592-607): solve for dw with prior dw^{k+}, references Yhat^{k+}, rho^{k+} */
+        const real g1 = R(P->gamma[0]), g2v = R(P->gamma[1]), g3 = R(P->gamma[2]);
+        const real kap = R(P->gamma[3]) / (R(P->gamma[3]) + R(P->gamma[4]));
+        real* dw = malloc(sizeof(real) * 3 * n);
+        for (long p = 0; p < n; ++p) {
+            const real* s = S->geo1 + 10 * p;
+            const real d2 = s[9];
+            const real d2r = d2 * rh[p];
+            real m[3];
+            for (int a = 0; a < 3; ++a) m[a] = FMA(d2r, s[a], drho[3 * p + a]);
+            const real cY = d2 * (yh1[p] - F[8 * p + 7]);
+            const real cr = d2 * (rh[p] - F[8 * p + 6]);
+            ls_solve(ghat + 3 * p, m, cY, cr, F + 8 * p + 3, g1, valid[p] ? g2v : R(0), g3, dw + 3 * p);
+        }
+        or_smooth(H, W, P->smooth_iters, dw);
+        for (long p = 0; p < n; ++p) {
+            for (int a = 0; a < 3; ++a) F[8 * p + 3 + a] = dw[3 * p + a];
+            const real kappa = valid[p] ? kap : R(0);
+            F[8 * p + 6] = FMA(kappa, rh[p] - F[8 * p + 6], F[8 * p + 6]);
+            F[8 * p + 7] = yh1[p];
+        }
+        free(dw);
+    }
+    /* reconstruction [R] (eq:hflow_reconstruction): w = up(w^2) + dw */
+    or_up2(Hc, Wc, S->w2, up);
+    for (long p = 0; p < n; ++p)
+        for (int a = 0; a < 3; ++a) F[8 * p + a] = up[3 * p + a] + F[8 * p + 3 + a];
+    for (long p = 0; p < n; ++p)
+        for (int c = 0; c < 7; ++c)
+            if (!isfinite(F[8 * p + c])) flags |= OR_FLAG_NONFINITE;
+    free(yh1);
+    free(b1);
+    free(b2);
+    free(ghat);
+    free(rh);
+    free(br1);
+    free(br2);
+    free(drho);
+    free(valid);
+    free(up);
+    return flags;
+}
+
+/* Flat-argument entry point for the Python binding. */
+unsigned or_pyr_step_flat(const or_params* top, const or_params* low, const real* geo2, const real* geo1, real* w2,
+                          real* rho2, real* yhat2, real* F, const float* Y, const float* depth, float* Y2, float* D2,
+                          int init)
+{
+    or_pyr S = {*top, *low, geo2, geo1, w2, rho2, yhat2, F};
+    return or_pyr_step(&S, Y, depth, Y2, D2, init);
+}
+
+/* Bottom-level prediction alone (for the pins): N substeps of pass_low on F [H][W][8], in place. */
+unsigned or_predict_low(const or_params* P, const real* geo, real* F)
+{
+    const long n = (long)P->H * P->W;
+    real* F2 = malloc(sizeof(real) * 8 * n);
+    real* u = malloc(sizeof(real) * n);
+    unsigned flags = 0;
+    for (int s = 0; s < P->N; ++s) {
+        flags |= pass_low(P, geo, 0, F, F2, u);
+        flags |= pass_low(P, geo, 1, F2, F, u);
+    }
+    free(F2);
+    free(u);
+    return flags;
+}

@@ -109,6 +109,7 @@ class Sequence:
     w_gt: np.ndarray | None  # [F][H][W][3] float32
     params: Params
     scene: Scene
+    fov: float = 0.0
 
 
 MAX_NORMAL_RATE = 0.02  # |<s, w_gt>| <= 2 % depth change per frame (time to contact >= 50 frames)
@@ -161,7 +162,7 @@ def make_sequence(H: int, W: int, fov: float, max_flow: float, frames: int, seed
         if with_gt:
             Ws.append(w)
     return Sequence(geom, np.stack(Ys), np.stack(Ds), np.stack(Ws) if with_gt else None,
-                    default_params(geom, max_flow, smooth_iters), sc)
+                    default_params(geom, max_flow, smooth_iters), sc, fov)
 
 
 def band_sequence(cid: int, r0: int, r1: int, frames: int, seed: int | None = None):

@@ -108,6 +108,18 @@ def gnomonic_rows(H: int, W: int, fov_deg: float, r0: int, r1: int, as_f64: bool
     return g if as_f64 else g.astype(np.float32)
 
 
+def gnomonic_pyramid(H: int, W: int, fov_deg: float, levels: int = 2) -> list:
+    """Spherepix pyramid of a GNOMONIC patch: level h has (H / 2^(h-1)) x (W / 2^(h-1)) pixels and
+    the same field of view, so a coarse pixel's direction is its 2 x 2 block centre (the image-plane
+    points are affine in the pixel index).  Returns [level 1, level 2, ...] float32 geometries."""
+    out = []
+    for h in range(levels):
+        if H % (1 << h) or W % (1 << h):
+            raise ValueError("grid size must be divisible by 2^(levels-1)")
+        out.append(gnomonic(H >> h, W >> h, fov_deg))
+    return out
+
+
 def flat(H: int, W: int, ds: float = 2.0 ** -8) -> np.ndarray:
     """FLAT test grid: s = e_z, b1 = e_x, b2 = e_y, constant ds (SURVEY 8(c) pin C2).
 
