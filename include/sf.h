@@ -43,7 +43,7 @@ typedef enum {
     SF_E_STATE = 5,       /* call not valid in the context's current state              */
     SF_E_CUDA = 6,        /* a CUDA runtime call failed                                 */
     SF_E_NCCL = 7,        /* halo exchange failed (banded mode)                         */
-    SF_E_UNSUPPORTED = 8  /* valid request this build does not implement (levels > 1)   */
+    SF_E_UNSUPPORTED = 8  /* valid request this build does not implement (levels > 2 ...) */
 } sf_status;
 
 /* Dominant-flow rule (DESIGN reading 1). */
@@ -69,7 +69,7 @@ typedef struct {
     int32_t abi_version;            /* == SF_ABI_VERSION                                              */
     int32_t height, width;          /* grid H x W, each >= 2                                          */
     int32_t batch;                  /* B >= 1 independent sequences sharing the grid                  */
-    int32_t levels;                 /* pyramid levels H; this build accepts 1 only       */
+    int32_t levels;                 /* pyramid levels H: 1, or 2 (see "Pyramid" below)   */
     float max_flow_px;              /* > 0. N = ceil(max_flow_px) substeps, dt = 1/N;
                                        also the clamp bound on u_hat, v_hat (reading 12)              */
     float gamma[5];                 /* gamma1..gamma5 exactly as in eq:cost_top and
@@ -92,8 +92,21 @@ typedef struct {
     int32_t band_own_begin;
     int32_t band_own_end;
     int32_t global_height;
-    int32_t reserved[3];            /* zero                                                           */
+    int32_t smooth_iters_top;       /* levels = 2: box passes S_2 of the top level; 0 = 4 (Table 3)   */
+    int32_t reserved[2];            /* zero                                                           */
 } sf_config;
+
+/* Pyramid (levels = 2; DESIGN readings 24-30).  height and
+ * width even.  The geometry passed to sf_create holds level 1 ([H][W][10]) followed by level 2
+ * ([H/2][W/2][10], the Spherepix grid of the same patch at half resolution).  The context runs
+ * the top level as an H = 1 filter on the half grid with 2x2-mean inputs, max flow
+ * max_flow_px / 2, S_2 = smooth_iters_top box passes and gains gamma1,2 scaled by
+ * (ds1 / ds2)^2 (centre pixel separations; gamma3..5 unchanged), and the bottom level as the
+ * increment filter (8-field transport by the reconstructed flow, increment LS with
+ * smooth_iters passes, reconstruction w = up(w^2) + dw).  The state seen through the API is the
+ * bottom level: w = reconstructed flow, rho = bottom-level inverse depth, Yhat = its brightness
+ * model.  Only sf_step / sf_step_host advance a pyramid context (sf_predict, sf_update,
+ * sf_set_fields, SF_FIELDS_PREDICTED and banded mode return SF_E_UNSUPPORTED). */
 
 /* Fill *cfg with defaults for an H x W grid (batch 1, max flow 1 px, S = 2, sigma = 0.5,
  * LARGEST, clamp on, gamma = {1,1,1,1,1}, device 0, own stream, AUTO kernel). */

@@ -35,7 +35,7 @@ class sf_config(C.Structure):
                 ("clamp_advection", C.c_int32), ("input_is_inverse_depth", C.c_int32), ("device", C.c_int32),
                 ("stream", C.c_void_p), ("kernel", C.c_int32), ("band_ext_begin", C.c_int32),
                 ("band_own_begin", C.c_int32), ("band_own_end", C.c_int32), ("global_height", C.c_int32),
-                ("reserved", C.c_int32 * 3)]
+                ("smooth_iters_top", C.c_int32), ("reserved", C.c_int32 * 2)]
 
 
 class SFError(RuntimeError):
@@ -207,22 +207,34 @@ def sf_nccl_comm_destroy(comm: int) -> None:
 class StructureFlow:
     """One libsf context over torch CUDA tensors (marshalling only).
 
-    geometry: [H][W][10] float32 (s, b1, b2, ds), host numpy or torch tensor.
+    geometry: [H][W][10] float32 (s, b1, b2, ds), host numpy or torch tensor; or a list
+    [level 1, level 2] of them for the H = 2 pyramid (level 2 = the half-resolution grid).
     params: any object with max_flow, gamma, smooth_iters, sigma, dominant_rule,
     clamp_advection, input_is_inverse_depth (e.g. sfgen.Params).
     """
 
     def __init__(self, geometry, params, batch: int = 1, device: int = 0, stream=None, kernel: int = SF_KERNEL_AUTO,
-                 band: tuple | None = None):
+                 band: tuple | None = None, smooth_iters_top: int = 0):
         """band: None, or (ext_begin, own_begin, own_end, global_height) for a row-band context
         whose geometry holds the global rows [ext_begin, ext_begin + H)."""
         import numpy as np
         import torch
 
         self.torch = torch
-        g = geometry if isinstance(geometry, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(geometry))
-        g = g.to(dtype=torch.float32, device=f"cuda:{device}").contiguous()
-        H, W, ch = g.shape
+
+        def dev(x):
+            t = x if isinstance(x, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(x))
+            return t.to(dtype=torch.float32, device=f"cuda:{device}").contiguous()
+
+        levels = len(geometry) if isinstance(geometry, (list, tuple)) else 1
+        if levels == 1:
+            g = dev(geometry)
+            H, W, ch = g.shape
+        else:
+            parts = [dev(x) for x in geometry]
+            H, W, ch = parts[0].shape
+            assert all(p.shape == (H >> h, W >> h, 10) for h, p in enumerate(parts))
+            g = torch.cat([p.reshape(-1) for p in parts])
         assert ch == 10
         self.H, self.W, self.B, self.device = H, W, batch, torch.device(f"cuda:{device}")
         cfg = sf_config_default(H, W)
@@ -241,6 +253,10 @@ class StructureFlow:
         # pass cudaStreamLegacy (0x1) so libsf orders with torch's work on that stream.
         cfg.stream = self.stream.cuda_stream or 1
         cfg.kernel = kernel
+        cfg.levels = levels
+        cfg.smooth_iters_top = smooth_iters_top
+        self.levels = levels
+        self._geometry = g  # keep the device copy alive until sf_create has read it
         if band is not None:
             cfg.band_ext_begin, cfg.band_own_begin, cfg.band_own_end, cfg.global_height = (int(x) for x in band)
         self.cfg = cfg

@@ -42,18 +42,64 @@ static sf_status validate(const sf_config* c) {
     } else if (c->band_ext_begin != 0 || c->band_own_begin != 0 || (c->global_height != 0 && c->global_height != c->height)) {
         return SF_E_CONFIG;
     }
-    if (c->levels != 1) return SF_E_UNSUPPORTED;
+    if (c->levels == 2) {
+        if ((c->height & 1) || (c->width & 1) || c->height < 4 || c->width < 4) return SF_E_CONFIG;
+        if (c->smooth_iters_top < 0 || c->smooth_iters_top > 64) return SF_E_CONFIG;
+        if (c->band_own_end != 0) return SF_E_UNSUPPORTED;
+    } else if (c->levels != 1) {
+        return SF_E_UNSUPPORTED;
+    }
     return SF_OK;
 }
 
 static void free_ctx(sf_ctx* c) {
     if (!c) return;
     void* ptrs[] = {c->G0, c->G1, c->G2, c->E, c->state[0], c->state[1], c->pred, c->tmp, c->tmp2,
-                    c->yhat[0], c->yhat[1], c->HG, c->HH, c->flags, c->hY, c->hD, c->hw, c->hr, c->eval_part};
+                    c->yhat[0], c->yhat[1], c->HG, c->HH, c->flags, c->hY, c->hD, c->hw, c->hr, c->eval_part,
+                    c->Wf[0], c->Wf[1], c->Wpred, c->Wtmp, c->Y2, c->D2};
     for (void* p : ptrs)
         if (p) cudaFree(p);
+    if (c->top) {
+        cudaStreamSynchronize(c->top->stream);
+        free_ctx(c->top);
+    }
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
     free(c);
+}
+
+// Pyramid (levels == 2): bottom-level buffers and the top-level H = 1 context on the half grid
+// (geometry level 2 follows level 1 in `geometry`).  Per-level parameters: DESIGN reading 29.
+static sf_status create_top(sf_ctx* c, const sf_config* cfg, const float* geometry) {
+    const FrameParams& f = c->fp;
+    const int Hc = f.H / 2, Wc = f.W / 2;
+    const size_t nall = (size_t)f.H * f.W * f.B, ncoarse = (size_t)Hc * Wc * f.B;
+    bool ok = cudaMalloc(&c->Wf[0], nall * sizeof(float4)) == cudaSuccess &&
+              cudaMalloc(&c->Wf[1], nall * sizeof(float4)) == cudaSuccess &&
+              cudaMalloc(&c->Wpred, nall * sizeof(float4)) == cudaSuccess &&
+              cudaMalloc(&c->Wtmp, nall * sizeof(float4)) == cudaSuccess &&
+              cudaMalloc(&c->Y2, ncoarse * sizeof(float)) == cudaSuccess &&
+              cudaMalloc(&c->D2, ncoarse * sizeof(float)) == cudaSuccess &&
+              cudaMemsetAsync(c->Wf[0], 0, nall * sizeof(float4), c->stream) == cudaSuccess;
+    if (!ok) return SF_E_CUDA;
+    const float* g2 = geometry + (size_t)f.H * f.W * 10;
+    float ds1 = 0.0f, ds2 = 0.0f;  // centre pixel separations (host or device geometry)
+    if (cudaMemcpy(&ds1, geometry + ((size_t)(f.H / 2) * f.W + f.W / 2) * 10 + 9, sizeof(float), cudaMemcpyDefault) !=
+            cudaSuccess ||
+        cudaMemcpy(&ds2, g2 + ((size_t)(Hc / 2) * Wc + Wc / 2) * 10 + 9, sizeof(float), cudaMemcpyDefault) != cudaSuccess)
+        return SF_E_CUDA;
+    if (!(ds1 > 0.0f) || !(ds2 > 0.0f)) return SF_E_DATA;
+    sf_config t = *cfg;
+    t.levels = 1;
+    t.height = Hc;
+    t.width = Wc;
+    t.max_flow_px = cfg->max_flow_px * 0.5f;
+    t.smooth_iters = cfg->smooth_iters_top > 0 ? cfg->smooth_iters_top : 4;
+    t.smooth_iters_top = 0;
+    const double r = (double)ds1 / (double)ds2, r2 = r * r;
+    t.gamma[0] = (float)((double)cfg->gamma[0] * r2);
+    t.gamma[1] = (float)((double)cfg->gamma[1] * r2);
+    t.stream = (void*)c->stream;
+    return sf_create(&t, g2, &c->top);
 }
 
 extern "C" sf_status sf_create(const sf_config* cfg, const float* geometry, sf_ctx** out) {
@@ -150,6 +196,17 @@ extern "C" sf_status sf_create(const sf_config* cfg, const float* geometry, sf_c
         free_ctx(c);
         return SF_E_CUDA;
     }
+    c->levels = cfg->levels;
+    if (c->levels == 2) {
+        st = create_top(c, cfg, geometry);
+        if (st != SF_OK) {
+            free_ctx(c);
+            return st;
+        }
+        c->kernel = SF_KERNEL_PASSES;  // the bottom level runs the pass kernels
+        *out = c;
+        return SF_OK;
+    }
     c->kernel = (cfg->kernel != SF_KERNEL_PASSES && sf_fused_supported(c)) ? SF_KERNEL_FUSED : SF_KERNEL_PASSES;
     if (cfg->kernel == SF_KERNEL_FUSED && c->kernel != SF_KERNEL_FUSED) {
         free_ctx(c);
@@ -167,6 +224,7 @@ extern "C" void sf_destroy(sf_ctx* c) {
 
 extern "C" sf_status sf_predict(sf_ctx* c) {
     if (!c) return SF_E_DATA;
+    if (c->levels == 2) return SF_E_UNSUPPORTED;
     if (!c->initialized || c->pending) return SF_E_STATE;
     SF_TRY(sf_launch_predict_passes(c));
     c->pending = true;
@@ -175,6 +233,7 @@ extern "C" sf_status sf_predict(sf_ctx* c) {
 
 extern "C" sf_status sf_update(sf_ctx* c, const float* Y, const float* D) {
     if (!c || !Y || !D) return SF_E_DATA;
+    if (c->levels == 2) return SF_E_UNSUPPORTED;
     if (!c->initialized) {
         SF_TRY(sf_launch_update_passes(c, Y, D, true));
         c->initialized = true;
@@ -187,8 +246,29 @@ extern "C" sf_status sf_update(sf_ctx* c, const float* Y, const float* D) {
     return SF_OK;
 }
 
+// One frame of the two-level filter (Fig. 3): top level on the down-sampled inputs, bottom
+// level predict [P_[]] + update [dU], reconstruction [R] with the new top flow.
+static sf_status pyr_step(sf_ctx* c, const float* Y, const float* D) {
+    SF_TRY(sf_launch_down2(c, Y, D));
+    sf_status st = sf_step(c->top, c->Y2, c->D2);
+    if (st != SF_OK) return st;
+    const float4* w2 = c->top->state[c->top->cur];
+    if (!c->initialized) {
+        SF_TRY(sf_launch_update_low(c, Y, D, true));
+        SF_TRY(sf_launch_up2_add(c, w2, c->state[c->cur], c->yhat[0], c->Wf[c->cur]));
+        c->initialized = true;
+        return SF_OK;
+    }
+    SF_TRY(sf_launch_predict_low(c));
+    SF_TRY(sf_launch_update_low(c, Y, D, false));
+    SF_TRY(sf_launch_up2_add(c, w2, c->state[1 - c->cur], c->yhat[0], c->Wf[1 - c->cur]));
+    c->cur = 1 - c->cur;
+    return SF_OK;
+}
+
 extern "C" sf_status sf_step(sf_ctx* c, const float* Y, const float* D) {
     if (!c || !Y || !D) return SF_E_DATA;
+    if (c->levels == 2) return pyr_step(c, Y, D);
     if (!c->initialized) return sf_update(c, Y, D);
     if (c->pending) return SF_E_STATE;
     if (c->kernel == SF_KERNEL_FUSED) {
@@ -214,7 +294,10 @@ extern "C" sf_status sf_step_host(sf_ctx* c, const float* Yh, const float* Dh, f
     sf_status st = sf_step(c, c->hY, c->hD);
     if (st != SF_OK) return st;
     if (wh || rh) {
-        SF_TRY(sf_launch_unpack(c, c->state[c->cur], wh ? c->hw : nullptr, rh ? c->hr : nullptr));
+        if (c->levels == 2)
+            SF_TRY(sf_launch_unpack_pyr(c, wh ? c->hw : nullptr, rh ? c->hr : nullptr, nullptr));
+        else
+            SF_TRY(sf_launch_unpack(c, c->state[c->cur], wh ? c->hw : nullptr, rh ? c->hr : nullptr));
         if (wh) SF_TRY(cudaMemcpyAsync(wh, c->hw, 3 * n * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
         if (rh) SF_TRY(cudaMemcpyAsync(rh, c->hr, n * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
     }
@@ -226,6 +309,11 @@ extern "C" sf_status sf_get_fields(sf_ctx* c, int32_t which, float* w, float* rh
     if (!c) return SF_E_DATA;
     if (!c->initialized) return SF_E_STATE;
     const size_t n = (size_t)c->fp.B * c->fp.H * c->fp.W;
+    if (c->levels == 2) {
+        if (which != SF_FIELDS_STATE) return which == SF_FIELDS_PREDICTED ? SF_E_UNSUPPORTED : SF_E_CONFIG;
+        SF_TRY(sf_launch_unpack_pyr(c, w, rho, yhat));
+        return SF_OK;
+    }
     const float4* src;
     if (which == SF_FIELDS_STATE) {
         src = c->state[c->cur];
@@ -242,6 +330,7 @@ extern "C" sf_status sf_get_fields(sf_ctx* c, int32_t which, float* w, float* rh
 
 extern "C" sf_status sf_set_fields(sf_ctx* c, const float* w, const float* rho, const float* yhat) {
     if (!c || !w || !rho) return SF_E_DATA;
+    if (c->levels == 2) return SF_E_UNSUPPORTED;
     const size_t n = (size_t)c->fp.B * c->fp.H * c->fp.W;
     SF_TRY(sf_launch_pack(c, w, rho, c->state[c->cur]));
     if (yhat)
@@ -255,10 +344,15 @@ extern "C" sf_status sf_set_fields(sf_ctx* c, const float* w, const float* rho, 
 
 extern "C" sf_status sf_status_flags(sf_ctx* c, uint32_t* flags, int32_t clear) {
     if (!c || !flags) return SF_E_DATA;
-    unsigned h = 0;
+    unsigned h = 0, ht = 0;
     SF_TRY(cudaMemcpyAsync(&h, c->flags, sizeof(unsigned), cudaMemcpyDeviceToHost, c->stream));
+    if (c->top) SF_TRY(cudaMemcpyAsync(&ht, c->top->flags, sizeof(unsigned), cudaMemcpyDeviceToHost, c->stream));
     SF_TRY(cudaStreamSynchronize(c->stream));
-    if (clear) SF_TRY(cudaMemsetAsync(c->flags, 0, sizeof(unsigned), c->stream));
+    h |= ht;
+    if (clear) {
+        SF_TRY(cudaMemsetAsync(c->flags, 0, sizeof(unsigned), c->stream));
+        if (c->top) SF_TRY(cudaMemsetAsync(c->top->flags, 0, sizeof(unsigned), c->stream));
+    }
     *flags = h;
     return (h & SF_FLAG_CFL) ? SF_E_STABILITY : SF_OK;
 }
@@ -267,6 +361,8 @@ extern "C" int32_t sf_kernel_in_use(const sf_ctx* c) { return c ? c->kernel : 0;
 
 extern "C" int32_t sf_launches_per_step(const sf_ctx* c) {
     if (!c) return 0;
+    if (c->levels == 2)  // down2 + top + 2N bottom passes + hconv + solve + 2S box + up2
+        return 1 + sf_launches_per_step(c->top) + 2 * c->fp.N + 2 + 2 * c->fp.S + 1;
     if (c->kernel == SF_KERNEL_FUSED) return sf_fused_launches(c);
     return 2 * c->fp.N + 2 + 2 * c->fp.S;
 }

@@ -83,7 +83,7 @@ extern "C" sf_status sf_flow_px(sf_ctx* c, float* tangent, float* normal) {
     const size_t HW = (size_t)f.H * f.W, n = HW * f.B;
     if (!tangent && !normal) return SF_OK;
     const int blocks = (int)((n + 255) / 256 < 4 * 148 ? (n + 255) / 256 : 4 * 148);
-    k_flow_px<<<blocks, 256, 0, c->stream>>>(c->state[c->cur], c->G0, c->G1, c->G2,
+    k_flow_px<<<blocks, 256, 0, c->stream>>>(sf_flow_plane(c), c->G0, c->G1, c->G2,
                                              reinterpret_cast<float2*>(tangent), normal, HW, n);
     SF_TRY(cudaGetLastError());
     return SF_OK;
@@ -99,7 +99,7 @@ extern "C" sf_status sf_eval(sf_ctx* c, const float* w_gt, float* rmse, double* 
     if (!c->eval_part) SF_TRY(cudaMalloc(&c->eval_part, np * sizeof(double)));
     // means over the owned rows (the whole grid unless banded)
     const int r0 = c->own_begin - c->ext_begin, r1 = c->own_end - c->ext_begin;
-    k_eval<<<dim3(SF_EVAL_BLOCKS, f.B), EB, 0, c->stream>>>(c->state[c->cur], w_gt, c->G1, rmse, aae_deg, f.W, HW,
+    k_eval<<<dim3(SF_EVAL_BLOCKS, f.B), EB, 0, c->stream>>>(sf_flow_plane(c), w_gt, c->G1, rmse, aae_deg, f.W, HW,
                                                           r0, r1, c->eval_part);
     SF_TRY(cudaGetLastError());
     if (mean_rmse || mean_aae) {

@@ -74,6 +74,62 @@ __global__ void __launch_bounds__(BX* BY) k_pass(const float4* __restrict__ in, 
     if (live) out[base + g] = o;
 }
 
+// ------------------------------------------------------------------ pyramid bottom level (NEXT #1)
+// One transport pass of the 8 bottom-level fields (reading 26-27): A = (dw, rho) and
+// Wf = (w, Yhat), all advected by the dominant flow of the reconstructed w; w, dw and rho carry
+// the dilation term sigma <s, w>, Yhat none (eq:img_propagation_low):
+//   f* = fma(-dt, fma(u_hat, D, f q), f)   and   Yhat* = fma(-dt, u_hat D, Yhat).
+template <int AXIS>
+__global__ void __launch_bounds__(BX* BY) k_pass_low(const float4* __restrict__ inA, const float4* __restrict__ inW,
+                                                    float4* __restrict__ outA, float4* __restrict__ outW,
+                                                    const float4* __restrict__ G0, const float4* __restrict__ Ge,
+                                                    FrameParams f, unsigned* flags) {
+    const int j = blockIdx.x * BX + threadIdx.x, i = blockIdx.y * BY + threadIdx.y, b = blockIdx.z;
+    const bool live = (i < f.H) && (j < f.W);
+    const int ii = live ? i : 0, jj = live ? j : 0;
+    int im = ii, ip = ii, jm = jj, jp = jj;
+    if (AXIS == 0) {
+        jm = max(jj - 1, 0);
+        jp = min(jj + 1, f.W - 1);
+    } else {
+        im = max(ii - 1, 0);
+        ip = min(ii + 1, f.H - 1);
+    }
+    const size_t base = (size_t)b * f.H * f.W;
+    const int g = ii * f.W + jj, gm = im * f.W + jm, gp = ip * f.W + jp;
+    const float4 w = inW[base + g], wm = inW[base + gm], wp = inW[base + gp];
+    const float4 a = inA[base + g], am = inA[base + gm], ap = inA[base + gp];
+    const float um = xdot3(Ge[gm], wm), up = xdot3(Ge[gp], wp);
+    float uh = dominant(um, up, f.rule);
+    bool clamped = false, cfl = false;
+    if (f.clamp) {
+        clamped = fabsf(uh) > f.U;
+        uh = fminf(fmaxf(uh, -f.U), f.U);
+    } else {
+        cfl = xmul(f.dt, fabsf(uh)) > 1.0f;
+    }
+    const float q = xmul(f.sigma, xdot3(G0[g], w));
+    const bool fwd = uh > 0.0f;
+    auto tr = [&](float c, float cm, float cp) {
+        return xfma(-f.dt, xfma(uh, fwd ? xsub(c, cm) : xsub(cp, c), xmul(c, q)), c);
+    };
+    float4 oA, oW;
+    oA.x = tr(a.x, am.x, ap.x);
+    oA.y = tr(a.y, am.y, ap.y);
+    oA.z = tr(a.z, am.z, ap.z);
+    oA.w = tr(a.w, am.w, ap.w);
+    oW.x = tr(w.x, wm.x, wp.x);
+    oW.y = tr(w.y, wm.y, wp.y);
+    oW.z = tr(w.z, wm.z, wp.z);
+    oW.w = xfma(-f.dt, xmul(uh, fwd ? xsub(w.w, wm.w) : xsub(wp.w, w.w)), w.w);
+    raise_flag(flags, live && clamped, SF_FLAG_CLAMPED);
+    raise_flag(flags, live && cfl, SF_FLAG_CFL);
+    if (live) {
+        outA[base + g] = oA;
+        outW[base + g] = oW;
+    }
+}
+
 // ------------------------------------------------------------------ update kernels (U1-U6)
 // Horizontal taps of the brightness model: HG = hz(g, Y), HH = hz(h, Y).
 __global__ void __launch_bounds__(BX* BY) k_hconv(const float* __restrict__ Y, float* HG, float* HH, FrameParams f,
@@ -141,7 +197,7 @@ __global__ void __launch_bounds__(BX* BY) k_init(const float* __restrict__ HG, c
 // Yhat^k (yin); writes (w_LS, rho^{k+1}) to out and Yhat^{k+1} to yout.
 __global__ void __launch_bounds__(BX* BY) k_solve(const float* __restrict__ HG, const float* __restrict__ HH,
                                                  const float* __restrict__ D, const float4* __restrict__ pred,
-                                                 const float4* __restrict__ st, const float* __restrict__ yin,
+                                                 const float4* __restrict__ st, const float* __restrict__ yin, int ys,
                                                  float* __restrict__ yout, float4* out,
                                                  const float4* __restrict__ G0, const float4* __restrict__ G1,
                                                  const float4* __restrict__ G2, FrameParams f, unsigned* flags) {
@@ -165,7 +221,7 @@ __global__ void __launch_bounds__(BX* BY) k_solve(const float* __restrict__ HG, 
         }
         const float4 wp = pred[p];
         const float4 sk = st[p];
-        const float cY = xmul(d2, xsub(M.yh, yin[p]));   // d2 (Yhat^{k+1} - Yhat^k), eq:img_cost_top
+        const float cY = xmul(d2, xsub(M.yh, yin[p * ys]));  // d2 (Yhat^{k+1} - Yhat^k), eq:img_cost_top
         const float cr = xmul(d2, xsub(M.rh, sk.w));     // d2 (rhohat - rho^k), eq:invdepth_cost_top
         const float wpa[3] = {wp.x, wp.y, wp.z};
         float x[3];
@@ -268,7 +324,7 @@ cudaError_t sf_launch_update_passes(sf_ctx* c, const float* Y, const float* D, b
     }
     float4* nxt = c->state[1 - c->cur];
     float4* solved = f.S > 0 ? c->tmp : nxt;
-    k_solve<<<g, blk, 0, c->stream>>>(c->HG, c->HH, D, c->pred, c->state[c->cur], c->yhat[c->cur],
+    k_solve<<<g, blk, 0, c->stream>>>(c->HG, c->HH, D, c->pred, c->state[c->cur], c->yhat[c->cur], 1,
                                       c->yhat[1 - c->cur], solved, c->G0, c->G1, c->G2, f, c->flags);
     for (int s = 0; s < f.S; ++s) {
         k_box_h<<<g, blk, 0, c->stream>>>(c->tmp, c->tmp2, f);
@@ -286,5 +342,43 @@ cudaError_t sf_launch_unpack(sf_ctx* c, const float4* src, float* w, float* rho)
 cudaError_t sf_launch_pack(sf_ctx* c, const float* w, const float* rho, float4* dst) {
     const size_t n = (size_t)c->fp.B * c->fp.H * c->fp.W;
     k_pack<<<(unsigned)((n + 255) / 256), 256, 0, c->stream>>>(w, rho, dst, n);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ pyramid bottom level launchers
+// Prediction [P_[]]: N x (column, row) passes of (A, Wf) = ((dw, rho), (w, Yhat)) -> (pred, Wpred).
+cudaError_t sf_launch_predict_low(sf_ctx* c) {
+    const FrameParams& f = c->fp;
+    const dim3 g = grid_for(f), blk(BX, BY);
+    const float4* sA = c->state[c->cur];
+    const float4* sW = c->Wf[c->cur];
+    for (int n = 0; n < f.N; ++n) {
+        k_pass_low<0><<<g, blk, 0, c->stream>>>(sA, sW, c->tmp, c->Wtmp, c->G0, c->G1, f, c->flags);
+        k_pass_low<1><<<g, blk, 0, c->stream>>>(c->tmp, c->Wtmp, c->pred, c->Wpred, c->G0, c->G2, f, c->flags);
+        sA = c->pred;
+        sW = c->Wpred;
+    }
+    return cudaGetLastError();
+}
+
+// Update [dU] (reading 28): the H = 1 solve with prior dw^{k+}, references Yhat^{k+}
+// (Wpred.w) and rho^{k+} (pred.w), S box passes on dw, fusion -> state[1 - cur]; Yhat^{k+1} ->
+// yhat[0] (consumed by the reconstruction).  init: dw = 0, rho = rhohat, Yhat = Yhat(Y).
+cudaError_t sf_launch_update_low(sf_ctx* c, const float* Y, const float* D, bool init) {
+    const FrameParams& f = c->fp;
+    const dim3 g = grid_for(f), blk(BX, BY);
+    k_hconv<<<g, blk, 0, c->stream>>>(Y, c->HG, c->HH, f, c->flags);
+    if (init) {
+        k_init<<<g, blk, 0, c->stream>>>(c->HG, c->HH, D, c->state[c->cur], c->yhat[0], f);
+        return cudaGetLastError();
+    }
+    float4* nxt = c->state[1 - c->cur];
+    float4* solved = f.S > 0 ? c->tmp : nxt;
+    k_solve<<<g, blk, 0, c->stream>>>(c->HG, c->HH, D, c->pred, c->pred, reinterpret_cast<const float*>(c->Wpred) + 3,
+                                      4, c->yhat[0], solved, c->G0, c->G1, c->G2, f, c->flags);
+    for (int s = 0; s < f.S; ++s) {
+        k_box_h<<<g, blk, 0, c->stream>>>(c->tmp, c->tmp2, f);
+        k_box_v<<<g, blk, 0, c->stream>>>(c->tmp2, s == f.S - 1 ? nxt : c->tmp, f);
+    }
     return cudaGetLastError();
 }

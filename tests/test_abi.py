@@ -61,13 +61,23 @@ def test_validation_without_gpu():
     g = np.zeros((8, 8, 10), np.float32)
     cases = [("height", 1, sf.SF_E_CONFIG), ("batch", 0, sf.SF_E_CONFIG), ("max_flow_px", 0.0, sf.SF_E_CONFIG),
              ("smooth_iters", -1, sf.SF_E_CONFIG), ("dominant_rule", 7, sf.SF_E_CONFIG),
-             ("levels", 2, sf.SF_E_UNSUPPORTED), ("abi_version", 99, sf.SF_E_CONFIG)]
+             ("levels", 3, sf.SF_E_UNSUPPORTED), ("levels", 0, sf.SF_E_UNSUPPORTED), ("abi_version", 99, sf.SF_E_CONFIG)]
     for field, val, want in cases:
         cfg = sf.sf_config_default(8, 8)
         setattr(cfg, field, val)
         with pytest.raises(sf.SFError) as e:
             sf.sf_create(cfg, g.ctypes.data)
         assert e.value.status == want, field
+    # pyramid: even sizes >= 4, smooth_iters_top in [0, 64], no banded mode
+    for (h, w, field, val, want) in [(10, 9, None, None, sf.SF_E_CONFIG), (8, 8, "smooth_iters_top", -1, sf.SF_E_CONFIG),
+                                     (2, 8, None, None, sf.SF_E_CONFIG)]:
+        cfg = sf.sf_config_default(h, w)
+        cfg.levels = 2
+        if field:
+            setattr(cfg, field, val)
+        with pytest.raises(sf.SFError) as e:
+            sf.sf_create(cfg, g.ctypes.data)
+        assert e.value.status == want, (h, w, field)
     cfg = sf.sf_config_default(8, 8)
     cfg.gamma[2] = 0.0  # gamma3 must be > 0 (A SPD)
     with pytest.raises(sf.SFError) as e:
