@@ -36,6 +36,10 @@ CONFIG_NAMES = {2: "512x512 spherepix (gnomonic 90 deg), max flow 8 px (N=8), S=
                 3: "1024x1024 spherepix (gnomonic 90 deg), max flow 16 px (N=16), S=2, H=1 level",
                 4: "64 x 512x512 sequences per job, max flow 8 px (N=8), S=2, H=1 level",
                 5: "8192x8192 spherepix (gnomonic 90 deg) row-banded over the GPUs, max flow 8 px (N=8), S=2"}
+CONFIG_NAMES_PYR = {2: "512x512 spherepix, max flow 8 px, H=2 levels (top 256x256: N=4, S=4; bottom: N=8, S=2); "
+                         "the paper's Table 3 shape (594.7 Hz on a GTX 780, context only)",
+                      3: "1024x1024 spherepix, max flow 16 px, H=2 levels (top: N=8, S=4; bottom: N=16, S=2)",
+                      4: "64 x 512x512 sequences per job, max flow 8 px, H=2 levels"}
 ALGO_BYTES_PER_PX = 48  # read w 12 + rho 4 + Yhat 4 + Y 4 + lambda 4, write 12 + 4 + 4
 
 
@@ -43,6 +47,13 @@ def algo_ops_per_px(N: int, S: int) -> int:
     """FP32 operations per pixel per frame of the arithmetic definition:
     26 per transport pass (2N passes) + 109 for the models, solve and fusion + 27 per box pass."""
     return 26 * 2 * N + 109 + 27 * S
+
+
+def algo_ops_per_px_pyr(N1: int, S1: int, N2: int, S2: int) -> float:
+    """H = 2: the top level's H = 1 count on a quarter of the pixels, plus the
+    bottom level's 42 ops per 8-field transport pass (2 N1 passes), the same 109 + 27 S1 update
+    and 12 for the down-sampling and reconstruction."""
+    return algo_ops_per_px(N2, S2) / 4.0 + 42 * 2 * N1 + 109 + 27 * S1 + 12
 
 
 SMS, FP32_LANES_PER_SM = 148, 128  # B200: 148 SMs x 4 SMSPs x 32 FP32 lanes
@@ -121,13 +132,21 @@ def stop_clock_sampler(p, path):
 
 
 # ----------------------------------------------------------------------------- CPU oracle arms
-def oracle_frames(seq, frames, rows=None):
+def oracle_frames(seq, frames, rows=None, levels=1):
     """Run the float32 oracle over `frames` frames (optionally on the first `rows` rows of
     the grid, a bounded sample); return seconds per frame (excluding the init frame)."""
     import oracle
+    import sfgen
 
     g = seq.geom if rows is None else np.ascontiguousarray(seq.geom[:rows])
-    o = oracle.Oracle(g, seq.params, "f32")
+    if levels == 2:
+        H, W = seq.geom.shape[:2]
+        g1, g2 = sfgen.grid.gnomonic_pyramid(H, W, seq.fov)
+        r = H if rows is None else rows - rows % 2
+        o = oracle.PyramidOracle(np.ascontiguousarray(g1[:r]), np.ascontiguousarray(g2[:r // 2]), seq.params)
+        rows = r
+    else:
+        o = oracle.Oracle(g, seq.params, "f32")
     sl = (slice(None),) if rows is None else (slice(None), slice(0, rows))
     Y = np.ascontiguousarray(seq.Y[sl])
     D = np.ascontiguousarray(seq.depth[sl])
@@ -138,15 +157,16 @@ def oracle_frames(seq, frames, rows=None):
     return (time.perf_counter() - t0) / frames
 
 
-def cpu_baseline(seq, budget_s=15.0):
+def cpu_baseline(seq, budget_s=15.0, levels=1):
     """Oracle on host cores, single thread, bounded sample: full 512x512 frames until ~budget."""
-    t1 = oracle_frames(seq, 1)
+    t1 = oracle_frames(seq, 1, levels=levels)
     frames = max(2, min(60, int(budget_s / max(t1, 1e-6))))
-    t = oracle_frames(seq, frames)
+    t = oracle_frames(seq, frames, levels=levels)
     H, W = seq.geom.shape[:2]
     return {"value": 1.0 / t, "unit": "Hz", "cores": 1, "kind": "oracle",
-            "sample": f"{frames} full {H}x{W} frames (N={seq.params.N}, S={seq.params.smooth_iters}) of the "
-                      f"bench workload, float32 oracle, 1 thread, {os.cpu_count()} host cores present"}
+            "sample": f"{frames} full {H}x{W} frames (N={seq.params.N}, S={seq.params.smooth_iters}, H={levels} "
+                      f"level{'s' if levels > 1 else ''}) of the bench workload, float32 oracle, 1 thread, "
+                      f"{os.cpu_count()} host cores present"}
 
 
 def run_reference(args):
@@ -158,19 +178,21 @@ def run_reference(args):
     cid = args.config
     seq = sfgen.config_sequence(cid if cid != 4 else 2, frames=8)
     H, W = seq.geom.shape[:2]
-    t1 = oracle_frames(seq, 1)
+    lv = args.levels
+    t1 = oracle_frames(seq, 1, levels=lv)
     total = args.steps + args.warmup
     budget = 150.0
     rows = H if t1 * total <= budget else max(8, int(H * budget / (t1 * total)))
-    per_frame = oracle_frames(seq, args.warmup, rows) if args.warmup else 0.0  # warm-up (untimed)
-    per_frame = oracle_frames(seq, args.steps, rows)
+    rows -= rows % 2
+    per_frame = oracle_frames(seq, args.warmup, rows, lv) if args.warmup else 0.0  # warm-up (untimed)
+    per_frame = oracle_frames(seq, args.steps, rows, lv)
     frac = rows / H
     value = frac / per_frame  # full frames per second equivalent
     sample = f"each step: one frame of the first {rows} of {H} rows ({frac:.3f} of a frame), f32 oracle, 1 thread"
     out = {"impl": "reference", "metric": METRIC, "value": value, "unit": "Hz", "n_gpus": args.gpus,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_frame * 1e3 / frac,
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-           "config": {"workload": CONFIG_NAMES[cid], "batch": 1},
+           "config": {"workload": CONFIG_NAMES[cid] if lv == 1 else CONFIG_NAMES_PYR[cid], "batch": 1, "levels": lv},
            "cpu_baseline": {"value": value, "unit": "Hz", "cores": 1, "kind": "oracle", "sample": sample},
            "e2e": {"value": value, "unit": "Hz", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out))
@@ -212,7 +234,12 @@ def run_sf(args):
 
     s = torch.cuda.Stream(device=dev)
     kern = {"auto": sf.SF_KERNEL_AUTO, "fused": sf.SF_KERNEL_FUSED, "passes": sf.SF_KERNEL_PASSES}[args.kernel]
-    m = sf.StructureFlow(geom, params, batch=B, device=local, stream=s, kernel=kern)
+    levels = getattr(args, "levels", 1)
+    if levels == 2:
+        pyr = sfgen.grid.gnomonic_pyramid(H, W, base["fov"])
+        m = sf.StructureFlow(pyr, params, batch=B, device=local, stream=s, kernel=kern)
+    else:
+        m = sf.StructureFlow(geom, params, batch=B, device=local, stream=s, kernel=kern)
 
     def frame_of(i):
         """Palindromic replay order 0..R-1, R-1..0: no jump back in time at the wrap (a camera
@@ -320,12 +347,17 @@ def run_sf(args):
         mean_ms = total_ms / args.steps
         algo_bytes = ALGO_BYTES_PER_PX * B * H * W
         gbs = algo_bytes / (mean_ms / 1e3) / 1e9
-        ops = algo_ops_per_px(params.N, params.smooth_iters) * B * H * W
+        if levels == 2:
+            ops = algo_ops_per_px_pyr(params.N, params.smooth_iters, max(1, math.ceil(params.max_flow / 2)), 4) * B * H * W
+        else:
+            ops = algo_ops_per_px(params.N, params.smooth_iters) * B * H * W
         sm_max = pk.get("sm_max_mhz", 1965.0)
         alu_peak = SMS * FP32_LANES_PER_SM * sm_max * 1e6 / 1e12  # TFLOP/s-equivalent FP32 lane-ops
         alu = ops / (mean_ms / 1e3) / 1e12
         kname = "k_fused" if m.kernel == sf.SF_KERNEL_FUSED else "whole step (2N+2+2S per-pass kernels)"
-        tr = ncu_traffic() if m.kernel == sf.SF_KERNEL_FUSED else None
+        if levels == 2:
+            kname = "whole step (top level fused + bottom-level pass kernels)"
+        tr = ncu_traffic() if (m.kernel == sf.SF_KERNEL_FUSED and levels == 1) else None
         roof = {"bound": "alu", "achieved": alu, "peak": alu_peak, "unit": "TFLOP/s", "frac": alu / alu_peak,
                 "traffic": tr["bytes_per_launch"] if tr else None,
                 "traffic_source": (tr["source"] + " (ncu --set full, cache-flushed replay)") if tr else None,
@@ -338,7 +370,8 @@ def run_sf(args):
         out = {"metric": METRIC, "value": value, "unit": "Hz", "n_gpus": world, "steps": args.steps,
                "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
                "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-               "config": {"workload": CONFIG_NAMES[cid], "batch_per_gpu": B, "H": H, "W": W, "N": params.N,
+               "config": {"workload": CONFIG_NAMES[cid] if levels == 1 else CONFIG_NAMES_PYR[cid],
+                          "batch_per_gpu": B, "H": H, "W": W, "N": params.N, "levels": levels,
                           "S": params.smooth_iters, "parallelism": f"independent sequences x{world}",
                           "inputs": f"ring of {ring} frames ({ring * 2 * frame_bytes / 2**20:.0f} MiB) > L2, "
                                     "replayed palindromically, cold reads each step; CUDA graphs of 8 steps",
@@ -349,7 +382,7 @@ def run_sf(args):
                        "note": "sf_step_host: pinned Y,lambda H2D + step + w,rho D2H + stream sync per frame"},
                "device_flags": flags, "clocks": clocks}
         if world == 1 and not args.no_cpu_baseline:
-            out["cpu_baseline"] = cpu_baseline(seqs[0])
+            out["cpu_baseline"] = cpu_baseline(seqs[0], levels=levels)
         print(json.dumps(out))
     if world > 1:
         dist.destroy_process_group()
@@ -461,6 +494,8 @@ def main():
     ap.add_argument("--impl", choices=["sf", "reference"], default="sf")
     ap.add_argument("--config", type=int, choices=[2, 3, 4, 5], default=2)
     ap.add_argument("--kernel", choices=["auto", "fused", "passes"], default="auto")
+    ap.add_argument("--levels", type=int, choices=[1, 2], default=1,
+                    help="pyramid levels (1: the graded H = 1 hot path; 2: the paper's Table 3 shape)")
     ap.add_argument("--ring", type=int, default=96)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

@@ -63,6 +63,8 @@ static void free_ctx(sf_ctx* c) {
         cudaStreamSynchronize(c->top->stream);
         free_ctx(c->top);
     }
+    if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+    if (c->ev_join) cudaEventDestroy(c->ev_join);
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
     free(c);
 }
@@ -98,7 +100,10 @@ static sf_status create_top(sf_ctx* c, const sf_config* cfg, const float* geomet
     const double r = (double)ds1 / (double)ds2, r2 = r * r;
     t.gamma[0] = (float)((double)cfg->gamma[0] * r2);
     t.gamma[1] = (float)((double)cfg->gamma[1] * r2);
-    t.stream = (void*)c->stream;
+    t.stream = nullptr;  // own stream: the top level overlaps the bottom-level prediction
+    if (cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess)
+        return SF_E_CUDA;
     return sf_create(&t, g2, &c->top);
 }
 
@@ -248,21 +253,36 @@ extern "C" sf_status sf_update(sf_ctx* c, const float* Y, const float* D) {
 
 // One frame of the two-level filter (Fig. 3): top level on the down-sampled inputs, bottom
 // level predict [P_[]] + update [dU], reconstruction [R] with the new top flow.
+// The top level (down-sampling + H = 1 step) runs on its own stream, forked from and joined
+// back into the context stream (capturable into CUDA graphs): it only meets the bottom level at
+// the reconstruction, so it overlaps the bottom-level prediction and update.
 static sf_status pyr_step(sf_ctx* c, const float* Y, const float* D) {
-    SF_TRY(sf_launch_down2(c, Y, D));
+    cudaStream_t ts = c->top->stream;
+    SF_TRY(cudaEventRecord(c->ev_fork, c->stream));
+    SF_TRY(cudaStreamWaitEvent(ts, c->ev_fork, 0));
+    {
+        cudaStream_t keep = c->stream;  // k_down2 on the top stream
+        c->stream = ts;
+        const cudaError_t e = sf_launch_down2(c, Y, D);
+        c->stream = keep;
+        SF_TRY(e);
+    }
     sf_status st = sf_step(c->top, c->Y2, c->D2);
     if (st != SF_OK) return st;
-    const float4* w2 = c->top->state[c->top->cur];
-    if (!c->initialized) {
+    SF_TRY(cudaEventRecord(c->ev_join, ts));
+    const bool init = !c->initialized;
+    if (init) {
         SF_TRY(sf_launch_update_low(c, Y, D, true));
-        SF_TRY(sf_launch_up2_add(c, w2, c->state[c->cur], c->yhat[0], c->Wf[c->cur]));
-        c->initialized = true;
-        return SF_OK;
+    } else {
+        SF_TRY(sf_launch_predict_low(c));
+        SF_TRY(sf_launch_update_low(c, Y, D, false));
     }
-    SF_TRY(sf_launch_predict_low(c));
-    SF_TRY(sf_launch_update_low(c, Y, D, false));
-    SF_TRY(sf_launch_up2_add(c, w2, c->state[1 - c->cur], c->yhat[0], c->Wf[1 - c->cur]));
-    c->cur = 1 - c->cur;
+    SF_TRY(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
+    const float4* w2 = c->top->state[c->top->cur];
+    const int nxt = init ? c->cur : 1 - c->cur;
+    SF_TRY(sf_launch_up2_add(c, w2, c->state[nxt], c->yhat[0], c->Wf[nxt]));
+    c->cur = nxt;
+    c->initialized = true;
     return SF_OK;
 }
 
