@@ -294,6 +294,23 @@ def predict_low(geom, params, F, precision="f32"):
     return F, f
 
 
+def map_inputs(geom, K, Ycam, Zcam, Rcg=None):
+    """Resample a pinhole camera's brightness and z-depth ([Hc][Wc]) onto the grid (reading 31);
+    K = (fx, fy, cx, cy), Rcg = grid -> camera rotation (identity by default)."""
+    geom = np.ascontiguousarray(geom, np.float32)
+    H, W, _ = geom.shape
+    Ycam = np.ascontiguousarray(Ycam, np.float32)
+    Zcam = np.ascontiguousarray(Zcam, np.float32)
+    Hc, Wc = Ycam.shape
+    R = np.ascontiguousarray(np.eye(3) if Rcg is None else Rcg, np.float32)
+    Kf = np.ascontiguousarray(K, np.float32)
+    Y = np.empty((H, W), np.float32)
+    D = np.empty((H, W), np.float32)
+    _lib("f32").or_map_inputs(C.c_long(H * W), _ptr(geom), _ptr(R), _ptr(Kf), Hc, Wc, _ptr(Ycam), _ptr(Zcam),
+                              _ptr(Y), _ptr(D))
+    return Y, D
+
+
 def down2(Y, depth, is_inverse=False):
     """2 x 2 mean pyramid step of brightness and depth (reading 24)."""
     Y = np.ascontiguousarray(Y, np.float32)

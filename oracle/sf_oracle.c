@@ -745,3 +745,59 @@ unsigned or_predict_low(const or_params* P, const real* geo, real* F)
     free(u);
     return flags;
 }
+
+/* ================================================================== Spherepix input mapping (NEXT #2)
+ * The measurements reach the filter on the Spherepix grid (L409); the paper's timed region
+ * includes "the time required to map image and depth measurements onto the spherepix image"
+ * (L785) but does not give the operator.  Reading 31: a pinhole camera with
+ * intrinsics K = (fx, fy, cx, cy) (pixel centres at integer coordinates) and rotation Rcg
+ * (grid -> camera, row-major 3x3); per grid pixel, in float32:
+ *   t = Rcg s (row r: dot3(R_r, s));  xn = t.x / t.z, yn = t.y / t.z;
+ *   u = fma(fx, xn, cx), v = fma(fy, yn, cy)            (camera pixel coordinates)
+ *   brightness: (u, v) clamped to [0, Wc-1] x [0, Hc-1]; j0 = floor(u), i0 = floor(v),
+ *     b = u - j0, a = v - i0, j1 = min(j0+1, Wc-1), i1 = min(i0+1, Hc-1);
+ *     r0 = fma(b, Y[i0][j1] - Y[i0][j0], Y[i0][j0]), r1 = fma(b, Y[i1][j1] - Y[i1][j0], Y[i1][j0]),
+ *     Y_grid = fma(a, r1 - r0, r0)
+ *   depth (the camera gives z-depth): invalid (NaN) if t.z <= 0, (u, v) outside the image's
+ *     pixel footprint [-1/2, Wc - 1/2] x [-1/2, Hc - 1/2] or any of the four samples invalid
+ *     (not finite or <= 0); else z = the same bilinear form at the clamped position and
+ *     lambda = z / t.z (range along s, since |s| = 1 and the point is lambda t).
+ * t.z <= 0 also gives the brightness of the clamped position of (0, 0).
+ */
+void or_map_inputs(long n, const float* g10, const float* Rcg, const float* K, int Hc, int Wc, const float* Ycam,
+                   const float* Zcam, float* Y, float* D)
+{
+    const float fx = K[0], fy = K[1], cx = K[2], cy = K[3];
+    for (long p = 0; p < n; ++p) {
+        const float* s = g10 + 10 * p;
+        float t[3];
+        for (int r = 0; r < 3; ++r) t[r] = fmaf(Rcg[3 * r + 2], s[2], fmaf(Rcg[3 * r + 1], s[1], Rcg[3 * r] * s[0]));
+        const int front = t[2] > 0.0f;
+        float u = 0.0f, v = 0.0f;
+        if (front) {
+            u = fmaf(fx, t[0] / t[2], cx);
+            v = fmaf(fy, t[1] / t[2], cy);
+        }
+        const int inside = front && u >= -0.5f && u <= (float)Wc - 0.5f && v >= -0.5f && v <= (float)Hc - 0.5f;
+        const float uc = fminf(fmaxf(u, 0.0f), (float)(Wc - 1)), vc = fminf(fmaxf(v, 0.0f), (float)(Hc - 1));
+        const int j0 = (int)floorf(uc), i0 = (int)floorf(vc);
+        const int j1 = j0 + 1 < Wc ? j0 + 1 : Wc - 1, i1 = i0 + 1 < Hc ? i0 + 1 : Hc - 1;
+        const float b = uc - (float)j0, a = vc - (float)i0;
+        const long q00 = (long)i0 * Wc + j0, q01 = (long)i0 * Wc + j1, q10 = (long)i1 * Wc + j0, q11 = (long)i1 * Wc + j1;
+        {
+            const float r0 = fmaf(b, Ycam[q01] - Ycam[q00], Ycam[q00]);
+            const float r1 = fmaf(b, Ycam[q11] - Ycam[q10], Ycam[q10]);
+            Y[p] = fmaf(a, r1 - r0, r0);
+        }
+        const float z00 = Zcam[q00], z01 = Zcam[q01], z10 = Zcam[q10], z11 = Zcam[q11];
+        const int zok = isfinite(z00) && z00 > 0.0f && isfinite(z01) && z01 > 0.0f && isfinite(z10) && z10 > 0.0f &&
+                        isfinite(z11) && z11 > 0.0f;
+        if (inside && zok) {
+            const float r0 = fmaf(b, z01 - z00, z00);
+            const float r1 = fmaf(b, z11 - z10, z10);
+            D[p] = fmaf(a, r1 - r0, r0) / t[2];
+        } else {
+            D[p] = NAN;
+        }
+    }
+}

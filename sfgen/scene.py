@@ -135,6 +135,26 @@ def render(scene: Scene, dirs: np.ndarray, k: float, row_block: int = 256):
     return Y, D, Wg
 
 
+def camera_directions(Hc: int, Wc: int, K) -> np.ndarray:
+    """Unit ray directions [Hc][Wc][3] (float64) of a pinhole camera with intrinsics
+    K = (fx, fy, cx, cy), pixel centres at integer coordinates, looking along +z."""
+    fx, fy, cx, cy = (float(x) for x in K)
+    u = (np.arange(Wc, dtype=np.float64) - cx) / fx
+    v = (np.arange(Hc, dtype=np.float64) - cy) / fy
+    U, V = np.meshgrid(u, v)
+    d = np.stack([U, V, np.ones_like(U)], -1)
+    return d / np.linalg.norm(d, axis=-1, keepdims=True)
+
+
+def render_camera(scene: "Scene", Hc: int, Wc: int, K, k: float):
+    """Frame k as a pinhole camera sees it: brightness [Hc][Wc] and z-DEPTH [Hc][Wc] (range
+    times the ray's z component; +inf where the ray hits nothing), float32."""
+    d = camera_directions(Hc, Wc, K)
+    Y, rng, _ = render(scene, d, k)
+    Z = (rng.astype(np.float64) * d[..., 2]).astype(np.float32)
+    return Y, Z
+
+
 def pixel_flow_max(geom64: np.ndarray, w: np.ndarray, margin: int = 0) -> float:
     """max over pixels of the tangent flow in pixels, |(b1.w, b2.w)| / ds."""
     b1 = geom64[..., 3:6]
