@@ -176,6 +176,20 @@ sf_status sf_flow_px(sf_ctx* ctx, float* tangent, float* normal);
  * stream.  Errors: SF_E_DATA (ctx or w_gt NULL), SF_E_STATE (fresh context), SF_E_CUDA. */
 sf_status sf_eval(sf_ctx* ctx, const float* w_gt, float* rmse, double* aae_deg, double* mean_rmse, double* mean_aae);
 
+/* ---- Spherepix input mapping -----------------------------------------
+ * Resample a pinhole camera's measurements onto the context's grid (inside the paper's
+ * timed region; operator: DESIGN reading 31).  Ycam, Zcam: device [B][cam_height][cam_width]
+ * float32 brightness and z-DEPTH (distance along the optical axis; <= 0 or non-finite = no
+ * measurement).  K = {fx, fy, cx, cy} (host, pixel centres at integer coordinates); Rcg: host
+ * row-major 3x3 rotation grid -> camera frame, or NULL for the identity.  Per grid pixel s:
+ * t = Rcg s, (u, v) = (fx t.x/t.z + cx, fy t.y/t.z + cy); Y = bilinear brightness at (u, v)
+ * clamped to the image; lambda = bilinear z-depth / t.z (range along s), NaN (invalid) when
+ * t.z <= 0, (u, v) is outside the pixel footprint or a sample is invalid.  Outputs Y, D: device
+ * [B][H][W] (the inputs of sf_step).  Asynchronous on the context stream.
+ * Errors: SF_E_DATA (NULL pointer), SF_E_CONFIG (bad camera size or intrinsics). */
+sf_status sf_map_inputs(sf_ctx* ctx, const float* Ycam, const float* Zcam, int32_t cam_height, int32_t cam_width,
+                        const float* K, const float* Rcg, float* Y, float* D);
+
 /* ---- banded mode -------------------------------------------------------------------------
  * Halo rows a band needs so that its owned rows are exact after one sf_step: the transport
  * moves information N rows per frame (eq:numerical_stability), the update reads +-2 rows of

@@ -25,7 +25,7 @@ SF_ABI_VERSION = 1
 EXPORTS = ("sf_config_default", "sf_create", "sf_destroy", "sf_predict", "sf_update", "sf_step", "sf_step_host",
            "sf_get_fields", "sf_set_fields", "sf_status_flags", "sf_kernel_in_use", "sf_launches_per_step",
            "sf_error_string", "sf_band_halo", "sf_band_partition", "sf_halo_exchange_peer", "sf_halo_exchange_nccl",
-           "sf_nccl_unique_id", "sf_nccl_comm_init", "sf_nccl_comm_destroy", "sf_flow_px", "sf_eval")
+           "sf_nccl_unique_id", "sf_nccl_comm_init", "sf_nccl_comm_destroy", "sf_flow_px", "sf_eval", "sf_map_inputs")
 
 
 class sf_config(C.Structure):
@@ -77,10 +77,11 @@ def _load():
     lib.sf_nccl_comm_destroy.restype = None
     lib.sf_flow_px.argtypes = [P, P, P]
     lib.sf_eval.argtypes = [P, P, P, P, P, P]
+    lib.sf_map_inputs.argtypes = [P, P, P, C.c_int32, C.c_int32, P, P, P, P]
     for name in ("sf_create", "sf_predict", "sf_update", "sf_step", "sf_step_host", "sf_get_fields",
                  "sf_set_fields", "sf_status_flags", "sf_kernel_in_use", "sf_launches_per_step", "sf_band_halo",
                  "sf_band_partition", "sf_halo_exchange_peer", "sf_halo_exchange_nccl", "sf_nccl_unique_id",
-                 "sf_nccl_comm_init", "sf_flow_px", "sf_eval"):
+                 "sf_nccl_comm_init", "sf_flow_px", "sf_eval", "sf_map_inputs"):
         getattr(lib, name).restype = C.c_int
     return lib
 
@@ -144,6 +145,16 @@ def sf_eval(ctx: int, wgt_ptr: int, rmse_ptr: int | None, aae_ptr: int | None, m
             mean_aae_ptr: int | None) -> None:
     _check(_lib.sf_eval(C.c_void_p(ctx), C.c_void_p(wgt_ptr), C.c_void_p(rmse_ptr), C.c_void_p(aae_ptr),
                         C.c_void_p(mean_rmse_ptr), C.c_void_p(mean_aae_ptr)), "sf_eval")
+
+
+def sf_map_inputs(ctx: int, ycam_ptr: int, zcam_ptr: int, cam_height: int, cam_width: int, K, Rcg,
+                  y_ptr: int, d_ptr: int) -> None:
+    """K: 4 floats (fx, fy, cx, cy); Rcg: 9 floats (row-major grid -> camera) or None."""
+    Kc = (C.c_float * 4)(*[float(x) for x in K])
+    Rc = (C.c_float * 9)(*[float(x) for x in list(Rcg)]) if Rcg is not None else None
+    _check(_lib.sf_map_inputs(C.c_void_p(ctx), C.c_void_p(ycam_ptr), C.c_void_p(zcam_ptr), cam_height, cam_width,
+                              C.cast(Kc, C.c_void_p), C.cast(Rc, C.c_void_p) if Rc is not None else None,
+                              C.c_void_p(y_ptr), C.c_void_p(d_ptr)), "sf_map_inputs")
 
 
 def sf_set_fields(ctx: int, w_ptr: int, rho_ptr: int, yhat_ptr: int | None) -> None:
@@ -311,6 +322,18 @@ class StructureFlow:
         sf_eval(self.ctx, self._in3(w_gt), rm.data_ptr() if rasters else None, aa.data_ptr() if rasters else None,
                 C.addressof(mr), C.addressof(ma))
         return {"rmse": rm, "aae_deg": aa, "mean_rmse": list(mr), "mean_aae_deg": list(ma)}
+
+    def map_inputs(self, Ycam, Zcam, K, Rcg=None):
+        """Camera brightness / z-depth (device [B][Hc][Wc]) -> grid (Y, depth) device tensors."""
+        t = self.torch
+        assert Ycam.is_cuda and Ycam.dtype == t.float32 and Ycam.is_contiguous() and Zcam.shape == Ycam.shape
+        Hc, Wc = Ycam.shape[-2:]
+        Y = t.empty((self.B, self.H, self.W), dtype=t.float32, device=self.device)
+        D = t.empty_like(Y)
+        Rf = None if Rcg is None else [float(x) for x in (Rcg.flatten() if hasattr(Rcg, "flatten") else Rcg)]
+        sf_map_inputs(self.ctx, Ycam.data_ptr(), Zcam.contiguous().data_ptr(), Hc, Wc, K, Rf, Y.data_ptr(),
+                      D.data_ptr())
+        return Y, D
 
     def set_fields(self, w, rho, yhat=None):
         sf_set_fields(self.ctx, self._in3(w), self._in(rho), self._in(yhat) if yhat is not None else None)
