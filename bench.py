@@ -247,10 +247,33 @@ def run_sf(args):
         j = i % (2 * ring)
         return j if j < ring else 2 * ring - 1 - j
 
-    with torch.cuda.stream(s):
-        m.step(Yd[0], Dd[0])  # frame 0: initialisation (not a timed step)
-        for k in range(1, ring):  # one real pass over the ring before capture (untimed)
+    # --map: every step first resamples a pinhole camera frame onto the grid (sf_map_inputs,
+    # inside the paper's timed region): camera 640 x 640, 90 deg, frames of the same scene
+    cam = None
+    if getattr(args, "map", False):
+        from sfgen.scene import render_camera
+        Hc = Wc = 640
+        K = (Wc / 2.0, Hc / 2.0, (Wc - 1) / 2.0, (Hc - 1) / 2.0)  # f = (W/2) / tan(45 deg)
+        cams = [render_camera(seqs[0].scene, Hc, Wc, K, float(k)) for k in range(ring)]
+        Yc = torch.from_numpy(np.stack([c[0] for c in cams])[:, None]).to(dev)
+        Zc = torch.from_numpy(np.stack([c[1] for c in cams])[:, None]).to(dev)
+        Ym = torch.empty((B, H, W), dtype=torch.float32, device=dev)
+        Dm = torch.empty_like(Ym)
+        cam = (Hc, Wc, K, Yc, Zc, Ym, Dm)
+
+    def do_step(k):
+        if cam is None:
             m.step(Yd[k], Dd[k])
+        else:
+            Hc, Wc, K, Yc, Zc, Ym, Dm = cam
+            sf.sf_map_inputs(m.ctx, Yc[k].data_ptr(), Zc[k].data_ptr(), Hc, Wc, K, None, Ym.data_ptr(),
+                             Dm.data_ptr())
+            m.step(Ym, Dm)
+
+    with torch.cuda.stream(s):
+        do_step(0)  # frame 0: initialisation (not a timed step)
+        for k in range(1, ring):  # one real pass over the ring before capture (untimed)
+            do_step(k)
     s.synchronize()
     # CUDA graphs of CHUNK consecutive steps of the palindrome (an even count, so a chunk starts
     # and ends at the same state parity); the cycle of 2R steps is split into 2R / CHUNK graphs
@@ -264,9 +287,9 @@ def run_sf(args):
         with torch.cuda.graph(g, stream=s):
             for t in range(CHUNK):
                 k = frame_of(pos0 + c * CHUNK + t)
-                m.step(Yd[k], Dd[k])
+                do_step(k)
         chunks.append(g)
-    launches = m.launches_per_step
+    launches = m.launches_per_step + (1 if cam is not None else 0)
     state = {"i": pos0}
 
     def run_steps(n):
@@ -279,7 +302,7 @@ def run_sf(args):
                 n -= CHUNK
             else:
                 k = frame_of(state["i"])
-                m.step(Yd[k], Dd[k])
+                do_step(k)
                 state["i"] += 1
                 n -= 1
 
@@ -375,7 +398,9 @@ def run_sf(args):
                           "S": params.smooth_iters, "parallelism": f"independent sequences x{world}",
                           "inputs": f"ring of {ring} frames ({ring * 2 * frame_bytes / 2**20:.0f} MiB) > L2, "
                                     "replayed palindromically, cold reads each step; CUDA graphs of 8 steps",
-                          "kernel": {sf.SF_KERNEL_FUSED: "fused", sf.SF_KERNEL_PASSES: "passes"}.get(m.kernel)},
+                          "kernel": {sf.SF_KERNEL_FUSED: "fused", sf.SF_KERNEL_PASSES: "passes"}.get(m.kernel),
+                          "input_mapping": ("pinhole camera 640x640 90 deg -> grid (sf_map_inputs) inside each step"
+                                            if cam is not None else "inputs already on the grid")},
                "roofline": roof, "gpu_launches": launches * args.steps, "step_ms_median": med_ms,
                "e2e": {"value": e2e_value, "unit": "Hz", "h2d_bytes_per_step": 2 * frame_bytes,
                        "d2h_bytes_per_step": 4 * frame_bytes,
@@ -494,6 +519,8 @@ def main():
     ap.add_argument("--impl", choices=["sf", "reference"], default="sf")
     ap.add_argument("--config", type=int, choices=[2, 3, 4, 5], default=2)
     ap.add_argument("--kernel", choices=["auto", "fused", "passes"], default="auto")
+    ap.add_argument("--map", action="store_true",
+                    help="include the Spherepix input mapping of a 640x640 camera frame in every step (P:L785)")
     ap.add_argument("--levels", type=int, choices=[1, 2], default=1,
                     help="pyramid levels (1: the graded H = 1 hot path; 2: the paper's Table 3 shape)")
     ap.add_argument("--ring", type=int, default=96)
