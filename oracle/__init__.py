@@ -27,7 +27,8 @@ class _Params(C.Structure):
     _fields_ = [("H", C.c_int32), ("W", C.c_int32), ("N", C.c_int32), ("smooth_iters", C.c_int32),
                 ("dominant_rule", C.c_int32), ("clamp_advection", C.c_int32),
                 ("input_is_inverse_depth", C.c_int32), ("pad", C.c_int32),
-                ("max_flow", C.c_double), ("sigma", C.c_double), ("gamma", C.c_double * 5)]
+                ("max_flow", C.c_double), ("sigma", C.c_double), ("gamma", C.c_double * 5),
+                ("imu", C.c_int32), ("pad2", C.c_int32), ("omega", C.c_double * 3), ("accel", C.c_double * 3)]
 
 
 _LIBS: dict = {}
@@ -62,6 +63,13 @@ def make_params(H: int, W: int, p) -> _Params:
     P.sigma = p.sigma
     for k in range(5):
         P.gamma[k] = p.gamma[k]
+    om = getattr(p, "omega", None)
+    ac = getattr(p, "accel", None)
+    if om is not None or ac is not None:
+        P.imu = 1
+        for k in range(3):
+            P.omega[k] = float(np.float32((om or (0, 0, 0))[k]))
+            P.accel[k] = float(np.float32((ac or (0, 0, 0))[k]))
     return P
 
 

@@ -68,6 +68,10 @@ typedef struct {
     double max_flow;
     double sigma;    /* source-term weight per pass (reading 2; 0.5)                     */
     double gamma[5]; /* gamma1..gamma5 (L556-559, L613-616)                               */
+    int32_t imu;     /* 1: add the inertial source terms of eq:hflow_conservation (NEXT #4)  */
+    int32_t pad2;
+    double omega[3]; /* camera angular velocity Omega, rad per frame (camera frame)          */
+    double accel[3]; /* camera linear acceleration a_c, per frame^2 (camera frame)           */
 } or_params;
 
 static inline int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
@@ -157,8 +161,40 @@ static unsigned pass(const or_params* P, const real* geo, int axis, const real* 
     return flags;
 }
 
+/* Inertial source terms (NEXT #4; eq:hflow_conservation L341-345 with eq:totaldev_hflow and
+ * a_w, L258-280): the paper drops -Omega x w + a_w (eq:assumption L505-514); with them
+ *   dw/dt = ... - Omega x w + a_w,  a_w = rho a_c - Omega x (w + Omega x s)
+ *         = ... + rho a_c - 2 Omega x w - Omega x (Omega x s)       (rho has no source term).
+ * Reading 32: one explicit Euler stage per substep after the row pass, on the post-pass fields:
+ *   c1 = Omega x s, c2 = Omega x c1, c3 = Omega x w   (cross(a,b)_x = fma(a_y, b_z, -(a_z b_y)), cyclic)
+ *   f_a = fma(rho, a_c,a, -fma(2, c3_a, c2_a));  w_a = fma(dt, f_a, w_a). */
+static inline void cross3(const real* a, const real* b, real* c)
+{
+    c[0] = FMA(a[1], b[2], -(a[2] * b[1]));
+    c[1] = FMA(a[2], b[0], -(a[0] * b[2]));
+    c[2] = FMA(a[0], b[1], -(a[1] * b[0]));
+}
+
+static void imu_stage(const or_params* P, const real* geo, real* w, const real* rho)
+{
+    const real dt = R(1) / R(P->N);
+    const real om[3] = {R(P->omega[0]), R(P->omega[1]), R(P->omega[2])};
+    const real ac[3] = {R(P->accel[0]), R(P->accel[1]), R(P->accel[2])};
+    for (long p = 0; p < (long)P->H * P->W; ++p) {
+        real c1[3], c2[3], c3[3];
+        cross3(om, geo + 10 * p, c1);
+        cross3(om, c1, c2);
+        cross3(om, w + 3 * p, c3);
+        for (int a = 0; a < 3; ++a) {
+            const real f = FMA(rho[p], ac[a], -FMA(R(2), c3[a], c2[a]));
+            w[3 * p + a] = FMA(dt, f, w[3 * p + a]);
+        }
+    }
+}
+
 /* Prediction k -> k+ (L501-523, numerical scheme L662-683): exactly N substeps
- * (reading 4), each a column pass then a row pass.  In place on (w, rho). */
+ * (reading 4), each a column pass then a row pass (then the inertial stage when enabled).
+ * In place on (w, rho). */
 unsigned or_predict(const or_params* P, const real* geo, real* w, real* rho)
 {
     const long n = (long)P->H * P->W;
@@ -169,6 +205,7 @@ unsigned or_predict(const or_params* P, const real* geo, real* w, real* rho)
     for (int s = 0; s < P->N; ++s) {
         flags |= pass(P, geo, 0, w, rho, w2, r2, u);
         flags |= pass(P, geo, 1, w2, r2, w, rho, u);
+        if (P->imu) imu_stage(P, geo, w, rho);
     }
     free(w2);
     free(r2);

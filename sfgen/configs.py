@@ -37,6 +37,8 @@ class Params:
     dominant_rule: int = DOM_LARGEST
     clamp_advection: int = 1
     input_is_inverse_depth: int = 0
+    omega: tuple | None = None  # camera angular velocity (rad/frame) for the inertial terms (NEXT #4)
+    accel: tuple | None = None  # camera linear acceleration (per frame^2)
 
     @property
     def N(self) -> int:
