@@ -159,6 +159,17 @@ sf_status sf_set_fields(sf_ctx* ctx, const float* w, const float* rho, const flo
  * SF_E_STABILITY if SF_FLAG_CFL is set, else SF_OK. */
 sf_status sf_status_flags(sf_ctx* ctx, uint32_t* flags, int32_t clear);
 
+/* ---- inertial source terms -------------------------------------------
+ * Camera motion for the following frames (until changed): omega = camera angular velocity
+ * Omega (rad per frame), accel = camera linear acceleration a_c (per frame^2, the units of
+ * rho a_c being those of w per frame), both host float[3] in the camera frame; NULL = zero.
+ * With either given, every prediction substep ends with the explicit stage
+ * w += dt (rho a_c - 2 Omega x w - Omega x (Omega x s)) of the terms eq:assumption drops
+ * (-Omega x w + a_w, eq:hflow_conservation, eq:totaldev_hflow P:L258-280, P:L341-345;
+ * DESIGN reading 32); both NULL switches them off (the paper's predictor).  One motion for
+ * all batch members.  Errors: SF_E_DATA, SF_E_CONFIG (non-finite), SF_E_UNSUPPORTED (levels 2). */
+sf_status sf_set_motion(sf_ctx* ctx, const float* omega, const float* accel);
+
 /* ---- evaluation outputs ----------------------------------------------
  * Tangent and normal flow of the current state w^k in pixels per frame: tangent [B][H][W][2] =
  * B^T P(s) w / ds (eq:tangent_flow), evaluated as (e1 . t, e2 . t) with

@@ -25,7 +25,7 @@ SF_ABI_VERSION = 1
 EXPORTS = ("sf_config_default", "sf_create", "sf_destroy", "sf_predict", "sf_update", "sf_step", "sf_step_host",
            "sf_get_fields", "sf_set_fields", "sf_status_flags", "sf_kernel_in_use", "sf_launches_per_step",
            "sf_error_string", "sf_band_halo", "sf_band_partition", "sf_halo_exchange_peer", "sf_halo_exchange_nccl",
-           "sf_nccl_unique_id", "sf_nccl_comm_init", "sf_nccl_comm_destroy", "sf_flow_px", "sf_eval", "sf_map_inputs")
+           "sf_nccl_unique_id", "sf_nccl_comm_init", "sf_nccl_comm_destroy", "sf_flow_px", "sf_eval", "sf_map_inputs", "sf_set_motion")
 
 
 class sf_config(C.Structure):
@@ -78,10 +78,11 @@ def _load():
     lib.sf_flow_px.argtypes = [P, P, P]
     lib.sf_eval.argtypes = [P, P, P, P, P, P]
     lib.sf_map_inputs.argtypes = [P, P, P, C.c_int32, C.c_int32, P, P, P, P]
+    lib.sf_set_motion.argtypes = [P, P, P]
     for name in ("sf_create", "sf_predict", "sf_update", "sf_step", "sf_step_host", "sf_get_fields",
                  "sf_set_fields", "sf_status_flags", "sf_kernel_in_use", "sf_launches_per_step", "sf_band_halo",
                  "sf_band_partition", "sf_halo_exchange_peer", "sf_halo_exchange_nccl", "sf_nccl_unique_id",
-                 "sf_nccl_comm_init", "sf_flow_px", "sf_eval", "sf_map_inputs"):
+                 "sf_nccl_comm_init", "sf_flow_px", "sf_eval", "sf_map_inputs", "sf_set_motion"):
         getattr(lib, name).restype = C.c_int
     return lib
 
@@ -155,6 +156,14 @@ def sf_map_inputs(ctx: int, ycam_ptr: int, zcam_ptr: int, cam_height: int, cam_w
     _check(_lib.sf_map_inputs(C.c_void_p(ctx), C.c_void_p(ycam_ptr), C.c_void_p(zcam_ptr), cam_height, cam_width,
                               C.cast(Kc, C.c_void_p), C.cast(Rc, C.c_void_p) if Rc is not None else None,
                               C.c_void_p(y_ptr), C.c_void_p(d_ptr)), "sf_map_inputs")
+
+
+def sf_set_motion(ctx: int, omega=None, accel=None) -> None:
+    """omega, accel: 3 floats each (camera frame) or None."""
+    om = (C.c_float * 3)(*[float(x) for x in omega]) if omega is not None else None
+    ac = (C.c_float * 3)(*[float(x) for x in accel]) if accel is not None else None
+    _check(_lib.sf_set_motion(C.c_void_p(ctx), C.cast(om, C.c_void_p) if om is not None else None,
+                              C.cast(ac, C.c_void_p) if ac is not None else None), "sf_set_motion")
 
 
 def sf_set_fields(ctx: int, w_ptr: int, rho_ptr: int, yhat_ptr: int | None) -> None:
@@ -273,6 +282,8 @@ class StructureFlow:
         self.cfg = cfg
         torch.cuda.synchronize(self.device)
         self.ctx = sf_create(cfg, g.data_ptr())
+        if getattr(params, "omega", None) is not None or getattr(params, "accel", None) is not None:
+            sf_set_motion(self.ctx, params.omega or (0.0, 0.0, 0.0), params.accel or (0.0, 0.0, 0.0))
 
     def __del__(self):
         ctx = getattr(self, "ctx", None)

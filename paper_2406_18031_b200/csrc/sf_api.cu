@@ -377,6 +377,23 @@ extern "C" sf_status sf_status_flags(sf_ctx* c, uint32_t* flags, int32_t clear) 
     return (h & SF_FLAG_CFL) ? SF_E_STABILITY : SF_OK;
 }
 
+extern "C" sf_status sf_set_motion(sf_ctx* c, const float* omega, const float* accel) {
+    if (!c) return SF_E_DATA;
+    if (c->levels == 2) return SF_E_UNSUPPORTED;
+    FrameParams& f = c->fp;
+    if (!omega && !accel) {
+        f.imu = 0;
+        return SF_OK;
+    }
+    for (int k = 0; k < 3; ++k) {
+        f.om[k] = omega ? omega[k] : 0.0f;
+        f.ac[k] = accel ? accel[k] : 0.0f;
+        if (!isfinite(f.om[k]) || !isfinite(f.ac[k])) return SF_E_CONFIG;
+    }
+    f.imu = 1;
+    return SF_OK;
+}
+
 extern "C" int32_t sf_kernel_in_use(const sf_ctx* c) { return c ? c->kernel : 0; }
 
 extern "C" int32_t sf_launches_per_step(const sf_ctx* c) {

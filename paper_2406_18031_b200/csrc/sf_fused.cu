@@ -378,6 +378,13 @@ __device__ __forceinline__ void transport_passes(const FrameParams& f, int M, fl
             row_update(0, vt, v[1], t, o1);
             row_update(K - 1, v[K - 2], vb, oK, bb);
         }
+        if (f.imu) {  // inertial stage after the row pass (reading 32), per cell
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                imu_stage(f, SX[k].x, SY[k].x, SZ[k].x, W[0][k].x, W[1][k].x, W[2][k].x, W[3][k].x);
+                imu_stage(f, SX[k].y, SY[k].y, SZ[k].y, W[0][k].y, W[1][k].y, W[2][k].y, W[3][k].y);
+            }
+        }
         // (row passes keep column replicas valid; the next column pass keeps row replicas as
         //  they are and they are refreshed again before the next row pass)
     }

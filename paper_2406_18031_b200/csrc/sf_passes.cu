@@ -71,6 +71,10 @@ __global__ void __launch_bounds__(BX* BY) k_pass(const float4* __restrict__ in, 
     const bool own = live && i >= f.fr0 && i < f.fr1;  // banded mode: owned rows only
     raise_flag(flags, own && clamped, SF_FLAG_CLAMPED);
     raise_flag(flags, own && cfl, SF_FLAG_CFL);
+    if (AXIS == 1 && f.imu) {  // inertial stage after the row pass (reading 32)
+        const float4 sg = G0[g];
+        imu_stage(f, sg.x, sg.y, sg.z, o.x, o.y, o.z, o.w);
+    }
     if (live) out[base + g] = o;
 }
 
