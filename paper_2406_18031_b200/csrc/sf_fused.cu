@@ -223,15 +223,15 @@ __device__ __forceinline__ void transport_passes(const FrameParams& f, int M, fl
     const int keT = rmin - r0, keB = rmax - r0;                // edge rows in this thread's run
 
     // dominant flow of both cells -> flag max, clamp, (|u_hat0|, |u_hat1|)
+    // (the clamp keeps the sign since U > 0, and |clamp(u, -U, U)| = min(|u|, U) -- also for a
+    //  NaN u_hat, which the clamp turns into -U: upwind side "not > 0", weight U)
     auto flow = [&](int k, float uh0, float uh1, bool& p0, bool& p1) -> float2 {
-        mx[k] = fmaxf(mx[k], fmaxf(fabsf(uh0), in1 ? fabsf(uh1) : 0.0f));
-        if (CLAMP) {
-            uh0 = fminf(fmaxf(uh0, -U), U);
-            uh1 = fminf(fmaxf(uh1, -U), U);
-        }
         p0 = uh0 > 0.0f;
         p1 = uh1 > 0.0f;
-        return make_float2(fabsf(uh0), fabsf(uh1));
+        const float a0 = fabsf(uh0), a1 = fabsf(uh1);
+        mx[k] = fmaxf(mx[k], fmaxf(a0, in1 ? a1 : 0.0f));
+        if (CLAMP) return make_float2(fminf(a0, U), fminf(a1, U));
+        return make_float2(a0, a1);
     };
 
     for (int n = 0; n < M; ++n) {
