@@ -195,6 +195,58 @@ __device__ __forceinline__ float2 sel2(bool p0, bool p1, float2 a, float2 b) {
     return make_float2(p0 ? a.x : b.x, p1 ? a.y : b.y);
 }
 
+// Cell-paired update arithmetic (the order of sf_internal.cuh's tap_g / tap_h / ls_solve3 per
+// lane of the pair; reciprocals stay scalar __frcp_rn).
+__device__ __forceinline__ float2 bc2(float x) { return make_float2(x, x); }
+__device__ __forceinline__ float2 neg2(float2 a) { return make_float2(-a.x, -a.y); }
+__device__ __forceinline__ float2 tap2_g(float2 x0, float2 x1, float2 x2, float2 x3, float2 x4) {
+    float2 a = mul2(bc2(SF_G0), x0);
+    a = fma2(bc2(SF_G1), x1, a);
+    a = fma2(bc2(SF_G2), x2, a);
+    a = fma2(bc2(SF_G1), x3, a);
+    return fma2(bc2(SF_G0), x4, a);
+}
+__device__ __forceinline__ float2 tap2_h(float2 x0, float2 x1, float2 x2, float2 x3, float2 x4) {
+    float2 a = mul2(bc2(SF_H0), x0);
+    a = fma2(bc2(SF_H1), x1, a);
+    a = fma2(bc2(0.0f), x2, a);
+    a = fma2(bc2(SF_H3), x3, a);
+    return fma2(bc2(SF_H4), x4, a);
+}
+__device__ __forceinline__ float2 rcp2(float2 a) { return make_float2(__frcp_rn(a.x), __frcp_rn(a.y)); }
+__device__ __forceinline__ void ls_solve3x2(const float2 g[3], const float2 m[3], float2 cY, float2 cr,
+                                            const float2 wp[3], float g1, float2 g2, float g3, float2 x[3]) {
+    float2 g1g[3], g2m[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        g1g[a] = mul2(bc2(g1), g[a]);
+        g2m[a] = mul2(g2, m[a]);
+    }
+    const float2 G3 = bc2(g3);
+    const float2 A00 = add2(fma2(g2m[0], m[0], mul2(g1g[0], g[0])), G3);
+    const float2 A10 = fma2(g2m[1], m[0], mul2(g1g[1], g[0]));
+    const float2 A11 = add2(fma2(g2m[1], m[1], mul2(g1g[1], g[1])), G3);
+    const float2 A20 = fma2(g2m[2], m[0], mul2(g1g[2], g[0]));
+    const float2 A21 = fma2(g2m[2], m[1], mul2(g1g[2], g[1]));
+    const float2 A22 = add2(fma2(g2m[2], m[2], mul2(g1g[2], g[2])), G3);
+    float2 b[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) b[a] = fma2(neg2(g2m[a]), cr, fma2(neg2(g1g[a]), cY, mul2(G3, wp[a])));
+    const float2 r0 = rcp2(A00);
+    const float2 l10 = mul2(A10, r0), l20 = mul2(A20, r0);
+    const float2 d1 = fma2(neg2(l10), A10, A11);
+    const float2 r1 = rcp2(d1);
+    const float2 t = fma2(neg2(l20), A10, A21);
+    const float2 l21 = mul2(t, r1);
+    const float2 dd2 = fma2(neg2(l21), t, fma2(neg2(l20), A20, A22));
+    const float2 r2 = rcp2(dd2);
+    const float2 y1 = fma2(neg2(l10), b[0], b[1]);
+    const float2 y2 = fma2(neg2(l21), y1, fma2(neg2(l20), b[0], b[2]));
+    x[2] = mul2(y2, r2);
+    x[1] = fma2(neg2(l21), x[2], mul2(y1, r1));
+    x[0] = fma2(neg2(l20), x[2], fma2(neg2(l10), x[1], mul2(b[0], r0)));
+}
+
 // The transport: M substeps of a column pass then a row pass on the thread's
 // 2 x K cells, held cell-paired: W[0..2][k] = w (x, y, z), W[3][k] = rho, each a float2 over the
 // thread's two columns.  Grid borders (replicate clamp, reading 10) are handled by REPLICA cells:
@@ -627,67 +679,85 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
         }
         __syncthreads();
         SF_TICK();
-        // per-pixel LS on the solve region; the cell's global inputs (s, 1/ds^2, Y, rho^k) are
-        // fetched one cell ahead (L2 latency hidden behind the previous cell's solve)
+        // per-pixel LS on the solve region, two horizontally adjacent cells per iteration (the
+        // arithmetic cell-paired as f32x2; a ragged last pair computes its first cell twice and
+        // stores it once).  The pair's global inputs (s, ds^2, Y, rho^k) are fetched one pair ahead.
         {
-            const int nc = ((a.dbg_skip & 1024) ? clo - 1 : chi) - clo + 1, dr = NT / nc, dc = NT % nc;
-            int rn = rlo + tid / nc, cn = clo + tid % nc;
-            float4 s4n = make_float4(0.f, 0.f, 0.f, 0.f);
-            float yn = 0.f, skn = 0.f;
-            if (nc > 0 && rn <= rhi) {
-                const size_t g = (size_t)(gi0 + rn) * f.W + (gj0 + cn);
-                s4n = __ldg(a.G0 + g);
-                yn = __ldg(a.yin + plane + g);
-                skn = __ldg(&a.sk[plane + g].w);
-            }
+            const int ncol = ((a.dbg_skip & 1024) ? clo - 1 : chi) - clo + 1;
+            const int nc = (ncol + 1) >> 1, dr = nc > 0 ? NT / nc : 0, dc = nc > 0 ? NT % nc : 0;
+            int rn = nc > 0 ? rlo + tid / nc : rhi + 1, pn = nc > 0 ? tid % nc : 0;
+            auto fetch = [&](int r, int pc, float4& sa, float4& sb, float2& y, float2& sk) {
+                const int c = clo + 2 * pc, c1 = min(c + 1, chi);
+                const size_t ga = (size_t)(gi0 + r) * f.W + (gj0 + c), gb = (size_t)(gi0 + r) * f.W + (gj0 + c1);
+                sa = __ldg(a.G0 + ga);
+                sb = __ldg(a.G0 + gb);
+                y = make_float2(__ldg(a.yin + plane + ga), __ldg(a.yin + plane + gb));
+                sk = make_float2(__ldg(&a.sk[plane + ga].w), __ldg(&a.sk[plane + gb].w));
+            };
+            float4 san, sbn;
+            float2 yn, skn;
+            if (rn <= rhi) fetch(rn, pn, san, sbn, yn, skn);
 #pragma unroll 1
-            while (nc > 0 && rn <= rhi) {
-                const int r = rn, c = cn;
-                const float4 s4 = s4n;
-                const float ycur = yn, skcur = skn;
-                rn += dr + ((cn + dc > chi) ? 1 : 0);
-                cn = (cn + dc > chi) ? cn + dc - nc : cn + dc;
-                if (rn <= rhi) {
-                    const size_t gq = (size_t)(gi0 + rn) * f.W + (gj0 + cn);
-                    s4n = __ldg(a.G0 + gq);
-                    yn = __ldg(a.yin + plane + gq);
-                    skn = __ldg(&a.sk[plane + gq].w);
-                }
-                const int idx = r * RW + c;
-                const float g0 = HG[idx - 2 * RW], g1 = HG[idx - RW], g2 = HG[idx], g3 = HG[idx + RW], g4 = HG[idx + 2 * RW];
-                const float h0 = HH[idx - 2 * RW], h1 = HH[idx - RW], h2 = HH[idx], h3 = HH[idx + RW], h4 = HH[idx + 2 * RW];
-                const float yh = tap_g(g0, g1, g2, g3, g4);  // Yhat^{k+1}
-                const float be1 = tap_g(h0, h1, h2, h3, h4);
-                const float be2 = tap_h(g0, g1, g2, g3, g4);
-                const float rc = Ds[idx], rl = Ds[idx - 1], rr = Ds[idx + 1], ru = Ds[idx - RW], rd = Ds[idx + RW];
-                const bool vc = !isnan(rc), vl = !isnan(rl), vr = !isnan(rr), vu = !isnan(ru), vd = !isnan(rd);
-                const float rh = vc ? rc : 0.0f;
-                const float br1 = pick_side(rh, vc, rl, vl, rr, vr);  // eq:dominant_b1
-                const float br2 = pick_side(rh, vc, ru, vu, rd, vd);  // eq:dominant_b2
-                const size_t g = (size_t)(gi0 + r) * f.W + (gj0 + c);
-                const float d2 = s4.w;
-                const float e1a[3] = {Es[idx], Es[P + idx], Es[2 * P + idx]};
-                const float e2a[3] = {Es[3 * P + idx], Es[4 * P + idx], Es[5 * P + idx]};
-                const float sa[3] = {s4.x, s4.y, s4.z};
-                float gh[3], m[3];
-                const float d2r = xmul(d2, rh);
-    #pragma unroll
+            while (rn <= rhi) {
+                const int r = rn, c = clo + 2 * pn;
+                const float4 sA = san, sB = sbn;
+                const float2 ycur = yn, skcur = skn;
+                rn += dr + ((pn + dc >= nc) ? 1 : 0);
+                pn = (pn + dc >= nc) ? pn + dc - nc : pn + dc;
+                if (rn <= rhi) fetch(rn, pn, san, sbn, yn, skn);
+                const bool full = c + 1 <= chi;
+                const int idx = r * RW + c;  // even: 8-byte aligned pairs (reads past chi are harmless)
+                auto ld2 = [&](const float* pl, int i) { return *reinterpret_cast<const float2*>(pl + i); };
+                const float2 g0 = ld2(HG, idx - 2 * RW), g1 = ld2(HG, idx - RW), g2 = ld2(HG, idx),
+                             g3 = ld2(HG, idx + RW), g4 = ld2(HG, idx + 2 * RW);
+                const float2 h0 = ld2(HH, idx - 2 * RW), h1 = ld2(HH, idx - RW), h2 = ld2(HH, idx),
+                             h3 = ld2(HH, idx + RW), h4 = ld2(HH, idx + 2 * RW);
+                const float2 yh = tap2_g(g0, g1, g2, g3, g4);  // Yhat^{k+1}
+                const float2 be1 = tap2_g(h0, h1, h2, h3, h4);
+                const float2 be2 = tap2_h(g0, g1, g2, g3, g4);
+                const float2 rc = ld2(Ds, idx), ru = ld2(Ds, idx - RW), rd = ld2(Ds, idx + RW);
+                const float rl = Ds[idx - 1], rr = Ds[idx + 2];
+                const bool vc0 = !isnan(rc.x), vc1 = !isnan(rc.y);
+                const float2 rh = make_float2(vc0 ? rc.x : 0.0f, vc1 ? rc.y : 0.0f);
+                // eq:dominant_b1 / b2 per cell (the pair's cells are each other's row neighbour)
+                const float2 br1 = make_float2(pick_side(rh.x, vc0, rl, !isnan(rl), rc.y, vc1),
+                                               pick_side(rh.y, vc1, rc.x, vc0, rr, !isnan(rr)));
+                const float2 br2 = make_float2(pick_side(rh.x, vc0, ru.x, !isnan(ru.x), rd.x, !isnan(rd.x)),
+                                               pick_side(rh.y, vc1, ru.y, !isnan(ru.y), rd.y, !isnan(rd.y)));
+                const float2 d2 = make_float2(sA.w, sB.w);
+                const float2 e1a[3] = {ld2(Es, idx), ld2(Es, P + idx), ld2(Es, 2 * P + idx)};
+                const float2 e2a[3] = {ld2(Es, 3 * P + idx), ld2(Es, 4 * P + idx), ld2(Es, 5 * P + idx)};
+                const float2 sp[3] = {make_float2(sA.x, sB.x), make_float2(sA.y, sB.y), make_float2(sA.z, sB.z)};
+                float2 gh[3], m[3];
+                const float2 d2r = mul2(d2, rh);
+#pragma unroll
                 for (int q = 0; q < 3; ++q) {
-                    gh[q] = xmul(d2, xfma(e2a[q], be2, xmul(e1a[q], be1)));
-                    const float dr = xmul(d2, xfma(e2a[q], br2, xmul(e1a[q], br1)));
-                    m[q] = xfma(d2r, sa[q], dr);
+                    gh[q] = mul2(d2, fma2(e2a[q], be2, mul2(e1a[q], be1)));
+                    const float2 drq = mul2(d2, fma2(e2a[q], br2, mul2(e1a[q], br1)));
+                    m[q] = fma2(d2r, sp[q], drq);
                 }
-                const float cY = xmul(d2, xsub(yh, ycur));   // eq:img_cost_top
-                const float cr = xmul(d2, xsub(rh, skcur));  // eq:invdepth_cost_top
-                const float wp[3] = {Fx[idx], Fy[idx], Fz[idx]};
-                float x[3];
-                ls_solve3(gh, m, cY, cr, wp, f.g1, vc ? f.g2 : 0.0f, f.g3, x);
-                Fx[idx] = x[0];
-                Fy[idx] = x[1];
-                Fz[idx] = x[2];
-                if (!(isfinite(x[0]) && isfinite(x[1]) && isfinite(x[2])) && gi0 + r >= f.fr0 && gi0 + r < f.fr1)
-                    fl |= SF_FLAG_NONFINITE;
-                if (r >= R && r < R + TH && c >= R && c < R + TW) a.yout[plane + g] = yh;
+                const float2 cY = mul2(d2, sub2(yh, ycur));   // eq:img_cost_top
+                const float2 cr = mul2(d2, sub2(rh, skcur));  // eq:invdepth_cost_top
+                const float2 wp[3] = {ld2(Fx, idx), ld2(Fy, idx), ld2(Fz, idx)};
+                float2 x[3];
+                ls_solve3x2(gh, m, cY, cr, wp, f.g1, make_float2(vc0 ? f.g2 : 0.0f, vc1 ? f.g2 : 0.0f), f.g3, x);
+                const bool bad0 = !(isfinite(x[0].x) && isfinite(x[1].x) && isfinite(x[2].x));
+                const bool bad1 = full && !(isfinite(x[0].y) && isfinite(x[1].y) && isfinite(x[2].y));
+                if (full) {
+                    *reinterpret_cast<float2*>(Fx + idx) = x[0];
+                    *reinterpret_cast<float2*>(Fy + idx) = x[1];
+                    *reinterpret_cast<float2*>(Fz + idx) = x[2];
+                } else {
+                    Fx[idx] = x[0].x;
+                    Fy[idx] = x[1].x;
+                    Fz[idx] = x[2].x;
+                }
+                if ((bad0 || bad1) && gi0 + r >= f.fr0 && gi0 + r < f.fr1) fl |= SF_FLAG_NONFINITE;
+                if (r >= R && r < R + TH) {
+                    const size_t g = plane + (size_t)(gi0 + r) * f.W + (gj0 + c);
+                    if (c >= R && c < R + TW) a.yout[g] = yh.x;
+                    if (full && c + 1 >= R && c + 1 < R + TW) a.yout[g + 1] = yh.y;
+                }
             }
         }
         // ---- S x 5x5 box (reading 13) as a register-tiled 2-D stencil: one work item = one
