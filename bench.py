@@ -340,26 +340,39 @@ def run_sf(args):
     st, flags = sf.sf_status_flags(m.ctx)
 
     # ---- end to end through the host-buffer C-ABI call (pinned host memory), same metric
-    e2e_steps = max(3, min(args.steps, 200))
+    e2e_steps = max(3, min(args.steps, 400))
     Yp = torch.empty((ring, B, H, W), dtype=torch.float32, pin_memory=True)
     Dp = torch.empty_like(Yp).pin_memory()
     Yp.copy_(Yd.cpu())
     Dp.copy_(Dd.cpu())
-    w_out = torch.empty((B, H, W, 3), dtype=torch.float32, pin_memory=True)
-    r_out = torch.empty((B, H, W), dtype=torch.float32, pin_memory=True)
-    for i in range(3):
-        sf.sf_step_host(m.ctx, Yp[i].data_ptr(), Dp[i].data_ptr(), w_out.data_ptr(), r_out.data_ptr())
+    # two pinned result sets: frame k's w, rho land in set k % 2 (the pipelined API overlaps
+    # frame k's copies with frame k-1's output copies and frame k+1's input copies)
+    w_out = [torch.empty((B, H, W, 3), dtype=torch.float32, pin_memory=True) for _ in range(2)]
+    r_out = [torch.empty((B, H, W), dtype=torch.float32, pin_memory=True) for _ in range(2)]
+
+    def e2e_run(n, fn):
+        for i in range(n):
+            k = frame_of(state["i"])
+            state["i"] += 1
+            fn(m.ctx, Yp[k].data_ptr(), Dp[k].data_ptr(), w_out[i % 2].data_ptr(), r_out[i % 2].data_ptr())
+        sf.sf_wait(m.ctx)
+
+    e2e_run(4, sf.sf_step_host_async)
+    e2e_run(2, sf.sf_step_host)
     if world > 1:
         dist.barrier()
     t0 = time.perf_counter()
-    for i in range(e2e_steps):
-        k = frame_of(state["i"])
-        state["i"] += 1
-        sf.sf_step_host(m.ctx, Yp[k].data_ptr(), Dp[k].data_ptr(), w_out.data_ptr(), r_out.data_ptr())
+    e2e_run(e2e_steps, sf.sf_step_host_async)
     e2e_s = torch.tensor([time.perf_counter() - t0], device=dev)
+    t0 = time.perf_counter()
+    sync_steps = max(3, e2e_steps // 4)
+    e2e_run(sync_steps, sf.sf_step_host)
+    sync_s = torch.tensor([time.perf_counter() - t0], device=dev)
     if world > 1:
         dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
+        dist.all_reduce(sync_s, op=dist.ReduceOp.MAX)
     e2e_value = world * B * e2e_steps / float(e2e_s.item())
+    e2e_sync_value = world * B * sync_steps / float(sync_s.item())
 
     if rank == 0:
         value = world * B * args.steps / (total_ms / 1e3)
@@ -404,7 +417,10 @@ def run_sf(args):
                "roofline": roof, "gpu_launches": launches * args.steps, "step_ms_median": med_ms,
                "e2e": {"value": e2e_value, "unit": "Hz", "h2d_bytes_per_step": 2 * frame_bytes,
                        "d2h_bytes_per_step": 4 * frame_bytes,
-                       "note": "sf_step_host: pinned Y,lambda H2D + step + w,rho D2H + stream sync per frame"},
+                       "note": "sf_step_host_async per frame (pinned Y,lambda H2D + step + w,rho D2H, copies "
+                               "overlapped across frames) then sf_wait; wall clock",
+                       "synchronous_value": e2e_sync_value,
+                       "synchronous_note": "sf_step_host: the same copies + step + stream sync per frame"},
                "device_flags": flags, "clocks": clocks}
         if world == 1 and not args.no_cpu_baseline:
             out["cpu_baseline"] = cpu_baseline(seqs[0], levels=levels)

@@ -146,6 +146,18 @@ sf_status sf_step(sf_ctx* ctx, const float* Y, const float* depth);
  * ([B][H][W]) (either may be NULL), and synchronises the stream before returning. */
 sf_status sf_step_host(sf_ctx* ctx, const float* Y_host, const float* depth_host, float* w_host, float* rho_host);
 
+/* Pipelined variant of sf_step_host for a stream of frames: enqueues the input copies (own
+ * copy-in stream), the step and the output copies (own copy-out stream) and returns without
+ * synchronising, so frame k's copies overlap frame k-1's output copies and frame k+1's input
+ * copies (two device staging slots, ordered by events).  Host buffers must be pinned
+ * (cudaHostAlloc / torch pin_memory) and stay untouched until sf_wait; w_host / rho_host
+ * receive frame k's new state.  Errors: as sf_step. */
+sf_status sf_step_host_async(sf_ctx* ctx, const float* Y_host, const float* depth_host, float* w_host,
+                             float* rho_host);
+
+/* Wait for every frame enqueued by sf_step_host_async (and all context work). */
+sf_status sf_wait(sf_ctx* ctx);
+
 /* Copy fields out (asynchronously, canonical layout): which = SF_FIELDS_STATE (w^k, rho^k,
  * Yhat^k) or SF_FIELDS_PREDICTED (w^{k+}, rho^{k+}; needs a pending prediction).  Any
  * output pointer may be NULL.  Errors: SF_E_STATE (fresh, or no prediction). */

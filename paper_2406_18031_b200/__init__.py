@@ -25,7 +25,7 @@ SF_ABI_VERSION = 1
 EXPORTS = ("sf_config_default", "sf_create", "sf_destroy", "sf_predict", "sf_update", "sf_step", "sf_step_host",
            "sf_get_fields", "sf_set_fields", "sf_status_flags", "sf_kernel_in_use", "sf_launches_per_step",
            "sf_error_string", "sf_band_halo", "sf_band_partition", "sf_halo_exchange_peer", "sf_halo_exchange_nccl",
-           "sf_nccl_unique_id", "sf_nccl_comm_init", "sf_nccl_comm_destroy", "sf_flow_px", "sf_eval", "sf_map_inputs", "sf_set_motion")
+           "sf_nccl_unique_id", "sf_nccl_comm_init", "sf_nccl_comm_destroy", "sf_flow_px", "sf_eval", "sf_map_inputs", "sf_set_motion", "sf_step_host_async", "sf_wait")
 
 
 class sf_config(C.Structure):
@@ -79,10 +79,12 @@ def _load():
     lib.sf_eval.argtypes = [P, P, P, P, P, P]
     lib.sf_map_inputs.argtypes = [P, P, P, C.c_int32, C.c_int32, P, P, P, P]
     lib.sf_set_motion.argtypes = [P, P, P]
+    lib.sf_step_host_async.argtypes = [P, P, P, P, P]
+    lib.sf_wait.argtypes = [P]
     for name in ("sf_create", "sf_predict", "sf_update", "sf_step", "sf_step_host", "sf_get_fields",
                  "sf_set_fields", "sf_status_flags", "sf_kernel_in_use", "sf_launches_per_step", "sf_band_halo",
                  "sf_band_partition", "sf_halo_exchange_peer", "sf_halo_exchange_nccl", "sf_nccl_unique_id",
-                 "sf_nccl_comm_init", "sf_flow_px", "sf_eval", "sf_map_inputs", "sf_set_motion"):
+                 "sf_nccl_comm_init", "sf_flow_px", "sf_eval", "sf_map_inputs", "sf_set_motion", "sf_step_host_async", "sf_wait"):
         getattr(lib, name).restype = C.c_int
     return lib
 
@@ -131,6 +133,15 @@ def sf_step(ctx: int, Y_ptr: int, depth_ptr: int) -> None:
 def sf_step_host(ctx: int, Y_ptr: int, depth_ptr: int, w_ptr: int | None, rho_ptr: int | None) -> None:
     _check(_lib.sf_step_host(C.c_void_p(ctx), C.c_void_p(Y_ptr), C.c_void_p(depth_ptr), C.c_void_p(w_ptr),
                              C.c_void_p(rho_ptr)), "sf_step_host")
+
+
+def sf_step_host_async(ctx: int, Y_ptr: int, depth_ptr: int, w_ptr: int | None, rho_ptr: int | None) -> None:
+    _check(_lib.sf_step_host_async(C.c_void_p(ctx), C.c_void_p(Y_ptr), C.c_void_p(depth_ptr), C.c_void_p(w_ptr),
+                                   C.c_void_p(rho_ptr)), "sf_step_host_async")
+
+
+def sf_wait(ctx: int) -> None:
+    _check(_lib.sf_wait(C.c_void_p(ctx)), "sf_wait")
 
 
 def sf_get_fields(ctx: int, which: int, w_ptr: int | None, rho_ptr: int | None, yhat_ptr: int | None) -> None:

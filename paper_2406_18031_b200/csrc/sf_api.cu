@@ -65,6 +65,21 @@ static void free_ctx(sf_ctx* c) {
     }
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);
     if (c->ev_join) cudaEventDestroy(c->ev_join);
+    if (c->async_ready) {
+        cudaStreamSynchronize(c->s_in);
+        cudaStreamSynchronize(c->s_out);
+        for (int i = 0; i < 2; ++i) {
+            cudaFree(c->aY[i]);
+            cudaFree(c->aD[i]);
+            cudaFree(c->aw[i]);
+            cudaFree(c->ar[i]);
+            cudaEventDestroy(c->ev_in[i]);
+            cudaEventDestroy(c->ev_done[i]);
+            cudaEventDestroy(c->ev_out[i]);
+        }
+        cudaStreamDestroy(c->s_in);
+        cudaStreamDestroy(c->s_out);
+    }
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
     free(c);
 }
@@ -320,6 +335,77 @@ extern "C" sf_status sf_step_host(sf_ctx* c, const float* Yh, const float* Dh, f
             SF_TRY(sf_launch_unpack(c, c->state[c->cur], wh ? c->hw : nullptr, rh ? c->hr : nullptr));
         if (wh) SF_TRY(cudaMemcpyAsync(wh, c->hw, 3 * n * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
         if (rh) SF_TRY(cudaMemcpyAsync(rh, c->hr, n * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
+    }
+    SF_TRY(cudaStreamSynchronize(c->stream));
+    return SF_OK;
+}
+
+// Pipelined host-buffer frames: frame k's input copies (stream s_in), step + unpack (the
+// context stream) and output copies (stream s_out) overlap frame k-1's output copies and
+// frame k+1's input copies; slot k % 2 holds the device staging of frame k.
+static sf_status async_setup(sf_ctx* c) {
+    const size_t n = (size_t)c->fp.B * c->fp.H * c->fp.W;
+    for (int i = 0; i < 2; ++i) {
+        if (cudaMalloc(&c->aY[i], n * sizeof(float)) != cudaSuccess || cudaMalloc(&c->aD[i], n * sizeof(float)) != cudaSuccess ||
+            cudaMalloc(&c->aw[i], 3 * n * sizeof(float)) != cudaSuccess ||
+            cudaMalloc(&c->ar[i], n * sizeof(float)) != cudaSuccess ||
+            cudaEventCreateWithFlags(&c->ev_in[i], cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&c->ev_done[i], cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&c->ev_out[i], cudaEventDisableTiming) != cudaSuccess)
+            return SF_E_CUDA;
+        // "previous use finished" is true initially
+        if (cudaEventRecord(c->ev_done[i], c->stream) != cudaSuccess || cudaEventRecord(c->ev_out[i], c->stream) != cudaSuccess)
+            return SF_E_CUDA;
+    }
+    if (cudaStreamCreateWithFlags(&c->s_in, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&c->s_out, cudaStreamNonBlocking) != cudaSuccess)
+        return SF_E_CUDA;
+    c->async_ready = true;
+    c->slot = 0;
+    return SF_OK;
+}
+
+extern "C" sf_status sf_step_host_async(sf_ctx* c, const float* Yh, const float* Dh, float* wh, float* rh) {
+    if (!c || !Yh || !Dh) return SF_E_DATA;
+    if (!c->async_ready) {
+        sf_status st = async_setup(c);
+        if (st != SF_OK) return st;
+    }
+    const size_t n = (size_t)c->fp.B * c->fp.H * c->fp.W;
+    const int i = c->slot;
+    c->slot ^= 1;
+    // inputs: wait until the step that last read slot i is done, then copy in
+    SF_TRY(cudaStreamWaitEvent(c->s_in, c->ev_done[i], 0));
+    SF_TRY(cudaMemcpyAsync(c->aY[i], Yh, n * sizeof(float), cudaMemcpyHostToDevice, c->s_in));
+    SF_TRY(cudaMemcpyAsync(c->aD[i], Dh, n * sizeof(float), cudaMemcpyHostToDevice, c->s_in));
+    SF_TRY(cudaEventRecord(c->ev_in[i], c->s_in));
+    // step on the context stream
+    SF_TRY(cudaStreamWaitEvent(c->stream, c->ev_in[i], 0));
+    sf_status st = sf_step(c, c->aY[i], c->aD[i]);
+    if (st != SF_OK) return st;
+    if (wh || rh) {
+        SF_TRY(cudaStreamWaitEvent(c->stream, c->ev_out[i], 0));  // slot i's outputs drained
+        if (c->levels == 2) {
+            SF_TRY(sf_launch_unpack_pyr(c, wh ? c->aw[i] : nullptr, rh ? c->ar[i] : nullptr, nullptr));
+        } else {
+            SF_TRY(sf_launch_unpack(c, c->state[c->cur], wh ? c->aw[i] : nullptr, rh ? c->ar[i] : nullptr));
+        }
+    }
+    SF_TRY(cudaEventRecord(c->ev_done[i], c->stream));
+    if (wh || rh) {
+        SF_TRY(cudaStreamWaitEvent(c->s_out, c->ev_done[i], 0));
+        if (wh) SF_TRY(cudaMemcpyAsync(wh, c->aw[i], 3 * n * sizeof(float), cudaMemcpyDeviceToHost, c->s_out));
+        if (rh) SF_TRY(cudaMemcpyAsync(rh, c->ar[i], n * sizeof(float), cudaMemcpyDeviceToHost, c->s_out));
+        SF_TRY(cudaEventRecord(c->ev_out[i], c->s_out));
+    }
+    return SF_OK;
+}
+
+extern "C" sf_status sf_wait(sf_ctx* c) {
+    if (!c) return SF_E_DATA;
+    if (c->async_ready) {
+        SF_TRY(cudaStreamSynchronize(c->s_in));
+        SF_TRY(cudaStreamSynchronize(c->s_out));
     }
     SF_TRY(cudaStreamSynchronize(c->stream));
     return SF_OK;
