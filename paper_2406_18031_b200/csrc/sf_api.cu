@@ -223,7 +223,9 @@ extern "C" sf_status sf_create(const sf_config* cfg, const float* geometry, sf_c
             free_ctx(c);
             return st;
         }
-        c->kernel = SF_KERNEL_PASSES;  // the bottom level runs the pass kernels
+        // bottom level: fused prediction unless the pass kernels are requested; update on passes
+        c->low_fused = cfg->kernel != SF_KERNEL_PASSES && sf_low_fused_supported(c);
+        c->kernel = c->low_fused ? SF_KERNEL_FUSED : SF_KERNEL_PASSES;
         *out = c;
         return SF_OK;
     }
@@ -289,7 +291,7 @@ static sf_status pyr_step(sf_ctx* c, const float* Y, const float* D) {
     if (init) {
         SF_TRY(sf_launch_update_low(c, Y, D, true));
     } else {
-        SF_TRY(sf_launch_predict_low(c));
+        SF_TRY(c->low_fused ? sf_launch_predict_low_fused(c) : sf_launch_predict_low(c));
         SF_TRY(sf_launch_update_low(c, Y, D, false));
     }
     SF_TRY(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
@@ -484,8 +486,9 @@ extern "C" int32_t sf_kernel_in_use(const sf_ctx* c) { return c ? c->kernel : 0;
 
 extern "C" int32_t sf_launches_per_step(const sf_ctx* c) {
     if (!c) return 0;
-    if (c->levels == 2)  // down2 + top + 2N bottom passes + hconv + solve + 2S box + up2
-        return 1 + sf_launches_per_step(c->top) + 2 * c->fp.N + 2 + 2 * c->fp.S + 1;
+    if (c->levels == 2)  // down2 + top + bottom prediction + hconv + solve + 2S box + up2
+        return 1 + sf_launches_per_step(c->top) + (c->low_fused ? sf_low_fused_launches(c) : 2 * c->fp.N) + 2 +
+               2 * c->fp.S + 1;
     if (c->kernel == SF_KERNEL_FUSED) return sf_fused_launches(c);
     return 2 * c->fp.N + 2 + 2 * c->fp.S;
 }

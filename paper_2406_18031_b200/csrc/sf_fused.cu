@@ -255,15 +255,32 @@ __device__ __forceinline__ void ls_solve3x2(const float2 g[3], const float2 m[3]
 // returns its own value and the pass bodies carry no boundary logic.  A grid edge on the
 // region border itself needs no replica: it lies R cells from the tile, outside the tile's
 // dependency cone, like any cut edge.
-template <int K, int NWY, int RULE, bool CLAMP>
-__device__ __forceinline__ void transport_passes(const FrameParams& f, int M, float2 (&W)[4][K], const float2 (&SX)[K],
+template <int K, int NWY, int RULE, bool CLAMP, int NF = 4>
+__device__ __forceinline__ void transport_passes(const FrameParams& f, int M, float2 (&W)[NF][K], const float2 (&SX)[K],
                                                  const float2 (&SY)[K], const float2 (&SZ)[K], float (&mx)[K],
                                                  const float* Es, float2* XB0, int lane, int wy, int cmin, int cmax,
-                                                 int rmin, int rmax, int dbg) {
+                                                 int rmin, int rmax, int dbg, const float* Ss = nullptr) {
     using C = Cfg<K, NWY>;
     constexpr int RW = C::RW, P = C::P, RH = C::RH;
+    // NF = 4: (w, rho), all dilated.  NF = 8 (pyramid bottom level): (w, dw, rho, Yhat), the last
+    // one without dilation (eq:img_propagation_low)
+    constexpr int ND = NF == 8 ? 7 : NF;
+    constexpr int XBS = NF * NWY * 2 * 32;  // float2 slots of one row-exchange buffer
+    // NF = 4: two buffers (substep parity); NF = 8: one buffer (shared memory is short) and a
+    // second barrier per substep after the neighbour rows are read
+    constexpr int NXB = NF == 8 ? 1 : 2;
     const int c0 = 2 * lane, r0 = K * wy;
     const float U = f.U;
+    // s of the lane's cells: registers (NF = 4), or shared planes Ss[3][P] (NF = 8: registers
+    // are taken by the 8 fields)
+    auto sdot = [&](int k) -> float2 {
+        if (NF == 8) {
+            const int ib = (r0 + k) * RW + c0;
+            return dot2(*reinterpret_cast<const float2*>(Ss + ib), *reinterpret_cast<const float2*>(Ss + P + ib),
+                        *reinterpret_cast<const float2*>(Ss + 2 * P + ib), W[0][k], W[1][k], W[2][k]);
+        }
+        return dot2(SX[k], SY[k], SZ[k], W[0][k], W[1][k], W[2][k]);
+    };
     const float2 T2 = make_float2(-f.dt, -f.dt), SG = make_float2(f.sigma, f.sigma);
     const int srcL = lane - 1, srcR = lane + 1;
     // replica bookkeeping (block-uniform except for the lane / k tests)
@@ -303,11 +320,11 @@ __device__ __forceinline__ void transport_passes(const FrameParams& f, int M, fl
             // upwind value by per-lane source: cell 0 takes lane-1's cell 1 (u_hat > 0) or its own
             // cell 1; cell 1 takes its own cell 0 (u_hat > 0) or lane+1's cell 0
             const int s0 = p0 ? srcL : lane, s1 = p1 ? lane : srcR;
-            const float2 q = mul2(SG, dot2(SX[k], SY[k], SZ[k], W[0][k], W[1][k], W[2][k]));
+            const float2 q = mul2(SG, sdot(k));
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
+            for (int c = 0; c < NF; ++c) {
                 const float2 fu = make_float2(__shfl_sync(FULL, W[c][k].y, s0), __shfl_sync(FULL, W[c][k].x, s1));
-                W[c][k] = tr2(W[c][k], fu, A, q, T2);
+                W[c][k] = c < ND ? tr2(W[c][k], fu, A, q, T2) : fma2(T2, mul2(A, sub2(W[c][k], fu)), W[c][k]);
             }
         }
         // column replicas <- their edge cells
@@ -316,7 +333,7 @@ __device__ __forceinline__ void transport_passes(const FrameParams& f, int M, fl
 #pragma unroll
             for (int k = 0; k < K; ++k)
 #pragma unroll
-                for (int c = 0; c < 4; ++c) {
+                for (int c = 0; c < NF; ++c) {
                     const float e = __shfl_down_sync(FULL, W[c][k].x, 1);
                     W[c][k].y = me ? e : W[c][k].y;
                 }
@@ -327,7 +344,7 @@ __device__ __forceinline__ void transport_passes(const FrameParams& f, int M, fl
 #pragma unroll
                 for (int k = 0; k < K; ++k)
 #pragma unroll
-                    for (int c = 0; c < 4; ++c) {
+                    for (int c = 0; c < NF; ++c) {
                         const float e = __shfl_up_sync(FULL, W[c][k].y, 1);
                         W[c][k].x = me ? e : W[c][k].x;
                     }
@@ -335,7 +352,7 @@ __device__ __forceinline__ void transport_passes(const FrameParams& f, int M, fl
 #pragma unroll
                 for (int k = 0; k < K; ++k)
 #pragma unroll
-                    for (int c = 0; c < 4; ++c) W[c][k].y = me ? W[c][k].x : W[c][k].y;
+                    for (int c = 0; c < NF; ++c) W[c][k].y = me ? W[c][k].x : W[c][k].y;
             }
         }
         // row replicas inside this thread's run <- their edge rows (before the row pass reads)
@@ -344,7 +361,7 @@ __device__ __forceinline__ void transport_passes(const FrameParams& f, int M, fl
             for (int k = 0; k < K - 1; ++k) {
                 const bool p = (keT - 1 - k) == 0;
 #pragma unroll
-                for (int c = 0; c < 4; ++c) W[c][k] = sel2(p, p, W[c][k + 1], W[c][k]);
+                for (int c = 0; c < NF; ++c) W[c][k] = sel2(p, p, W[c][k + 1], W[c][k]);
             }
         }
         if (repB && keB >= 0 && keB <= K - 2) {
@@ -352,15 +369,15 @@ __device__ __forceinline__ void transport_passes(const FrameParams& f, int M, fl
             for (int k = K - 1; k >= 1; --k) {
                 const bool p = (keB + 1 - k) == 0;
 #pragma unroll
-                for (int c = 0; c < 4; ++c) W[c][k] = sel2(p, p, W[c][k - 1], W[c][k]);
+                for (int c = 0; c < NF; ++c) W[c][k] = sel2(p, p, W[c][k - 1], W[c][k]);
             }
         }
         // ================= row pass (beta_2, reading 3)
         if (!(dbg & 128)) {
             // run-end rows to the exchange buffer: [comp][warp][end][lane] float2
-            float2* const XB = XB0 + (n & 1) * C::XR;
+            float2* const XB = XB0 + (NXB == 2 ? (n & 1) * XBS : 0);
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
+            for (int c = 0; c < NF; ++c) {
                 XB[((c * NWY + wy) * 2 + 0) * 32 + lane] = W[c][0];
                 XB[((c * NWY + wy) * 2 + 1) * 32 + lane] = W[c][K - 1];
             }
@@ -373,47 +390,50 @@ __device__ __forceinline__ void transport_passes(const FrameParams& f, int M, fl
                             *reinterpret_cast<const float2*>(Es + 5 * P + ib), W[0][k], W[1][k], W[2][k]);
             }
             // row k in place from its upwind values fu (selected from the pre-pass rows k-1 / k+1)
-            auto row_update = [&](int k, float2 vm, float2 vp, const float2 (&fm)[4], const float2 (&fp)[4]) {
+            auto row_update = [&](int k, float2 vm, float2 vp, const float2 (&fm)[NF], const float2 (&fp)[NF]) {
                 bool p0, p1;
                 const float2 A = flow(k, dominant(vm.x, vp.x, RULE), dominant(vm.y, vp.y, RULE), p0, p1);
-                const float2 q = mul2(SG, dot2(SX[k], SY[k], SZ[k], W[0][k], W[1][k], W[2][k]));
+                const float2 q = mul2(SG, sdot(k));
 #pragma unroll
-                for (int c = 0; c < 4; ++c) W[c][k] = tr2(W[c][k], sel2(p0, p1, fm[c], fp[c]), A, q, T2);
+                for (int c = 0; c < NF; ++c) {
+                    const float2 fu = sel2(p0, p1, fm[c], fp[c]);
+                    W[c][k] = c < ND ? tr2(W[c][k], fu, A, q, T2) : fma2(T2, mul2(A, sub2(W[c][k], fu)), W[c][k]);
+                }
             };
             // pre-pass rows 1 and K-2 are kept for the run ends; the interior rows 1..K-2 need no
             // exchanged value and are updated before the barrier, in place, in increasing k: row
             // k's neighbours are the pre-pass row k-1 (kept one step) and row k+1 (not yet updated)
-            float2 o1[4], oK[4], prev[4];
+            float2 o1[NF], oK[NF], prev[NF];
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
+            for (int c = 0; c < NF; ++c) {
                 o1[c] = W[c][1];
                 oK[c] = W[c][K - 2];
                 prev[c] = W[c][0];
             }
 #pragma unroll
             for (int k = 1; k <= K - 2; ++k) {
-                float2 cur[4], nxt[4];
+                float2 cur[NF], nxt[NF];
 #pragma unroll
-                for (int c = 0; c < 4; ++c) {
+                for (int c = 0; c < NF; ++c) {
                     cur[c] = W[c][k];
                     nxt[c] = W[c][k + 1];
                 }
                 row_update(k, v[k - 1], v[k + 1], prev, nxt);
 #pragma unroll
-                for (int c = 0; c < 4; ++c) prev[c] = cur[c];
+                for (int c = 0; c < NF; ++c) prev[c] = cur[c];
             }
             __syncthreads();
-            float2 t[4], bb[4];
+            float2 t[NF], bb[NF];
             float2 vt = v[0], vb = v[K - 1];
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
+            for (int c = 0; c < NF; ++c) {
                 t[c] = W[c][0];
                 bb[c] = W[c][K - 1];
             }
             // neighbour run ends; at an edge row on a run boundary the replica is the row itself
             if (wy > 0 && !(repT && keT == 0)) {
 #pragma unroll
-                for (int c = 0; c < 4; ++c) t[c] = XB[((c * NWY + wy - 1) * 2 + 1) * 32 + lane];
+                for (int c = 0; c < NF; ++c) t[c] = XB[((c * NWY + wy - 1) * 2 + 1) * 32 + lane];
                 const int ib = (r0 - 1) * RW + c0;
                 vt = dot2(*reinterpret_cast<const float2*>(Es + 3 * P + ib),
                           *reinterpret_cast<const float2*>(Es + 4 * P + ib),
@@ -421,7 +441,7 @@ __device__ __forceinline__ void transport_passes(const FrameParams& f, int M, fl
             }
             if (wy < NWY - 1 && !(repB && keB == K - 1)) {
 #pragma unroll
-                for (int c = 0; c < 4; ++c) bb[c] = XB[((c * NWY + wy + 1) * 2 + 0) * 32 + lane];
+                for (int c = 0; c < NF; ++c) bb[c] = XB[((c * NWY + wy + 1) * 2 + 0) * 32 + lane];
                 const int ib = (r0 + K) * RW + c0;
                 vb = dot2(*reinterpret_cast<const float2*>(Es + 3 * P + ib),
                           *reinterpret_cast<const float2*>(Es + 4 * P + ib),
@@ -429,8 +449,9 @@ __device__ __forceinline__ void transport_passes(const FrameParams& f, int M, fl
             }
             row_update(0, vt, v[1], t, o1);
             row_update(K - 1, v[K - 2], vb, oK, bb);
+            if (NXB == 1) __syncthreads();  // the single exchange buffer is rewritten next substep
         }
-        if (f.imu) {  // inertial stage after the row pass (reading 32), per cell
+        if (NF == 4 && f.imu) {  // inertial stage after the row pass (reading 32), per cell
 #pragma unroll
             for (int k = 0; k < K; ++k) {
                 imu_stage(f, SX[k].x, SY[k].x, SZ[k].x, W[0][k].x, W[1][k].x, W[2][k].x, W[3][k].x);
@@ -888,6 +909,162 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
     if (lane == 0 && any) atomicOr(a.flags, any);
 }
 
+// ================================================================== pyramid bottom level (NEXT #1)
+// Fused prediction [P_[]] of the bottom level: M substeps of the 8-field transport (w, dw, rho,
+// Yhat advected by the reconstructed w; readings 26-27) for one tile, fields in registers
+// (cell-paired), e planes staged by TMA, deep halo R = M (rounded up to 4).  The update runs on
+// the per-pass kernels (sf_passes.cu).
+struct LowArgs {
+    CUtensorMap tmE;   // [6][H][W] e planes, box RW x RH x 3 (valid when tma)
+    int tma;
+    const float4* finA;  // (dw, rho)
+    const float4* finW;  // (w, Yhat)
+    float4* foutA;
+    float4* foutW;
+    const float4* G0;
+    const float* E;
+    unsigned* flags;
+    FrameParams f;
+    int M, R, TH, TW;
+};
+
+template <int K, int NWY>
+struct LowCfg {
+    static constexpr int RW = 64, RH = K * NWY, P = RW * RH, NT = 32 * NWY;
+    static constexpr int XBF = 8 * NWY * 2 * 32 * 2;  // floats of the (single) row-exchange buffer
+    static constexpr size_t SMEM = sizeof(float) * (9 * (size_t)P + XBF) + 64;  // e | s | XB | bars
+};
+
+template <int K, int NWY, int RULE, bool CLAMP>
+__global__ void __launch_bounds__(32 * NWY, 1) k_low(const __grid_constant__ LowArgs a) {
+    using C = LowCfg<K, NWY>;
+    constexpr int RW = C::RW, RH = C::RH, P = C::P;
+    extern __shared__ __align__(1024) float4 smem4[];
+    float* const sm = reinterpret_cast<float*>(smem4);
+    float* const Es = sm;
+    float* const Ss = sm + 6 * P;  // s.x, s.y, s.z planes
+    float2* const XB0 = reinterpret_cast<float2*>(sm + 9 * P);
+    uint64_t* const bars = reinterpret_cast<uint64_t*>(sm + 9 * P + C::XBF);
+    const FrameParams& f = a.f;
+    const int tid = threadIdx.x, lane = tid & 31, wy = tid >> 5;
+    const int c0 = 2 * lane, r0 = K * wy;
+    const int b = blockIdx.z, R = a.R, TH = a.TH, TW = a.TW;
+    const int gi0 = blockIdx.y * TH - R, gj0 = blockIdx.x * TW - R;
+    const int cmin = max(0, -gj0), cmax = min(RW - 1, f.W - 1 - gj0);
+    const int rmin = max(0, -gi0), rmax = min(RH - 1, f.H - 1 - gi0);
+    const size_t HW = (size_t)f.H * f.W, plane = (size_t)b * HW;
+    if (a.tma) {
+        if (tid == 0) {
+            mbar_init(&bars[0], 1);
+            mbar_init(&bars[1], 1);
+            asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        }
+        __syncthreads();
+        if (tid == 0) {
+            mbar_expect_tx(&bars[0], 3u * P * 4u);
+            tma_load_3d(Es, &a.tmE, gj0, gi0, 0, &bars[0]);
+            mbar_expect_tx(&bars[1], 3u * P * 4u);
+            tma_load_3d(Es + 3 * P, &a.tmE, gj0, gi0, 3, &bars[1]);
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const int r = r0 + k;
+            const size_t gr = (size_t)iclamp(gi0 + r, 0, f.H - 1) * f.W;
+            const size_t ga = gr + iclamp(gj0 + c0, 0, f.W - 1), gb = gr + iclamp(gj0 + c0 + 1, 0, f.W - 1);
+#pragma unroll
+            for (int p = 0; p < 6; ++p) {
+                float* dst = Es + p * P + r * RW + c0;
+                cp_async4(dst, a.E + p * HW + ga);
+                cp_async4(dst + 1, a.E + p * HW + gb);
+            }
+        }
+        cp_async_commit();
+    }
+    float2 W[8][K];
+    float2 SX[K], SY[K], SZ[K];
+    float mx[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        const size_t gr = (size_t)iclamp(gi0 + r0 + k, 0, f.H - 1) * f.W;
+        const size_t ga = gr + iclamp(gj0 + c0, 0, f.W - 1), gb = gr + iclamp(gj0 + c0 + 1, 0, f.W - 1);
+        const float4 sa = __ldg(a.G0 + ga), sb = __ldg(a.G0 + gb);
+        const int ib = (r0 + k) * RW + c0;  // own cells only: no barrier needed before the reads
+        *reinterpret_cast<float2*>(Ss + ib) = make_float2(sa.x, sb.x);
+        *reinterpret_cast<float2*>(Ss + P + ib) = make_float2(sa.y, sb.y);
+        *reinterpret_cast<float2*>(Ss + 2 * P + ib) = make_float2(sa.z, sb.z);
+        SX[k] = SY[k] = SZ[k] = make_float2(0.0f, 0.0f);  // unused (s lives in Ss)
+        mx[k] = 0.0f;
+    }
+    griddep_wait();
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        const size_t gr = (size_t)iclamp(gi0 + r0 + k, 0, f.H - 1) * f.W;
+        const size_t ga = plane + gr + iclamp(gj0 + c0, 0, f.W - 1), gb = plane + gr + iclamp(gj0 + c0 + 1, 0, f.W - 1);
+        const float4 wa = a.finW[ga], wb = a.finW[gb], da = a.finA[ga], db = a.finA[gb];
+        W[0][k] = make_float2(wa.x, wb.x);
+        W[1][k] = make_float2(wa.y, wb.y);
+        W[2][k] = make_float2(wa.z, wb.z);
+        W[3][k] = make_float2(da.x, db.x);
+        W[4][k] = make_float2(da.y, db.y);
+        W[5][k] = make_float2(da.z, db.z);
+        W[6][k] = make_float2(da.w, db.w);
+        W[7][k] = make_float2(wa.w, wb.w);
+    }
+    griddep_launch_dependents();
+    if (a.tma) {
+        mbar_wait(&bars[0], 0);
+        mbar_wait(&bars[1], 0);
+    } else {
+        cp_async_wait<0>();
+    }
+    if (cmin > 0 || cmax < RW - 1 || rmin > 0 || rmax < RH - 1) {  // replica e cells (reading 10)
+        __syncthreads();
+        if (cmin > 0 || cmax < RW - 1)
+            for (int t = tid; t < 6 * RH; t += C::NT) {
+                float* row = Es + (t / RH) * P + (t % RH) * RW;
+                if (cmin > 0) row[cmin - 1] = row[cmin];
+                if (cmax < RW - 1) row[cmax + 1] = row[cmax];
+            }
+        __syncthreads();
+        if (rmin > 0 || rmax < RH - 1)
+            for (int t = tid; t < 6 * RW; t += C::NT) {
+                float* col = Es + (t / RW) * P + (t % RW);
+                if (rmin > 0) col[(rmin - 1) * RW] = col[rmin * RW];
+                if (rmax < RH - 1) col[(rmax + 1) * RW] = col[rmax * RW];
+            }
+    }
+    __syncthreads();
+    transport_passes<K, NWY, RULE, CLAMP, 8>(f, a.M, W, SX, SY, SZ, mx, Es, XB0, lane, wy, cmin, cmax, rmin, rmax, 0,
+                                             Ss);
+    unsigned fl = 0;
+    const bool tcol = c0 >= R && c0 < R + TW && c0 >= cmin && c0 <= cmax;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        const int r = r0 + k;
+        if (r >= R && r < R + TH && r >= rmin && r <= rmax) {
+            if (tcol) {
+                if (CLAMP) {
+                    if (mx[k] > f.U) fl |= SF_FLAG_CLAMPED;
+                } else if (xmul(f.dt, mx[k]) > 1.0f) {
+                    fl |= SF_FLAG_CFL;
+                }
+            }
+            const size_t g = plane + (size_t)(gi0 + r) * f.W + (gj0 + c0);
+            if (c0 >= R && c0 < R + TW && c0 >= cmin && c0 <= cmax) {
+                a.foutW[g] = make_float4(W[0][k].x, W[1][k].x, W[2][k].x, W[7][k].x);
+                a.foutA[g] = make_float4(W[3][k].x, W[4][k].x, W[5][k].x, W[6][k].x);
+            }
+            if (c0 + 1 >= R && c0 + 1 < R + TW && c0 + 1 >= cmin && c0 + 1 <= cmax) {
+                a.foutW[g + 1] = make_float4(W[0][k].y, W[1][k].y, W[2][k].y, W[7][k].y);
+                a.foutA[g + 1] = make_float4(W[3][k].y, W[4][k].y, W[5][k].y, W[6][k].y);
+            }
+        }
+    }
+    const unsigned any = __reduce_or_sync(FULL, fl);
+    if (lane == 0 && any) atomicOr(a.flags, any);
+}
+
 // The configuration used today: RW = 64, RH = 72 (K = 6 rows x 12 warps), 384 threads, 1 CTA / SM.
 constexpr int MMAX = 8;  // substeps per launch
 
@@ -1024,6 +1201,67 @@ cudaError_t launch_cfg(sf_ctx* c, const float* Y, const float* D) {
     return cudaSuccess;
 }
 
+// Bottom-level fused prediction: ceil(N / MMAX) launches of M <= MMAX substeps; the last one
+// writes (pred, Wpred), earlier ones ping-pong through (tmp, Wtmp).
+constexpr int LOW_K = 5, LOW_NWY = 12;
+
+template <int K, int NWY>
+bool prepare_low() {
+    using LC = LowCfg<K, NWY>;
+    const void* fns[] = {(const void*)k_low<K, NWY, SF_DOM_LARGEST, true>, (const void*)k_low<K, NWY, SF_DOM_LARGEST, false>,
+                         (const void*)k_low<K, NWY, SF_DOM_PRINTED, true>, (const void*)k_low<K, NWY, SF_DOM_PRINTED, false>};
+    for (const void* fn : fns)
+        if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LC::SMEM) != cudaSuccess)
+            return false;
+    return true;
+}
+
+template <int K, int NWY>
+cudaError_t launch_low(sf_ctx* c) {
+    using LC = LowCfg<K, NWY>;
+    const FrameParams& f = c->fp;
+    const int L = (f.N + MMAX - 1) / MMAX;
+    const float4* srcA = c->state[c->cur];
+    const float4* srcW = c->Wf[c->cur];
+    for (int l = 0; l < L; ++l) {
+        LowArgs a;
+        a.M = (l < L - 1) ? MMAX : f.N - MMAX * (L - 1);
+        a.R = (a.M + 3) & ~3;
+        a.TW = LC::RW - 2 * a.R;
+        a.TH = LC::RH - 2 * a.R;
+        a.tma = getenv("SF_NO_TMA") == nullptr && encode3d(&a.tmE, c->E, f.W, f.H, 6, LC::RW, LC::RH, 3);
+        a.finA = srcA;
+        a.finW = srcW;
+        const bool last = ((L - 1 - l) & 1) == 0;
+        a.foutA = last ? c->pred : c->tmp;
+        a.foutW = last ? c->Wpred : c->Wtmp;
+        a.G0 = c->G0;
+        a.E = c->E;
+        a.flags = c->flags;
+        a.f = f;
+        const dim3 grid((f.W + a.TW - 1) / a.TW, (f.H + a.TH - 1) / a.TH, f.B);
+        void (*kern)(LowArgs) = f.rule == SF_DOM_PRINTED
+                                    ? (f.clamp ? k_low<K, NWY, SF_DOM_PRINTED, true> : k_low<K, NWY, SF_DOM_PRINTED, false>)
+                                    : (f.clamp ? k_low<K, NWY, SF_DOM_LARGEST, true> : k_low<K, NWY, SF_DOM_LARGEST, false>);
+        cudaLaunchConfig_t lc = {};
+        lc.gridDim = grid;
+        lc.blockDim = dim3(LC::NT);
+        lc.dynamicSmemBytes = LC::SMEM;
+        lc.stream = c->stream;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = getenv("SF_NO_PDL") ? 0 : 1;
+        lc.attrs = at;
+        lc.numAttrs = 1;
+        cudaError_t e = cudaLaunchKernelEx(&lc, kern, a);
+        if (e == cudaSuccess) e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+        srcA = a.foutA;
+        srcW = a.foutW;
+    }
+    return cudaSuccess;
+}
+
 }  // namespace
 
 bool sf_fused_supported(const sf_ctx* c) {
@@ -1040,3 +1278,12 @@ int sf_fused_launches(const sf_ctx* c) { return make_plan(c->fp).launches; }
 cudaError_t sf_launch_fused_step(sf_ctx* c, const float* Y, const float* D) {
     return fused_cfg() == 1 ? launch_cfg<4, 18>(c, Y, D) : launch_cfg<6, 12>(c, Y, D);
 }
+
+bool sf_low_fused_supported(const sf_ctx* c) {
+    if ((c->fp.N + MMAX - 1) / MMAX > 8) return false;
+    return prepare_low<LOW_K, LOW_NWY>();
+}
+
+int sf_low_fused_launches(const sf_ctx* c) { return (c->fp.N + MMAX - 1) / MMAX; }
+
+cudaError_t sf_launch_predict_low_fused(sf_ctx* c) { return launch_low<LOW_K, LOW_NWY>(c); }
