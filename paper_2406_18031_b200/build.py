@@ -30,10 +30,18 @@ def _deps():
     return files
 
 
+STAMP = os.path.join(HERE, "build_flags.txt")
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= max(os.path.getmtime(f) for f in _deps()):
+    """SF_BUILD_DEBUG=1 compiles the timing / phase-skip knobs of the fused kernel (SF_DEBUG_SKIP);
+    the default build folds them away."""
+    extra = ["-DSF_DEBUG_KNOBS"] if os.environ.get("SF_BUILD_DEBUG") == "1" else []
+    cmd = [NVCC, *FLAGS, *extra, *[os.path.join(CSRC, s) for s in SOURCES], "-o", LIB]
+    same = os.path.exists(STAMP) and open(STAMP).read() == " ".join(cmd)
+    if (not force and same and os.path.exists(LIB) and
+            os.path.getmtime(LIB) >= max(os.path.getmtime(f) for f in _deps())):
         return LIB
-    cmd = [NVCC, *FLAGS, *[os.path.join(CSRC, s) for s in SOURCES], "-o", LIB]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
@@ -42,6 +50,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         sys.stderr.write(r.stderr)
     with open(os.path.join(HERE, "build_ptxas.log"), "w") as fh:
         fh.write(r.stderr)
+    with open(STAMP, "w") as fh:
+        fh.write(" ".join(cmd))
     return LIB
 
 

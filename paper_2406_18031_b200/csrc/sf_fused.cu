@@ -487,10 +487,15 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
     const bool edgeR = rmin > 0 || rmax < RH - 1;
     const size_t HW = (size_t)f.H * f.W, plane = (size_t)b * HW;
 
-    if (a.dbg_skip & 32) return;
+#ifdef SF_DEBUG_KNOBS
+    const int dbg = a.dbg_skip;  // timing experiments (build with SF_BUILD_DEBUG=1)
+#else
+    constexpr int dbg = 0;       // production build: every knob folds away
+#endif
+    if (dbg & 32) return;
     long long T_[16];
     int nT_ = 0;
-    const bool tim = (a.dbg_skip & 256) && blockIdx.z == 0 &&
+    const bool tim = (dbg & 256) && blockIdx.z == 0 &&
                      ((blockIdx.x == 6 && blockIdx.y == 5) || (blockIdx.x == 0 && blockIdx.y == 0) ||
                       (blockIdx.x == 0 && blockIdx.y == 5) || (blockIdx.x == gridDim.x - 1 && blockIdx.y == gridDim.y - 1));
 #define SF_TICK() do { if (tim) { __syncthreads(); if (tid == 0) T_[nT_] = clock64(); ++nT_; } } while (0)
@@ -507,7 +512,7 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
             asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
         }
         __syncthreads();
-        if (tid == 0 && !(a.dbg_skip & 4)) {  // geometry: independent of the previous frame
+        if (tid == 0 && !(dbg & 4)) {  // geometry: independent of the previous frame
             mbar_expect_tx(&bars[0], 3u * P * 4u);
             tma_load_3d(Es, &a.tmE, gj0, gi0, 0, &bars[0]);
             mbar_expect_tx(&bars[1], 3u * P * 4u);
@@ -561,8 +566,8 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
     for (int k = 0; k < K; ++k) {
         const size_t gr = (size_t)iclamp(gi0 + r0 + k, 0, f.H - 1) * f.W;
         const size_t ga = gr + iclamp(gj0 + c0, 0, f.W - 1), gb = gr + iclamp(gj0 + c0 + 1, 0, f.W - 1);
-        const float4 sa = (a.dbg_skip & 16) ? make_float4(0, 0, 1, 0) : __ldg(a.G0 + ga);
-        const float4 sb = (a.dbg_skip & 16) ? make_float4(0, 0, 1, 0) : __ldg(a.G0 + gb);
+        const float4 sa = (dbg & 16) ? make_float4(0, 0, 1, 0) : __ldg(a.G0 + ga);
+        const float4 sb = (dbg & 16) ? make_float4(0, 0, 1, 0) : __ldg(a.G0 + gb);
         SX[k] = make_float2(sa.x, sb.x);
         SY[k] = make_float2(sa.y, sb.y);
         SZ[k] = make_float2(sa.z, sb.z);
@@ -572,7 +577,7 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
     // and the frame's inputs may be written by the preceding kernel in the stream
     if (a.tma) {
         griddep_wait();
-        if (tid == 0 && a.upd && !(a.dbg_skip & 8)) {
+        if (tid == 0 && a.upd && !(dbg & 8)) {
             mbar_expect_tx(&bars[2], 2u * P * 4u);
             tma_load_3d(Ys, &a.tmY, gj0, gi0, b, &bars[2]);
             tma_load_3d(Ds, &a.tmD, gj0, gi0, b, &bars[2]);
@@ -582,8 +587,8 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
     for (int k = 0; k < K; ++k) {
         const size_t gr = (size_t)iclamp(gi0 + r0 + k, 0, f.H - 1) * f.W;
         const size_t ga = gr + iclamp(gj0 + c0, 0, f.W - 1), gb = gr + iclamp(gj0 + c0 + 1, 0, f.W - 1);
-        const float4 fa = (a.dbg_skip & 16) ? make_float4(0, 0, 0, 0.5f) : a.fin[plane + ga];
-        const float4 fb = (a.dbg_skip & 16) ? make_float4(0, 0, 0, 0.5f) : a.fin[plane + gb];
+        const float4 fa = (dbg & 16) ? make_float4(0, 0, 0, 0.5f) : a.fin[plane + ga];
+        const float4 fb = (dbg & 16) ? make_float4(0, 0, 0, 0.5f) : a.fin[plane + gb];
         W[0][k] = make_float2(fa.x, fb.x);
         W[1][k] = make_float2(fa.y, fb.y);
         W[2][k] = make_float2(fa.z, fb.z);
@@ -591,7 +596,7 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
     }
     griddep_launch_dependents();  // the next frame's CTAs may start their geometry loads
     SF_TICK();
-    if (a.tma && !(a.dbg_skip & 4)) {
+    if (a.tma && !(dbg & 4)) {
         mbar_wait(&bars[0], 0);
         mbar_wait(&bars[1], 0);
         if (edgeC || edgeR) {  // replica cells next to grid edges take the edge cell's e (reading 10)
@@ -615,9 +620,9 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
         cp_async_wait<1>();  // own e cells landed (each thread reads only what it copied until the 1st barrier)
     }
 
-    if (!(a.dbg_skip & 1))
+    if (!(dbg & 1))
     transport_passes<K, NWY, RULE, CLAMP>(f, a.M, W, SX, SY, SZ, mx, Es, XB0, lane, wy, cmin,
-                                          cmax, rmin, rmax, a.dbg_skip);
+                                          cmax, rmin, rmax, dbg);
     const float U = f.U;
 
     // ---------------- flags from tile cells (exact at every pass); |u_hat| before the clamp
@@ -638,7 +643,7 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
     }
 
     SF_TICK();
-    if (!a.upd || (a.dbg_skip & 2)) {  // intermediate launch: store the partial prediction of the tile
+    if (!a.upd || (dbg & 2)) {  // intermediate launch: store the partial prediction of the tile
 #pragma unroll
         for (int k = 0; k < K; ++k) {
             const int r = r0 + k;
@@ -663,7 +668,7 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
         // solve region = tile + 2S (clipped to the grid); models needed on it +-2 rows, +-1 cols
         const int rlo = max(R - 2 * S, rmin), rhi = min(R + TH + 2 * S - 1, rmax);
         const int clo = max(R - 2 * S, cmin), chi = min(R + TW + 2 * S - 1, cmax);
-        if (a.tma && !(a.dbg_skip & 8)) {
+        if (a.tma && !(dbg & 8)) {
             mbar_wait(&bars[2], 0);
             if (edgeC || edgeR) {  // out-of-grid cells of Y / depth read below take their clamped cell's value
                 __syncthreads();
@@ -704,7 +709,7 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
         // arithmetic cell-paired as f32x2; a ragged last pair computes its first cell twice and
         // stores it once).  The pair's global inputs (s, ds^2, Y, rho^k) are fetched one pair ahead.
         {
-            const int ncol = ((a.dbg_skip & 1024) ? clo - 1 : chi) - clo + 1;
+            const int ncol = ((dbg & 1024) ? clo - 1 : chi) - clo + 1;
             const int nc = (ncol + 1) >> 1, dr = nc > 0 ? NT / nc : 0, dc = nc > 0 ? NT % nc : 0;
             int rn = nc > 0 ? rlo + tid / nc : rhi + 1, pn = nc > 0 ? tid % nc : 0;
             auto fetch = [&](int r, int pc, float4& sa, float4& sb, float2& y, float2& sk) {
@@ -791,7 +796,7 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
         const bool edge = edgeC || edgeR;
         float* src[3] = {Fx, Fy, Fz};
         float* dst[3] = {Es, Es + P, Es + 2 * P};
-        for (int it = 0; it < ((a.dbg_skip & 512) ? 0 : S); ++it) {
+        for (int it = 0; it < ((dbg & 512) ? 0 : S); ++it) {
             const int m = 2 * (S - 1 - it);  // output of this pass: tile + 2(S-1-it), in the grid
             const int or0 = max(R - m, rmin), or1 = min(R + TH + m - 1, rmax);
             const int oc0 = max(R - m, cmin), oc1 = min(R + TW + m - 1, cmax);
@@ -1155,8 +1160,11 @@ cudaError_t launch_cfg(sf_ctx* c, const float* Y, const float* D) {
         const bool upd = l == p.launches - 1;
         FusedArgs a;
         {
-            const char* dbg = getenv("SF_DEBUG_SKIP");
-            a.dbg_skip = dbg ? atoi(dbg) : 0;
+            static const int dbg_env = [] {
+                const char* e = getenv("SF_DEBUG_SKIP");
+                return e ? atoi(e) : 0;
+            }();
+            a.dbg_skip = dbg_env;
         }
         a.tma = getenv("SF_NO_TMA") == nullptr && encode3d(&a.tmE, c->E, f.W, f.H, 6, FC::RW, FC::RH, 3) &&
                 encode3d(&a.tmY, Y, f.W, f.H, f.B, FC::RW, FC::RH, 1) &&
