@@ -25,6 +25,8 @@
 #include <stdio.h>
 #include <stdlib.h>
 
+#include <mutex>
+
 #include "sf_internal.cuh"
 
 namespace {
@@ -1136,8 +1138,52 @@ EncodeTiledFn encode_fn() {
     return fn;
 }
 
-// 3-D fp32 tensor [d2][H][W], box RW x RH x bz
+// Process-wide switches read once: SF_NO_TMA (cp.async staging), SF_NO_PDL (no programmatic
+// dependent launch).
+bool env_flag(const char* name) { return getenv(name) != nullptr; }
+bool no_tma() {
+    static const bool v = env_flag("SF_NO_TMA");
+    return v;
+}
+bool no_pdl() {
+    static const bool v = env_flag("SF_NO_PDL");
+    return v;
+}
+
+// 3-D fp32 tensor [d2][H][W], box RW x RH x bz.  Encodings are memoised (a few host µs each;
+// the per-frame inputs alternate between a handful of buffers): a small direct-mapped cache.
+bool encode3d_raw(CUtensorMap* m, const float* base, int W, int H, int d2, int RW, int RH, int bz);
 bool encode3d(CUtensorMap* m, const float* base, int W, int H, int d2, int RW, int RH, int bz) {
+    struct Entry {
+        const float* base;
+        int W, H, d2, RW, RH, bz;
+        bool ok;
+        CUtensorMap map;
+    };
+    static Entry cache[16];
+    static bool valid[16];
+    static std::mutex mu;  // contexts may launch from several host threads
+    std::lock_guard<std::mutex> lock(mu);
+    const size_t h = ((reinterpret_cast<uintptr_t>(base) >> 8) ^ (size_t)(W * 31 + H * 7 + d2 * 3 + RH + bz)) & 15;
+    Entry& e = cache[h];
+    if (valid[h] && e.base == base && e.W == W && e.H == H && e.d2 == d2 && e.RW == RW && e.RH == RH && e.bz == bz) {
+        *m = e.map;
+        return e.ok;
+    }
+    e.ok = encode3d_raw(&e.map, base, W, H, d2, RW, RH, bz);
+    e.base = base;
+    e.W = W;
+    e.H = H;
+    e.d2 = d2;
+    e.RW = RW;
+    e.RH = RH;
+    e.bz = bz;
+    valid[h] = true;
+    *m = e.map;
+    return e.ok;
+}
+
+bool encode3d_raw(CUtensorMap* m, const float* base, int W, int H, int d2, int RW, int RH, int bz) {
     EncodeTiledFn fn = encode_fn();
     if (!fn || (W & 3) || (reinterpret_cast<uintptr_t>(base) & 15)) return false;
     const cuuint64_t dims[3] = {(cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)d2};
@@ -1166,7 +1212,7 @@ cudaError_t launch_cfg(sf_ctx* c, const float* Y, const float* D) {
             }();
             a.dbg_skip = dbg_env;
         }
-        a.tma = getenv("SF_NO_TMA") == nullptr && encode3d(&a.tmE, c->E, f.W, f.H, 6, FC::RW, FC::RH, 3) &&
+        a.tma = !no_tma() && encode3d(&a.tmE, c->E, f.W, f.H, 6, FC::RW, FC::RH, 3) &&
                 encode3d(&a.tmY, Y, f.W, f.H, f.B, FC::RW, FC::RH, 1) &&
                 encode3d(&a.tmD, D, f.W, f.H, f.B, FC::RW, FC::RH, 1);
         a.fin = src;
@@ -1198,7 +1244,7 @@ cudaError_t launch_cfg(sf_ctx* c, const float* Y, const float* D) {
         lc.stream = c->stream;
         cudaLaunchAttribute at[1];
         at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL
-        at[0].val.programmaticStreamSerializationAllowed = getenv("SF_NO_PDL") ? 0 : 1;
+        at[0].val.programmaticStreamSerializationAllowed = no_pdl() ? 0 : 1;
         lc.attrs = at;
         lc.numAttrs = 1;
         cudaError_t e = cudaLaunchKernelEx(&lc, kern, a);
@@ -1237,7 +1283,7 @@ cudaError_t launch_low(sf_ctx* c) {
         a.R = (a.M + 3) & ~3;
         a.TW = LC::RW - 2 * a.R;
         a.TH = LC::RH - 2 * a.R;
-        a.tma = getenv("SF_NO_TMA") == nullptr && encode3d(&a.tmE, c->E, f.W, f.H, 6, LC::RW, LC::RH, 3);
+        a.tma = !no_tma() && encode3d(&a.tmE, c->E, f.W, f.H, 6, LC::RW, LC::RH, 3);
         a.finA = srcA;
         a.finW = srcW;
         const bool last = ((L - 1 - l) & 1) == 0;
@@ -1258,7 +1304,7 @@ cudaError_t launch_low(sf_ctx* c) {
         lc.stream = c->stream;
         cudaLaunchAttribute at[1];
         at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-        at[0].val.programmaticStreamSerializationAllowed = getenv("SF_NO_PDL") ? 0 : 1;
+        at[0].val.programmaticStreamSerializationAllowed = no_pdl() ? 0 : 1;
         lc.attrs = at;
         lc.numAttrs = 1;
         cudaError_t e = cudaLaunchKernelEx(&lc, kern, a);
