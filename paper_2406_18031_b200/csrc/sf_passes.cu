@@ -239,43 +239,47 @@ __global__ void __launch_bounds__(BX* BY) k_solve(const float* __restrict__ HG, 
     raise_flag(flags, bad, SF_FLAG_NONFINITE);
 }
 
-// 5x5 box smoothing (reading 13): horizontal 5-sum, then vertical 5-sum / 25.
-// .w (rho^{k+1}) rides along unchanged.
-__global__ void __launch_bounds__(BX* BY) k_box_h(const float4* __restrict__ in, float4* __restrict__ out,
-                                                 FrameParams f) {
-    const int j = blockIdx.x * BX + threadIdx.x, i = blockIdx.y * BY + threadIdx.y, b = blockIdx.z;
-    if (i >= f.H || j >= f.W) return;
-    const float4* row = in + ((size_t)b * f.H + i) * f.W;
-    float4 a = row[max(j - 2, 0)];
-#pragma unroll
-    for (int k = -1; k <= 2; ++k) {
-        const float4 v = row[iclamp(j + k, 0, f.W - 1)];
-        a.x = xadd(a.x, v.x);
-        a.y = xadd(a.y, v.y);
-        a.z = xadd(a.z, v.z);
-    }
-    a.w = row[j].w;
-    out[((size_t)b * f.H + i) * f.W + j] = a;
-}
-
-__global__ void __launch_bounds__(BX* BY) k_box_v(const float4* __restrict__ in, float4* __restrict__ out,
-                                                 FrameParams f) {
-    const int j = blockIdx.x * BX + threadIdx.x, i = blockIdx.y * BY + threadIdx.y, b = blockIdx.z;
-    if (i >= f.H || j >= f.W) return;
+// 5x5 box smoothing (reading 13); .w (rho^{k+1}) rides along unchanged.
+// One whole box iteration (horizontal 5-sums, then vertical 5-sums / 25; the order of k_box_h +
+// k_box_v) per launch: the block stages its (BY + 4) x (BX + 4) window (replicate border) in
+// shared memory, forms the horizontal sums of its BY + 4 rows, then the vertical sums.
+__global__ void __launch_bounds__(BX* BY) k_box(const float4* __restrict__ in, float4* __restrict__ out,
+                                               FrameParams f) {
+    __shared__ float3 win[BY + 4][BX + 4];
+    __shared__ float3 hs[BY + 4][BX];
+    const int tx = threadIdx.x, ty = threadIdx.y, b = blockIdx.z;
+    const int j0 = blockIdx.x * BX, i0 = blockIdx.y * BY;
     const float4* pl = in + (size_t)b * f.H * f.W;
-    float4 a = pl[(size_t)max(i - 2, 0) * f.W + j];
+    for (int t = ty * BX + tx; t < (BY + 4) * (BX + 4); t += BX * BY) {
+        const int r = t / (BX + 4), c = t % (BX + 4);
+        const float4 v = pl[(size_t)iclamp(i0 + r - 2, 0, f.H - 1) * f.W + iclamp(j0 + c - 2, 0, f.W - 1)];
+        win[r][c] = make_float3(v.x, v.y, v.z);
+    }
+    __syncthreads();
+    for (int r = ty; r < BY + 4; r += BY) {
+        float3 a = win[r][tx];
 #pragma unroll
-    for (int k = -1; k <= 2; ++k) {
-        const float4 v = pl[(size_t)iclamp(i + k, 0, f.H - 1) * f.W + j];
+        for (int k = 1; k < 5; ++k) {
+            const float3 v = win[r][tx + k];
+            a.x = xadd(a.x, v.x);
+            a.y = xadd(a.y, v.y);
+            a.z = xadd(a.z, v.z);
+        }
+        hs[r][tx] = a;
+    }
+    __syncthreads();
+    const int i = i0 + ty, j = j0 + tx;
+    if (i >= f.H || j >= f.W) return;
+    float3 a = hs[ty][tx];
+#pragma unroll
+    for (int k = 1; k < 5; ++k) {
+        const float3 v = hs[ty + k][tx];
         a.x = xadd(a.x, v.x);
         a.y = xadd(a.y, v.y);
         a.z = xadd(a.z, v.z);
     }
-    a.x = div25(a.x);
-    a.y = div25(a.y);
-    a.z = div25(a.z);
-    a.w = pl[(size_t)i * f.W + j].w;
-    out[((size_t)b * f.H + i) * f.W + j] = a;
+    const size_t p = ((size_t)b * f.H + i) * f.W + j;
+    out[p] = make_float4(div25(a.x), div25(a.y), div25(a.z), in[p].w);
 }
 
 __global__ void k_unpack(const float4* __restrict__ src, float* w, float* rho, size_t n) {
@@ -330,9 +334,10 @@ cudaError_t sf_launch_update_passes(sf_ctx* c, const float* Y, const float* D, b
     float4* solved = f.S > 0 ? c->tmp : nxt;
     k_solve<<<g, blk, 0, c->stream>>>(c->HG, c->HH, D, c->pred, c->state[c->cur], c->yhat[c->cur], 1,
                                       c->yhat[1 - c->cur], solved, c->G0, c->G1, c->G2, f, c->flags);
-    for (int s = 0; s < f.S; ++s) {
-        k_box_h<<<g, blk, 0, c->stream>>>(c->tmp, c->tmp2, f);
-        k_box_v<<<g, blk, 0, c->stream>>>(c->tmp2, s == f.S - 1 ? nxt : c->tmp, f);
+    for (int s = 0; s < f.S; ++s) {  // ping-pong tmp <-> tmp2, the last pass into nxt
+        const float4* src = (s & 1) ? c->tmp2 : c->tmp;
+        float4* dst = s == f.S - 1 ? nxt : ((s & 1) ? c->tmp : c->tmp2);
+        k_box<<<g, blk, 0, c->stream>>>(src, dst, f);
     }
     return cudaGetLastError();
 }
@@ -380,9 +385,10 @@ cudaError_t sf_launch_update_low(sf_ctx* c, const float* Y, const float* D, bool
     float4* solved = f.S > 0 ? c->tmp : nxt;
     k_solve<<<g, blk, 0, c->stream>>>(c->HG, c->HH, D, c->pred, c->pred, reinterpret_cast<const float*>(c->Wpred) + 3,
                                       4, c->yhat[0], solved, c->G0, c->G1, c->G2, f, c->flags);
-    for (int s = 0; s < f.S; ++s) {
-        k_box_h<<<g, blk, 0, c->stream>>>(c->tmp, c->tmp2, f);
-        k_box_v<<<g, blk, 0, c->stream>>>(c->tmp2, s == f.S - 1 ? nxt : c->tmp, f);
+    for (int s = 0; s < f.S; ++s) {  // ping-pong tmp <-> tmp2, the last pass into nxt
+        const float4* src = (s & 1) ? c->tmp2 : c->tmp;
+        float4* dst = s == f.S - 1 ? nxt : ((s & 1) ? c->tmp : c->tmp2);
+        k_box<<<g, blk, 0, c->stream>>>(src, dst, f);
     }
     return cudaGetLastError();
 }
