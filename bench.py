@@ -390,7 +390,7 @@ def run_sf(args):
         sm_max = pk.get("sm_max_mhz", 1965.0)
         alu_peak = SMS * FP32_LANES_PER_SM * sm_max * 1e6 / 1e12  # TFLOP/s-equivalent FP32 lane-ops
         alu = ops / (mean_ms / 1e3) / 1e12
-        kname = "k_fused" if m.kernel == sf.SF_KERNEL_FUSED else "whole step (2N+2+S per-pass kernels)"
+        kname = "k_fused" if m.kernel == sf.SF_KERNEL_FUSED else "whole step (2N+1+S per-pass kernels)"
         if levels == 2:
             kname = "whole step (top level fused + bottom-level pass kernels)"
         tr = ncu_traffic() if (m.kernel == sf.SF_KERNEL_FUSED and levels == 1) else None

@@ -60,7 +60,7 @@ enum {
 enum {
     SF_KERNEL_AUTO = 0,   /* fused when available for the configuration, else passes     */
     SF_KERNEL_FUSED = 1,  /* one on-chip kernel per frame (predict + update)             */
-    SF_KERNEL_PASSES = 2  /* one kernel per pass / stage (2N + 2 + S launches per frame)  */
+    SF_KERNEL_PASSES = 2  /* one kernel per pass / stage (2N + 1 + S launches per frame)  */
 };
 
 typedef struct sf_ctx sf_ctx; /* opaque; owns all device state */

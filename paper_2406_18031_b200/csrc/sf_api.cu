@@ -486,11 +486,11 @@ extern "C" int32_t sf_kernel_in_use(const sf_ctx* c) { return c ? c->kernel : 0;
 
 extern "C" int32_t sf_launches_per_step(const sf_ctx* c) {
     if (!c) return 0;
-    if (c->levels == 2)  // down2 + top + bottom prediction + hconv + solve + S box + up2
-        return 1 + sf_launches_per_step(c->top) + (c->low_fused ? sf_low_fused_launches(c) : 2 * c->fp.N) + 2 +
+    if (c->levels == 2)  // down2 + top + bottom prediction + update + S box + up2
+        return 1 + sf_launches_per_step(c->top) + (c->low_fused ? sf_low_fused_launches(c) : 2 * c->fp.N) + 1 +
                c->fp.S + 1;
     if (c->kernel == SF_KERNEL_FUSED) return sf_fused_launches(c);
-    return 2 * c->fp.N + 2 + c->fp.S;
+    return 2 * c->fp.N + 1 + c->fp.S;
 }
 
 extern "C" const char* sf_error_string(sf_status s) {

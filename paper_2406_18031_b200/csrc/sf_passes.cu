@@ -197,19 +197,52 @@ __global__ void __launch_bounds__(BX* BY) k_init(const float* __restrict__ HG, c
     yhat[p] = M.yh;
 }
 
-// Models + per-pixel LS + fusion (U1-U3, U5).  Reads w^{k+}, rho^{k+} (pred), rho^k (st),
-// Yhat^k (yin); writes (w_LS, rho^{k+1}) to out and Yhat^{k+1} to yout.
-__global__ void __launch_bounds__(BX* BY) k_solve(const float* __restrict__ HG, const float* __restrict__ HH,
-                                                 const float* __restrict__ D, const float4* __restrict__ pred,
-                                                 const float4* __restrict__ st, const float* __restrict__ yin, int ys,
-                                                 float* __restrict__ yout, float4* out,
-                                                 const float4* __restrict__ G0, const float4* __restrict__ G1,
-                                                 const float4* __restrict__ G2, FrameParams f, unsigned* flags) {
-    const int j = blockIdx.x * BX + threadIdx.x, i = blockIdx.y * BY + threadIdx.y, b = blockIdx.z;
+// Models + per-pixel LS + fusion (U1-U3, U5) in one launch (reads w^{k+}, rho^{k+} from pred,
+// rho^k from st, Yhat^k from yin[i * ys]; writes (w_LS, rho^{k+1}) to out, Yhat^{k+1} to yout): the block stages its (BY + 4) x (BX + 4) brightness window
+// (replicate border) in shared memory, forms the horizontal g- and h-taps of its BY + 4 rows,
+// then every pixel takes the vertical taps, the inverse-depth model, the LS solve and the
+// fusion (operation order: DESIGN.md section 4).
+__global__ void __launch_bounds__(BX* BY) k_update(const float* __restrict__ Y, const float* __restrict__ D,
+                                                  const float4* __restrict__ pred, const float4* __restrict__ st,
+                                                  const float* __restrict__ yin, int ys, float* __restrict__ yout,
+                                                  float4* out, const float4* __restrict__ G0,
+                                                  const float4* __restrict__ G1, const float4* __restrict__ G2,
+                                                  FrameParams f, unsigned* flags) {
+    __shared__ float yw[BY + 4][BX + 4];
+    __shared__ float hgs[BY + 4][BX], hhs[BY + 4][BX];
+    const int tx = threadIdx.x, ty = threadIdx.y, b = blockIdx.z;
+    const int j0 = blockIdx.x * BX, i0 = blockIdx.y * BY;
+    const float* Yp = Y + (size_t)b * f.H * f.W;
+    for (int t = ty * BX + tx; t < (BY + 4) * (BX + 4); t += BX * BY) {
+        const int r = t / (BX + 4), c = t % (BX + 4);
+        yw[r][c] = Yp[(size_t)iclamp(i0 + r - 2, 0, f.H - 1) * f.W + iclamp(j0 + c - 2, 0, f.W - 1)];
+    }
+    __syncthreads();
+    for (int r = ty; r < BY + 4; r += BY) {
+        const float x0 = yw[r][tx], x1 = yw[r][tx + 1], x2 = yw[r][tx + 2], x3 = yw[r][tx + 3], x4 = yw[r][tx + 4];
+        hgs[r][tx] = tap_g(x0, x1, x2, x3, x4);
+        hhs[r][tx] = tap_h(x0, x1, x2, x3, x4);
+    }
+    __syncthreads();
+    const int j = j0 + tx, i = i0 + ty;
     const bool live = (i < f.H) && (j < f.W);
     bool bad = false;
     if (live) {
-        const Models M = eval_models(HG, HH, D, b, i, j, f);
+        bad = !isfinite(yw[ty + 2][tx + 2]) && i >= f.fr0 && i < f.fr1;  // as k_hconv
+        Models M;
+        M.yh = tap_g(hgs[ty][tx], hgs[ty + 1][tx], hgs[ty + 2][tx], hgs[ty + 3][tx], hgs[ty + 4][tx]);
+        M.b1 = tap_g(hhs[ty][tx], hhs[ty + 1][tx], hhs[ty + 2][tx], hhs[ty + 3][tx], hhs[ty + 4][tx]);
+        M.b2 = tap_h(hgs[ty][tx], hgs[ty + 1][tx], hgs[ty + 2][tx], hgs[ty + 3][tx], hgs[ty + 4][tx]);
+        const float* Dp = D + (size_t)b * f.H * f.W;
+        const float dc = Dp[(size_t)i * f.W + j];
+        const float dl = Dp[(size_t)i * f.W + max(j - 1, 0)], dr = Dp[(size_t)i * f.W + min(j + 1, f.W - 1)];
+        const float du = Dp[(size_t)max(i - 1, 0) * f.W + j], dd = Dp[(size_t)min(i + 1, f.H - 1) * f.W + j];
+        const bool vc = depth_valid(dc, f.is_inv), vl = depth_valid(dl, f.is_inv), vr = depth_valid(dr, f.is_inv),
+                   vu = depth_valid(du, f.is_inv), vd = depth_valid(dd, f.is_inv);
+        M.rh = rho_hat(dc, f.is_inv);
+        M.br1 = pick_side(M.rh, vc, rho_hat(dl, f.is_inv), vl, rho_hat(dr, f.is_inv), vr);
+        M.br2 = pick_side(M.rh, vc, rho_hat(du, f.is_inv), vu, rho_hat(dd, f.is_inv), vd);
+        M.valid = vc;
         const int gi = i * f.W + j;
         const size_t p = (size_t)b * f.H * f.W + gi;
         const float4 s = G0[gi], e1 = G1[gi], e2 = G2[gi];
@@ -219,22 +252,22 @@ __global__ void __launch_bounds__(BX* BY) k_solve(const float* __restrict__ HG, 
         const float d2r = xmul(d2, M.rh);
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
-            gh[a] = xmul(d2, xfma(e2a[a], M.b2, xmul(e1a[a], M.b1)));          // ghat (eq:img_gradient)
-            const float dr = xmul(d2, xfma(e2a[a], M.br2, xmul(e1a[a], M.br1)));  // drho (eq:inv_depth_gradient)
-            m[a] = xfma(d2r, sa[a], dr);
+            gh[a] = xmul(d2, xfma(e2a[a], M.b2, xmul(e1a[a], M.b1)));
+            const float drr = xmul(d2, xfma(e2a[a], M.br2, xmul(e1a[a], M.br1)));
+            m[a] = xfma(d2r, sa[a], drr);
         }
         const float4 wp = pred[p];
         const float4 sk = st[p];
-        const float cY = xmul(d2, xsub(M.yh, yin[p * ys]));  // d2 (Yhat^{k+1} - Yhat^k), eq:img_cost_top
-        const float cr = xmul(d2, xsub(M.rh, sk.w));     // d2 (rhohat - rho^k), eq:invdepth_cost_top
+        const float cY = xmul(d2, xsub(M.yh, yin[p * ys]));
+        const float cr = xmul(d2, xsub(M.rh, sk.w));
         const float wpa[3] = {wp.x, wp.y, wp.z};
         float x[3];
         ls_solve3(gh, m, cY, cr, wpa, f.g1, M.valid ? f.g2 : 0.0f, f.g3, x);
         const float kap = M.valid ? f.kappa : 0.0f;
-        const float rn = xfma(kap, xsub(M.rh, wp.w), wp.w);  // fusion (reading 21)
+        const float rn = xfma(kap, xsub(M.rh, wp.w), wp.w);
         out[p] = make_float4(x[0], x[1], x[2], rn);
         yout[p] = M.yh;
-        bad = !(isfinite(x[0]) && isfinite(x[1]) && isfinite(x[2]) && isfinite(rn)) && i >= f.fr0 && i < f.fr1;
+        bad = bad || (!(isfinite(x[0]) && isfinite(x[1]) && isfinite(x[2]) && isfinite(rn)) && i >= f.fr0 && i < f.fr1);
     }
     raise_flag(flags, bad, SF_FLAG_NONFINITE);
 }
@@ -325,15 +358,15 @@ cudaError_t sf_launch_predict_passes(sf_ctx* c) {
 cudaError_t sf_launch_update_passes(sf_ctx* c, const float* Y, const float* D, bool init) {
     const FrameParams& f = c->fp;
     const dim3 g = grid_for(f), blk(BX, BY);
-    k_hconv<<<g, blk, 0, c->stream>>>(Y, c->HG, c->HH, f, c->flags);
     if (init) {
+        k_hconv<<<g, blk, 0, c->stream>>>(Y, c->HG, c->HH, f, c->flags);
         k_init<<<g, blk, 0, c->stream>>>(c->HG, c->HH, D, c->state[c->cur], c->yhat[c->cur], f);
         return cudaGetLastError();
     }
     float4* nxt = c->state[1 - c->cur];
     float4* solved = f.S > 0 ? c->tmp : nxt;
-    k_solve<<<g, blk, 0, c->stream>>>(c->HG, c->HH, D, c->pred, c->state[c->cur], c->yhat[c->cur], 1,
-                                      c->yhat[1 - c->cur], solved, c->G0, c->G1, c->G2, f, c->flags);
+    k_update<<<g, blk, 0, c->stream>>>(Y, D, c->pred, c->state[c->cur], c->yhat[c->cur], 1, c->yhat[1 - c->cur],
+                                       solved, c->G0, c->G1, c->G2, f, c->flags);
     for (int s = 0; s < f.S; ++s) {  // ping-pong tmp <-> tmp2, the last pass into nxt
         const float4* src = (s & 1) ? c->tmp2 : c->tmp;
         float4* dst = s == f.S - 1 ? nxt : ((s & 1) ? c->tmp : c->tmp2);
@@ -376,15 +409,15 @@ cudaError_t sf_launch_predict_low(sf_ctx* c) {
 cudaError_t sf_launch_update_low(sf_ctx* c, const float* Y, const float* D, bool init) {
     const FrameParams& f = c->fp;
     const dim3 g = grid_for(f), blk(BX, BY);
-    k_hconv<<<g, blk, 0, c->stream>>>(Y, c->HG, c->HH, f, c->flags);
     if (init) {
+        k_hconv<<<g, blk, 0, c->stream>>>(Y, c->HG, c->HH, f, c->flags);
         k_init<<<g, blk, 0, c->stream>>>(c->HG, c->HH, D, c->state[c->cur], c->yhat[0], f);
         return cudaGetLastError();
     }
     float4* nxt = c->state[1 - c->cur];
     float4* solved = f.S > 0 ? c->tmp : nxt;
-    k_solve<<<g, blk, 0, c->stream>>>(c->HG, c->HH, D, c->pred, c->pred, reinterpret_cast<const float*>(c->Wpred) + 3,
-                                      4, c->yhat[0], solved, c->G0, c->G1, c->G2, f, c->flags);
+    k_update<<<g, blk, 0, c->stream>>>(Y, D, c->pred, c->pred, reinterpret_cast<const float*>(c->Wpred) + 3, 4,
+                                       c->yhat[0], solved, c->G0, c->G1, c->G2, f, c->flags);
     for (int s = 0; s < f.S; ++s) {  // ping-pong tmp <-> tmp2, the last pass into nxt
         const float4* src = (s & 1) ? c->tmp2 : c->tmp;
         float4* dst = s == f.S - 1 ? nxt : ((s & 1) ? c->tmp : c->tmp2);
