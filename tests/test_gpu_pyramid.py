@@ -71,3 +71,25 @@ def test_pyramid_eval_and_unsupported():
             call()
         assert e.value.status == sf.SF_E_UNSUPPORTED
     assert sf.sf_launches_per_step(m.ctx) > 0
+
+
+@pytest.mark.parametrize("max_flow,S,rule", [(11.0, 1, 0), (3.0, 3, 1)])
+def test_pyramid_multi_launch_and_variants(max_flow, S, rule):
+    """N1 = 11 (two bottom-level k_low launches, top N2 = 6), S1 = 1; and N1 = 3 with S1 = 3 and the
+    printed dominant rule — bitwise against the pyramid oracle every frame."""
+    import dataclasses
+
+    import paper_2406_18031_b200 as sf
+    seq = sfgen.config_sequence(1, frames=4, H=128, W=96)
+    p = dataclasses.replace(seq.params, max_flow=max_flow, smooth_iters=S, dominant_rule=rule)
+    levels = grid.gnomonic_pyramid(128, 96, seq.fov)
+    po = oracle.PyramidOracle(levels[0], levels[1], p)
+    m = sf.StructureFlow(levels, p)
+    for k in range(4):
+        m.step(_dev(seq.Y[k][None]), _dev(seq.depth[k][None]))
+        po.step(seq.Y[k], seq.depth[k])
+        w, rho, yhat = m.get_fields()
+        torch.cuda.synchronize()
+        assert np.array_equal(w[0].cpu().numpy(), po.w), f"w frame {k}"
+        assert np.array_equal(rho[0].cpu().numpy(), po.rho), f"rho frame {k}"
+    assert sf.sf_status_flags(m.ctx)[1] == po.flags
