@@ -40,6 +40,9 @@ __global__ void k(float* out, float a, float b, long long* cyc) {
             if (OP == 6) { u[i] = u[i] * 2654435761u + 12345u; }
             if (OP == 7) { u[i] = (u[i] ^ 0x5a5a) + (u[i] >> 3); }
             if (OP == 8) { x[i] = fmaxf(x[i], y[i]) ; y[i] = fminf(y[i], x[i]); }
+            if (OP == 9) { x[i] = __shfl_sync(0xffffffffu, x[i], (threadIdx.x + i + 1) & 31); }
+            if (OP == 10) { x[i] = __shfl_down_sync(0xffffffffu, x[i], 1); }
+            if (OP == 11) { x[i] = (x[i] > y[i]) ? x[i] : y[i] + 1.0f; }
         }
     }
     long long t1 = clock64();
@@ -68,6 +71,8 @@ int main() {
         run<0>("FFMA", nt, 1); run<1>("FADD", nt, 1); run<2>("FMUL", nt, 1); run<3>("FFMA2", nt, 1);
         run<4>("FADD2", nt, 1); run<5>("FFMA+2alu", nt, 3); run<6>("IMAD", nt, 1); run<7>("LOP3/IADD", nt, 2);
         run<8>("FMNMX", nt, 2);
+        run<9>("SHFL.IDX", nt, 1);
+        run<10>("SHFL.DOWN", nt, 1);
     }
     return 0;
 }
