@@ -220,8 +220,9 @@ def run_sf(args):
     # batch steps already read > L2 per step (64 MiB x 2): a short ring of rendered frames
     ring = args.ring if B == 1 else 8
     # independent sequence(s) per rank (seeds differ); frames of the sequence fill the ring
-    seqs = [sfgen.config_sequence(2 if cid == 4 else cid, frames=ring,
-                                  seed=(base["seed"] + 1000 * rank + b)) for b in range(B)]
+    mf = getattr(args, "max_flow", None)
+    seqs = [sfgen.config_sequence(2 if cid == 4 else cid, frames=ring, seed=(base["seed"] + 1000 * rank + b),
+                                  max_flow=mf) for b in range(B)]
     geom, params = seqs[0].geom, seqs[0].params
     if B == 1:
         Yh, Dh = seqs[0].Y, seqs[0].depth
@@ -406,7 +407,8 @@ def run_sf(args):
         out = {"metric": METRIC, "value": value, "unit": "Hz", "n_gpus": world, "steps": args.steps,
                "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
                "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-               "config": {"workload": CONFIG_NAMES[cid] if levels == 1 else CONFIG_NAMES_PYR[cid],
+               "config": {"workload": (CONFIG_NAMES[cid] if levels == 1 else CONFIG_NAMES_PYR[cid]) +
+                                      (f" [max flow overridden: {mf} px]" if mf else ""),
                           "batch_per_gpu": B, "H": H, "W": W, "N": params.N, "levels": levels,
                           "S": params.smooth_iters, "parallelism": f"independent sequences x{world}",
                           "inputs": f"ring of {ring} frames ({ring * 2 * frame_bytes / 2**20:.0f} MiB) > L2, "
@@ -535,6 +537,8 @@ def main():
     ap.add_argument("--impl", choices=["sf", "reference"], default="sf")
     ap.add_argument("--config", type=int, choices=[2, 3, 4, 5], default=2)
     ap.add_argument("--kernel", choices=["auto", "fused", "passes"], default="auto")
+    ap.add_argument("--max-flow", type=float, default=None,
+                    help="override the workload's max flow (px; N = ceil) -- for the paper's Table 2/3 sweeps")
     ap.add_argument("--map", action="store_true",
                     help="include the Spherepix input mapping of a 640x640 camera frame in every step (P:L785)")
     ap.add_argument("--levels", type=int, choices=[1, 2], default=1,

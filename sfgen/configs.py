@@ -194,8 +194,10 @@ def band_sequence(cid: int, r0: int, r1: int, frames: int, seed: int | None = No
 
 
 def config_sequence(cid: int, frames: int | None = None, H: int | None = None, W: int | None = None,
-                    seed: int | None = None, with_gt: bool = False) -> Sequence:
+                    seed: int | None = None, with_gt: bool = False, max_flow: float | None = None) -> Sequence:
     c = dict(CONFIGS[cid])
+    if max_flow is not None:
+        c["max_flow"] = max_flow
     if frames is not None:
         c["frames"] = frames
     if H is not None:
