@@ -267,9 +267,7 @@ def run_sf(args):
             m.step(Yd[k], Dd[k])
         else:
             Hc, Wc, K, Yc, Zc, Ym, Dm = cam
-            sf.sf_map_inputs(m.ctx, Yc[k].data_ptr(), Zc[k].data_ptr(), Hc, Wc, K, None, Ym.data_ptr(),
-                             Dm.data_ptr())
-            m.step(Ym, Dm)
+            sf.sf_step_camera(m.ctx, Yc[k].data_ptr(), Zc[k].data_ptr(), Hc, Wc, K, None)
 
     with torch.cuda.stream(s):
         do_step(0)  # frame 0: initialisation (not a timed step)
@@ -290,7 +288,7 @@ def run_sf(args):
                 k = frame_of(pos0 + c * CHUNK + t)
                 do_step(k)
         chunks.append(g)
-    launches = m.launches_per_step + (1 if cam is not None else 0)
+    launches = m.launches_per_step + (1 if cam is not None else 0)  # sf_step_camera: + the mapping kernel
     state = {"i": pos0}
 
     def run_steps(n):
@@ -414,7 +412,7 @@ def run_sf(args):
                           "inputs": f"ring of {ring} frames ({ring * 2 * frame_bytes / 2**20:.0f} MiB) > L2, "
                                     "replayed palindromically, cold reads each step; CUDA graphs of 8 steps",
                           "kernel": {sf.SF_KERNEL_FUSED: "fused", sf.SF_KERNEL_PASSES: "passes"}.get(m.kernel),
-                          "input_mapping": ("pinhole camera 640x640 90 deg -> grid (sf_map_inputs) inside each step"
+                          "input_mapping": ("pinhole camera 640x640 90 deg -> grid (sf_step_camera) inside each step"
                                             if cam is not None else "inputs already on the grid")},
                "roofline": roof, "gpu_launches": launches * args.steps, "step_ms_median": med_ms,
                "e2e": {"value": e2e_value, "unit": "Hz", "h2d_bytes_per_step": 2 * frame_bytes,

@@ -213,6 +213,11 @@ sf_status sf_eval(sf_ctx* ctx, const float* w_gt, float* rmse, double* aae_deg, 
 sf_status sf_map_inputs(sf_ctx* ctx, const float* Ycam, const float* Zcam, int32_t cam_height, int32_t cam_width,
                         const float* K, const float* Rcg, float* Y, float* D);
 
+/* One frame straight from camera images (arguments as sf_map_inputs): sf_map_inputs into the
+ * context's own grid buffers, then sf_step.  Errors: as sf_map_inputs and sf_step. */
+sf_status sf_step_camera(sf_ctx* ctx, const float* Ycam, const float* Zcam, int32_t cam_height, int32_t cam_width,
+                         const float* K, const float* Rcg);
+
 /* ---- banded mode -------------------------------------------------------------------------
  * Halo rows a band needs so that its owned rows are exact after one sf_step: the transport
  * moves information N rows per frame (eq:numerical_stability), the update reads +-2 rows of

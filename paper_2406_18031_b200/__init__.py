@@ -25,7 +25,8 @@ SF_ABI_VERSION = 1
 EXPORTS = ("sf_config_default", "sf_create", "sf_destroy", "sf_predict", "sf_update", "sf_step", "sf_step_host",
            "sf_get_fields", "sf_set_fields", "sf_status_flags", "sf_kernel_in_use", "sf_launches_per_step",
            "sf_error_string", "sf_band_halo", "sf_band_partition", "sf_halo_exchange_peer", "sf_halo_exchange_nccl",
-           "sf_nccl_unique_id", "sf_nccl_comm_init", "sf_nccl_comm_destroy", "sf_flow_px", "sf_eval", "sf_map_inputs", "sf_set_motion", "sf_step_host_async", "sf_wait")
+           "sf_nccl_unique_id", "sf_nccl_comm_init", "sf_nccl_comm_destroy", "sf_flow_px", "sf_eval", "sf_map_inputs", "sf_set_motion", "sf_step_host_async", "sf_wait",
+           "sf_step_camera")
 
 
 class sf_config(C.Structure):
@@ -81,10 +82,12 @@ def _load():
     lib.sf_set_motion.argtypes = [P, P, P]
     lib.sf_step_host_async.argtypes = [P, P, P, P, P]
     lib.sf_wait.argtypes = [P]
+    lib.sf_step_camera.argtypes = [P, P, P, C.c_int32, C.c_int32, P, P]
     for name in ("sf_create", "sf_predict", "sf_update", "sf_step", "sf_step_host", "sf_get_fields",
                  "sf_set_fields", "sf_status_flags", "sf_kernel_in_use", "sf_launches_per_step", "sf_band_halo",
                  "sf_band_partition", "sf_halo_exchange_peer", "sf_halo_exchange_nccl", "sf_nccl_unique_id",
-                 "sf_nccl_comm_init", "sf_flow_px", "sf_eval", "sf_map_inputs", "sf_set_motion", "sf_step_host_async", "sf_wait"):
+                 "sf_nccl_comm_init", "sf_flow_px", "sf_eval", "sf_map_inputs", "sf_set_motion", "sf_step_host_async", "sf_wait",
+           "sf_step_camera"):
         getattr(lib, name).restype = C.c_int
     return lib
 
@@ -175,6 +178,14 @@ def sf_set_motion(ctx: int, omega=None, accel=None) -> None:
     ac = (C.c_float * 3)(*[float(x) for x in accel]) if accel is not None else None
     _check(_lib.sf_set_motion(C.c_void_p(ctx), C.cast(om, C.c_void_p) if om is not None else None,
                               C.cast(ac, C.c_void_p) if ac is not None else None), "sf_set_motion")
+
+
+def sf_step_camera(ctx: int, ycam_ptr: int, zcam_ptr: int, cam_height: int, cam_width: int, K, Rcg=None) -> None:
+    Kc = (C.c_float * 4)(*[float(x) for x in K])
+    Rc = (C.c_float * 9)(*[float(x) for x in list(Rcg)]) if Rcg is not None else None
+    _check(_lib.sf_step_camera(C.c_void_p(ctx), C.c_void_p(ycam_ptr), C.c_void_p(zcam_ptr), cam_height, cam_width,
+                               C.cast(Kc, C.c_void_p), C.cast(Rc, C.c_void_p) if Rc is not None else None),
+           "sf_step_camera")
 
 
 def sf_set_fields(ctx: int, w_ptr: int, rho_ptr: int, yhat_ptr: int | None) -> None:
@@ -298,7 +309,7 @@ class StructureFlow:
 
     def __del__(self):
         ctx = getattr(self, "ctx", None)
-        if ctx:
+        if ctx and callable(globals().get("sf_destroy")):  # (module globals are gone at interpreter exit)
             sf_destroy(ctx)
             self.ctx = None
 

@@ -56,7 +56,7 @@ static void free_ctx(sf_ctx* c) {
     if (!c) return;
     void* ptrs[] = {c->G0, c->G1, c->G2, c->E, c->state[0], c->state[1], c->pred, c->tmp, c->tmp2,
                     c->yhat[0], c->yhat[1], c->HG, c->HH, c->flags, c->hY, c->hD, c->hw, c->hr, c->eval_part,
-                    c->Wf[0], c->Wf[1], c->Wpred, c->Wtmp, c->Y2, c->D2};
+                    c->Wf[0], c->Wf[1], c->Wpred, c->Wtmp, c->Y2, c->D2, c->mY, c->mD};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (c->top) {
