@@ -24,10 +24,12 @@
  * ("Readings"); the arithmetic order below IS the definition the CUDA path
  * reproduces.
  *
- * Parity status: every function below is pinned by tests/test_oracle_*.py except
- * the full multi-frame trajectory on scenes with occlusions and an active flow
- * clamp, which is pinned only by invariants (C1-C7) and f32-vs-f64 agreement
- * (DESIGN.md "Parity unpinned").
+ * Parity status: every function below is pinned by tests/test_oracle_*.py
+ * (pins.py: the H = 1 filter; eval.py, pyramid.py, map.py, imu.py: the NEXT rows)
+ * except the full multi-frame trajectories on scenes with occlusions and an active
+ * flow clamp (H = 1 and the H = 2 pyramid), which are pinned only by invariants,
+ * closed-form special cases, f32-vs-f64 agreement and accuracy against the
+ * rendered ground truth.
  */
 #include <math.h>
 #include <stdint.h>
