@@ -221,8 +221,10 @@ def run_sf(args):
     ring = args.ring if B == 1 else 8
     # independent sequence(s) per rank (seeds differ); frames of the sequence fill the ring
     mf = getattr(args, "max_flow", None)
-    seqs = [sfgen.config_sequence(2 if cid == 4 else cid, frames=ring, seed=(base["seed"] + 1000 * rank + b),
-                                  max_flow=mf) for b in range(B)]
+    # config 4: the batch of 64 sequences has seeds 100..163, split over the ranks
+    seed0 = sfgen.CONFIGS[4]["seed"] + B * rank if cid == 4 else base["seed"] + 1000 * rank
+    seqs = [sfgen.config_sequence(2 if cid == 4 else cid, frames=ring, seed=seed0 + b, max_flow=mf)
+            for b in range(B)]
     geom, params = seqs[0].geom, seqs[0].params
     if B == 1:
         Yh, Dh = seqs[0].Y, seqs[0].depth

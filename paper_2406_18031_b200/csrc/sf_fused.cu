@@ -151,7 +151,7 @@ struct FusedArgs {
     int dbg_skip;       // timing experiments only (SF_DEBUG_SKIP): 1 = skip transport, 2 = skip update,
                         // 4 = no e TMA, 8 = no Y/depth TMA, 16 = no field / s loads, 32 = exit at entry,
                         // 64 = no column passes, 128 = no row passes, 256 = print phase clocks of CTA (6,5),
-                        // 512 = no box passes, 1024 = no solve
+                        // 512 = no box passes, 1024 = no solve, 2048 = print per-CTA globaltimer stamps
     const float4* fin;  // fields at launch start (state k or a partial prediction)
     const float4* sk;   // state k (rho^k for the update)
     float4* fout;       // state k+1 (upd) or partial prediction
@@ -502,6 +502,8 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
                       (blockIdx.x == 0 && blockIdx.y == 5) || (blockIdx.x == gridDim.x - 1 && blockIdx.y == gridDim.y - 1));
 #define SF_TICK() do { if (tim) { __syncthreads(); if (tid == 0) T_[nT_] = clock64(); ++nT_; } } while (0)
     SF_TICK();
+    unsigned long long gt0_ = 0, gt1_ = 0, gte_ = 0;  // dbg 2048: globaltimer at entry / griddep release / e planes in / exit
+    if (dbg & 2048) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt0_));
     // ---------------- staging: e1 / e2 planes (transport), Y and depth (update)
     uint64_t* const bars = reinterpret_cast<uint64_t*>(sm + 8 * P + C::XRF);
     if (a.tma) {
@@ -540,6 +542,7 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
         }
         cp_async_commit();
         griddep_wait();  // inputs / state of this frame may come from the preceding kernel
+        if (dbg & 2048) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt1_));
         if (a.upd) {
             if (!edgeC && !edgeR && (f.W & 3) == 0 && (gj0 & 3) == 0) {
                 for (int idx = tid; idx < P / 4; idx += NT) {
@@ -579,6 +582,7 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
     // and the frame's inputs may be written by the preceding kernel in the stream
     if (a.tma) {
         griddep_wait();
+        if (dbg & 2048) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt1_));
         if (tid == 0 && a.upd && !(dbg & 8)) {
             mbar_expect_tx(&bars[2], 2u * P * 4u);
             tma_load_3d(Ys, &a.tmY, gj0, gi0, b, &bars[2]);
@@ -601,6 +605,7 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
     if (a.tma && !(dbg & 4)) {
         mbar_wait(&bars[0], 0);
         mbar_wait(&bars[1], 0);
+        if (dbg & 2048) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gte_));
         if (edgeC || edgeR) {  // replica cells next to grid edges take the edge cell's e (reading 10)
             __syncthreads();
             if (cmin > 0 || cmax < RW - 1)
@@ -912,6 +917,11 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
                T_[nT_ - 1] - T_[0]);
     }
 #undef SF_TICK
+    if ((dbg & 2048) && tid == 0) {
+        unsigned long long t2_;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t2_));
+        printf("SFGT %d %d %llu %llu %llu %llu\n", blockIdx.x, blockIdx.y, gt0_, gt1_, t2_, gte_);
+    }
     const unsigned any = __reduce_or_sync(FULL, fl);
     if (lane == 0 && any) atomicOr(a.flags, any);
 }

@@ -264,6 +264,32 @@ def test_config3_1024_n16(kernel):
     run_pair(seq, 4, kernel)
 
 
+def test_config4_batch64_full_size():
+    """configs[3] at full size: 64 independent 512 x 512 sequences (seeds 100..163, the generator of
+    config 2) in ONE context, the launch configuration bench.py --config 4 times (fused kernel,
+    B = 64 -> 9152 CTAs); every member is checked against its own single-sequence oracle, bitwise,
+    after each of 3 frames."""
+    sf = _sf()
+    frames = 3
+    seqs = [sfgen.config_sequence(2, frames=frames, seed=100 + b) for b in range(64)]
+    geom, p = seqs[0].geom, seqs[0].params
+    m = sf.StructureFlow(geom, p, batch=64, kernel=_kernel_id("fused"))
+    os_ = [oracle.Oracle(geom, p, "f32") for _ in seqs]
+    for k in range(frames):
+        m.step(_dev(np.stack([s.Y[k] for s in seqs])), _dev(np.stack([s.depth[k] for s in seqs])))
+        w, rho, yhat = _fields(m)
+        for b, (o, s) in enumerate(zip(os_, seqs)):
+            o.step(s.Y[k], s.depth[k])
+            assert_parity(w[b], o.w, f"w[{b}] frame {k}")
+            assert_parity(rho[b], o.rho, f"rho[{b}] frame {k}")
+            assert_parity(yhat[b], o.yhat, f"yhat[{b}] frame {k}")
+    st, flags = sf.sf_status_flags(m.ctx)
+    want = 0
+    for o in os_:
+        want |= o.flags
+    assert flags == want, (flags, want)
+
+
 @pytest.mark.parametrize("H,W,N,S,B", [(97, 131, 3, 2, 1), (150, 61, 8, 2, 2), (200, 170, 11, 1, 1),
                                        (64, 300, 5, 0, 1), (33, 33, 1, 3, 3), (72, 64, 8, 2, 1),
                                        (300, 257, 17, 2, 1), (5, 7, 2, 2, 2)])
