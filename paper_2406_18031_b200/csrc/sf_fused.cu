@@ -215,9 +215,13 @@ __device__ __forceinline__ float2 tap2_h(float2 x0, float2 x1, float2 x2, float2
     a = fma2(bc2(SF_H3), x3, a);
     return fma2(bc2(SF_H4), x4, a);
 }
-__device__ __forceinline__ float2 rcp2(float2 a) { return make_float2(__frcp_rn(a.x), __frcp_rn(a.y)); }
-__device__ __forceinline__ void ls_solve3x2(const float2 g[3], const float2 m[3], float2 cY, float2 cr,
-                                            const float2 wp[3], float g1, float2 g2, float g3, float2 x[3]) {
+template <bool FAST>
+__device__ __forceinline__ float2 rcp2(float2 a, bool& ok) {
+    return make_float2(rcp_rn<FAST>(a.x, ok), rcp_rn<FAST>(a.y, ok));
+}
+template <bool FAST>
+__device__ __forceinline__ void ls_solve3x2_t(const float2 g[3], const float2 m[3], float2 cY, float2 cr,
+                                              const float2 wp[3], float g1, float2 g2, float g3, float2 x[3], bool& ok) {
     float2 g1g[3], g2m[3];
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
@@ -234,19 +238,26 @@ __device__ __forceinline__ void ls_solve3x2(const float2 g[3], const float2 m[3]
     float2 b[3];
 #pragma unroll
     for (int a = 0; a < 3; ++a) b[a] = fma2(neg2(g2m[a]), cr, fma2(neg2(g1g[a]), cY, mul2(G3, wp[a])));
-    const float2 r0 = rcp2(A00);
+    const float2 r0 = rcp2<FAST>(A00, ok);
     const float2 l10 = mul2(A10, r0), l20 = mul2(A20, r0);
     const float2 d1 = fma2(neg2(l10), A10, A11);
-    const float2 r1 = rcp2(d1);
+    const float2 r1 = rcp2<FAST>(d1, ok);
     const float2 t = fma2(neg2(l20), A10, A21);
     const float2 l21 = mul2(t, r1);
     const float2 dd2 = fma2(neg2(l21), t, fma2(neg2(l20), A20, A22));
-    const float2 r2 = rcp2(dd2);
+    const float2 r2 = rcp2<FAST>(dd2, ok);
     const float2 y1 = fma2(neg2(l10), b[0], b[1]);
     const float2 y2 = fma2(neg2(l21), y1, fma2(neg2(l20), b[0], b[2]));
     x[2] = mul2(y2, r2);
     x[1] = fma2(neg2(l21), x[2], mul2(y1, r1));
     x[0] = fma2(neg2(l20), x[2], fma2(neg2(l10), x[1], mul2(b[0], r0)));
+}
+// fast reciprocals; the whole solve is redone with __frcp_rn if an input left the exact range
+__device__ __forceinline__ void ls_solve3x2(const float2 g[3], const float2 m[3], float2 cY, float2 cr,
+                                            const float2 wp[3], float g1, float2 g2, float g3, float2 x[3]) {
+    bool ok = true;
+    ls_solve3x2_t<true>(g, m, cY, cr, wp, g1, g2, g3, x, ok);
+    if (!ok) ls_solve3x2_t<false>(g, m, cY, cr, wp, g1, g2, g3, x, ok);
 }
 
 // The transport: M substeps of a column pass then a row pass on the thread's
