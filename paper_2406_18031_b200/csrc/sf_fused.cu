@@ -268,7 +268,9 @@ __device__ __forceinline__ void ls_solve3x2(const float2 g[3], const float2 m[3]
 // returns its own value and the pass bodies carry no boundary logic.  A grid edge on the
 // region border itself needs no replica: it lies R cells from the tile, outside the tile's
 // dependency cone, like any cut edge.
-template <int K, int NWY, int RULE, bool CLAMP, int NF = 4>
+// EDGE = false (interior CTAs, no grid edge in the region) and IMU = false compile the edge
+// replicas and the inertial stage out, so the substep loop is straight-line code between barriers.
+template <int K, int NWY, int RULE, bool CLAMP, int NF = 4, bool EDGE = true, bool IMU = true>
 __device__ __forceinline__ void transport_passes(const FrameParams& f, int M, float2 (&W)[NF][K], const float2 (&SX)[K],
                                                  const float2 (&SY)[K], const float2 (&SZ)[K], float (&mx)[K],
                                                  const float* Es, float2* XB0, int lane, int wy, int cmin, int cmax,
@@ -297,11 +299,12 @@ __device__ __forceinline__ void transport_passes(const FrameParams& f, int M, fl
     const float2 T2 = make_float2(-f.dt, -f.dt), SG = make_float2(f.sigma, f.sigma);
     const int srcL = lane - 1, srcR = lane + 1;
     // replica bookkeeping (block-uniform except for the lane / k tests)
-    const bool repL = cmin > 0, repR = cmax < RW - 1, repT = rmin > 0, repB = rmax < RH - 1;
+    const bool repL = EDGE && cmin > 0, repR = EDGE && cmax < RW - 1, repT = EDGE && rmin > 0,
+               repB = EDGE && rmax < RH - 1;
     const int laneL = cmin / 2 - 1;                            // owns replica column cmin-1 as its cell 1
     const int laneR = (cmax & 1) ? (cmax + 1) / 2 : cmax / 2;  // owns replica column cmax+1
     const bool rOdd = (cmax & 1) != 0;                         // replica is cell 0 of laneR (else its cell 1)
-    const bool in1 = c0 + 1 <= cmax;                           // cell 1 inside the grid (for the flag max)
+    const bool in1 = !EDGE || c0 + 1 <= cmax;                  // cell 1 inside the grid (for the flag max)
     const int keT = rmin - r0, keB = rmax - r0;                // edge rows in this thread's run
 
     // dominant flow of both cells -> flag max, clamp, (|u_hat0|, |u_hat1|)
@@ -443,28 +446,38 @@ __device__ __forceinline__ void transport_passes(const FrameParams& f, int M, fl
                 t[c] = W[c][0];
                 bb[c] = W[c][K - 1];
             }
-            // neighbour run ends; at an edge row on a run boundary the replica is the row itself
-            if (wy > 0 && !(repT && keT == 0)) {
+            // neighbour run ends; at an edge row on a run boundary the replica is the row itself.
+            // Select form: the neighbour warp's entry (clamped warp index) and the e planes one row
+            // outside the run (in bounds of shared memory for the first / last warp) are always read.
+            {
+                const bool useT = wy > 0 && !(repT && keT == 0), useB = wy < NWY - 1 && !(repB && keB == K - 1);
+                const int wt = wy > 0 ? wy - 1 : 0, wb = wy < NWY - 1 ? wy + 1 : NWY - 1;
+                float2 tn[NF], bn[NF];
 #pragma unroll
-                for (int c = 0; c < NF; ++c) t[c] = XB[((c * NWY + wy - 1) * 2 + 1) * 32 + lane];
-                const int ib = (r0 - 1) * RW + c0;
-                vt = dot2(*reinterpret_cast<const float2*>(Es + 3 * P + ib),
-                          *reinterpret_cast<const float2*>(Es + 4 * P + ib),
-                          *reinterpret_cast<const float2*>(Es + 5 * P + ib), t[0], t[1], t[2]);
-            }
-            if (wy < NWY - 1 && !(repB && keB == K - 1)) {
+                for (int c = 0; c < NF; ++c) {
+                    tn[c] = XB[((c * NWY + wt) * 2 + 1) * 32 + lane];
+                    bn[c] = XB[((c * NWY + wb) * 2 + 0) * 32 + lane];
+                }
+                const int it = (r0 - 1) * RW + c0, ibb = (r0 + K) * RW + c0;
+                const float2 vtn = dot2(*reinterpret_cast<const float2*>(Es + 3 * P + it),
+                                        *reinterpret_cast<const float2*>(Es + 4 * P + it),
+                                        *reinterpret_cast<const float2*>(Es + 5 * P + it), tn[0], tn[1], tn[2]);
+                const float2 vbn = dot2(*reinterpret_cast<const float2*>(Es + 3 * P + ibb),
+                                        *reinterpret_cast<const float2*>(Es + 4 * P + ibb),
+                                        *reinterpret_cast<const float2*>(Es + 5 * P + ibb), bn[0], bn[1], bn[2]);
 #pragma unroll
-                for (int c = 0; c < NF; ++c) bb[c] = XB[((c * NWY + wy + 1) * 2 + 0) * 32 + lane];
-                const int ib = (r0 + K) * RW + c0;
-                vb = dot2(*reinterpret_cast<const float2*>(Es + 3 * P + ib),
-                          *reinterpret_cast<const float2*>(Es + 4 * P + ib),
-                          *reinterpret_cast<const float2*>(Es + 5 * P + ib), bb[0], bb[1], bb[2]);
+                for (int c = 0; c < NF; ++c) {
+                    t[c] = sel2(useT, useT, tn[c], t[c]);
+                    bb[c] = sel2(useB, useB, bn[c], bb[c]);
+                }
+                vt = sel2(useT, useT, vtn, vt);
+                vb = sel2(useB, useB, vbn, vb);
             }
             row_update(0, vt, v[1], t, o1);
             row_update(K - 1, v[K - 2], vb, oK, bb);
             if (NXB == 1) __syncthreads();  // the single exchange buffer is rewritten next substep
         }
-        if (NF == 4 && f.imu) {  // inertial stage after the row pass (reading 32), per cell
+        if (NF == 4 && IMU && f.imu) {  // inertial stage after the row pass (reading 32), per cell
 #pragma unroll
             for (int k = 0; k < K; ++k) {
                 imu_stage(f, SX[k].x, SY[k].x, SZ[k].x, W[0][k].x, W[1][k].x, W[2][k].x, W[3][k].x);
@@ -639,8 +652,14 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
     }
 
     if (!(dbg & 1))
-    transport_passes<K, NWY, RULE, CLAMP>(f, a.M, W, SX, SY, SZ, mx, Es, XB0, lane, wy, cmin,
-                                          cmax, rmin, rmax, dbg);
+    {
+        if (edgeC || edgeR || f.imu)
+            transport_passes<K, NWY, RULE, CLAMP, 4, true, true>(f, a.M, W, SX, SY, SZ, mx, Es, XB0, lane, wy, cmin,
+                                                                 cmax, rmin, rmax, dbg);
+        else
+            transport_passes<K, NWY, RULE, CLAMP, 4, false, false>(f, a.M, W, SX, SY, SZ, mx, Es, XB0, lane, wy,
+                                                                   cmin, cmax, rmin, rmax, dbg);
+    }
     const float U = f.U;
 
     // ---------------- flags from tile cells (exact at every pass); |u_hat| before the clamp
