@@ -694,17 +694,35 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
         }
     } else {
         // =========================== update (U1-U5) on shared planes, compact runtime loops
-        // planes: E (e1, e2) stay until the solve; HG, HH, Fy, Fz take the row-buffer region; Fx takes
-        // Y's plane once the brightness taps are done; rhohat replaces depth and lives to the end
+        // planes: E (e1, e2) stay until the solve; HG, HH, Fy and rhohat take the row-buffer region
+        // (rhohat lives to the end); Fx and Fz take Y's and depth's planes once the models are done
         float* const HG = Xb;
         float* const HH = Xb + P;
         float* const Fx = Ys;  // w^{k+} -> w_LS -> smoothed w (in place)
         float* const Fy = Xb + 2 * P;
-        float* const Fz = Xb + 3 * P;
+        float* const Fz = Ds;
+        float* const RHs = Xb + 3 * P;  // rhohat (NaN = invalid)
         const int S = f.S;
         // solve region = tile + 2S (clipped to the grid); models needed on it +-2 rows, +-1 cols
         const int rlo = max(R - 2 * S, rmin), rhi = min(R + TH + 2 * S - 1, rmax);
         const int clo = max(R - 2 * S, cmin), chi = min(R + TW + 2 * S - 1, cmax);
+        // the solve's work distribution (pairs of the solve region over the threads) and its first
+        // pair's global inputs (s, ds^2, Yhat^k, rho^k), fetched here so that their latency hides
+        // behind the models; later pairs are fetched one pair ahead inside the solve loop
+        const int ncol = ((dbg & 1024) ? clo - 1 : chi) - clo + 1;
+        const int nc = (ncol + 1) >> 1, dr = nc > 0 ? NT / nc : 0, dc = nc > 0 ? NT % nc : 0;
+        int rn = nc > 0 ? rlo + tid / nc : rhi + 1, pn = nc > 0 ? tid % nc : 0;
+        auto fetch = [&](int r, int pc, float4& sa, float4& sb, float2& y, float2& sk) {
+            const int c = clo + 2 * pc, c1 = min(c + 1, chi);
+            const size_t ga = (size_t)(gi0 + r) * f.W + (gj0 + c), gb = (size_t)(gi0 + r) * f.W + (gj0 + c1);
+            sa = __ldg(a.G0 + ga);
+            sb = __ldg(a.G0 + gb);
+            y = make_float2(__ldg(a.yin + plane + ga), __ldg(a.yin + plane + gb));
+            sk = make_float2(__ldg(&a.sk[plane + ga].w), __ldg(&a.sk[plane + gb].w));
+        };
+        float4 san, sbn;
+        float2 yn, skn;
+        if (rn <= rhi) fetch(rn, pn, san, sbn, yn, skn);
         if (a.tma && !(dbg & 8)) {
             mbar_wait(&bars[2], 0);
             if (edgeC || edgeR) {  // out-of-grid cells of Y / depth read below take their clamped cell's value
@@ -717,13 +735,18 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
         __syncthreads();  // Y / depth complete; row buffers dead
         const float qnan = __int_as_float(0x7fffffff);
         SF_TICK();
+        bool okall = true;  // every reciprocal below took rcp_fast's exact range
         {
             // rhohat plane + horizontal brightness taps on the solve region +-2 rows, +-1 cols
 #pragma unroll 2
             SF_FOR_RECT(r, c, rlo - 2, rhi + 2, clo - 1, chi + 1, NT, tid) {
                 const int idx = r * RW + c;
                 const float d = Ds[idx];
-                Ds[idx] = depth_valid(d, f.is_inv) ? rho_hat(d, f.is_inv) : qnan;
+                bool ok = true;
+                const float rh = f.is_inv ? d : rcp_fast(d, ok);
+                const bool valid = depth_valid(d, f.is_inv);
+                RHs[idx] = valid ? rh : qnan;
+                okall = okall && (ok || !valid);
                 const float x0 = Ys[idx - 2], x1 = Ys[idx - 1], x2 = Ys[idx], x3 = Ys[idx + 1], x4 = Ys[idx + 2];
                 HG[idx] = tap_g(x0, x1, x2, x3, x4);
                 HH[idx] = tap_h(x0, x1, x2, x3, x4);
@@ -732,7 +755,15 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
                     fl |= SF_FLAG_NONFINITE;
             }
         }
-        __syncthreads();  // Y plane dead: w^{k+} goes to the F planes
+        if (__syncthreads_or(!okall)) {  // (never for depths in [2^-126, 2^126)): exact reciprocals
+#pragma unroll 1
+            SF_FOR_RECT(r, c, rlo - 2, rhi + 2, clo - 1, chi + 1, NT, tid) {
+                const int idx = r * RW + c;
+                const float d = Ds[idx];
+                RHs[idx] = depth_valid(d, f.is_inv) ? rho_hat(d, f.is_inv) : qnan;
+            }
+        }
+        __syncthreads();  // Y and depth planes dead: w^{k+} goes to the F planes
 #pragma unroll
         for (int k = 0; k < K; ++k) {
             const int ib = (r0 + k) * RW + c0;
@@ -746,20 +777,6 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
         // arithmetic cell-paired as f32x2; a ragged last pair computes its first cell twice and
         // stores it once).  The pair's global inputs (s, ds^2, Y, rho^k) are fetched one pair ahead.
         {
-            const int ncol = ((dbg & 1024) ? clo - 1 : chi) - clo + 1;
-            const int nc = (ncol + 1) >> 1, dr = nc > 0 ? NT / nc : 0, dc = nc > 0 ? NT % nc : 0;
-            int rn = nc > 0 ? rlo + tid / nc : rhi + 1, pn = nc > 0 ? tid % nc : 0;
-            auto fetch = [&](int r, int pc, float4& sa, float4& sb, float2& y, float2& sk) {
-                const int c = clo + 2 * pc, c1 = min(c + 1, chi);
-                const size_t ga = (size_t)(gi0 + r) * f.W + (gj0 + c), gb = (size_t)(gi0 + r) * f.W + (gj0 + c1);
-                sa = __ldg(a.G0 + ga);
-                sb = __ldg(a.G0 + gb);
-                y = make_float2(__ldg(a.yin + plane + ga), __ldg(a.yin + plane + gb));
-                sk = make_float2(__ldg(&a.sk[plane + ga].w), __ldg(&a.sk[plane + gb].w));
-            };
-            float4 san, sbn;
-            float2 yn, skn;
-            if (rn <= rhi) fetch(rn, pn, san, sbn, yn, skn);
 #pragma unroll 1
             while (rn <= rhi) {
                 const int r = rn, c = clo + 2 * pn;
@@ -778,8 +795,8 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
                 const float2 yh = tap2_g(g0, g1, g2, g3, g4);  // Yhat^{k+1}
                 const float2 be1 = tap2_g(h0, h1, h2, h3, h4);
                 const float2 be2 = tap2_h(g0, g1, g2, g3, g4);
-                const float2 rc = ld2(Ds, idx), ru = ld2(Ds, idx - RW), rd = ld2(Ds, idx + RW);
-                const float rl = Ds[idx - 1], rr = Ds[idx + 2];
+                const float2 rc = ld2(RHs, idx), ru = ld2(RHs, idx - RW), rd = ld2(RHs, idx + RW);
+                const float rl = RHs[idx - 1], rr = RHs[idx + 2];
                 const bool vc0 = !isnan(rc.x), vc1 = !isnan(rc.y);
                 const float2 rh = make_float2(vc0 ? rc.x : 0.0f, vc1 ? rc.y : 0.0f);
                 // eq:dominant_b1 / b2 per cell (the pair's cells are each other's row neighbour)
@@ -927,7 +944,7 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
                 const float2 wx = *reinterpret_cast<const float2*>(Wx + idx);
                 const float2 wy2 = *reinterpret_cast<const float2*>(Wy + idx);
                 const float2 wz = *reinterpret_cast<const float2*>(Wz + idx);
-                const float2 rh2 = *reinterpret_cast<const float2*>(Ds + idx);
+                const float2 rh2 = *reinterpret_cast<const float2*>(RHs + idx);
                 const bool v0 = !isnan(rh2.x), v1 = !isnan(rh2.y);
                 const float rn0 = xfma(v0 ? kap : 0.0f, xsub(v0 ? rh2.x : 0.0f, W[3][k].x), W[3][k].x);
                 const float rn1 = xfma(v1 ? kap : 0.0f, xsub(v1 ? rh2.y : 0.0f, W[3][k].y), W[3][k].y);
