@@ -37,6 +37,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     """SF_BUILD_DEBUG=1 compiles the timing / phase-skip knobs of the fused kernel (SF_DEBUG_SKIP);
     the default build folds them away."""
     extra = ["-DSF_DEBUG_KNOBS"] if os.environ.get("SF_BUILD_DEBUG") == "1" else []
+    extra += os.environ.get("SF_NVCC_EXTRA", "").split()  # experiments only (e.g. -DSF_EXP_...)
     cmd = [NVCC, *FLAGS, *extra, *[os.path.join(CSRC, s) for s in SOURCES], "-o", LIB]
     same = os.path.exists(STAMP) and open(STAMP).read() == " ".join(cmd)
     if (not force and same and os.path.exists(LIB) and
