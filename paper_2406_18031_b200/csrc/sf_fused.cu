@@ -151,7 +151,8 @@ struct FusedArgs {
     int dbg_skip;       // timing experiments only (SF_DEBUG_SKIP): 1 = skip transport, 2 = skip update,
                         // 4 = no e TMA, 8 = no Y/depth TMA, 16 = no field / s loads, 32 = exit at entry,
                         // 64 = no column passes, 128 = no row passes, 256 = print phase clocks of CTA (6,5),
-                        // 512 = no box passes, 1024 = no solve, 2048 = print per-CTA globaltimer stamps
+                        // 512 = no box passes, 1024 = no solve, 2048 = print per-CTA globaltimer stamps,
+                        // 4096 = every CTA takes the edge instantiation of the transport
     const float4* fin;  // fields at launch start (state k or a partial prediction)
     const float4* sk;   // state k (rho^k for the update)
     float4* fout;       // state k+1 (upd) or partial prediction
@@ -304,7 +305,11 @@ __device__ __forceinline__ void transport_passes(const FrameParams& f, int M, fl
     const int laneL = cmin / 2 - 1;                            // owns replica column cmin-1 as its cell 1
     const int laneR = (cmax & 1) ? (cmax + 1) / 2 : cmax / 2;  // owns replica column cmax+1
     const bool rOdd = (cmax & 1) != 0;                         // replica is cell 0 of laneR (else its cell 1)
+#ifdef SF_EXP_NO_IN1
+    const bool in1 = true;
+#else
     const bool in1 = !EDGE || c0 + 1 <= cmax;                  // cell 1 inside the grid (for the flag max)
+#endif
     const int keT = rmin - r0, keB = rmax - r0;                // edge rows in this thread's run
 
     // dominant flow of both cells -> flag max, clamp, (|u_hat0|, |u_hat1|)
@@ -344,6 +349,7 @@ __device__ __forceinline__ void transport_passes(const FrameParams& f, int M, fl
             }
         }
         // column replicas <- their edge cells
+#ifndef SF_EXP_NO_COLREP  // (SF_EXP_*: timing experiments, tools/gpu_gtexp.sh; wrong results)
         if (repL) {
             const bool me = lane == laneL;
 #pragma unroll
@@ -371,7 +377,9 @@ __device__ __forceinline__ void transport_passes(const FrameParams& f, int M, fl
                     for (int c = 0; c < NF; ++c) W[c][k].y = me ? W[c][k].x : W[c][k].y;
             }
         }
+#endif
         // row replicas inside this thread's run <- their edge rows (before the row pass reads)
+#ifndef SF_EXP_NO_ROWREP
         if (repT && keT >= 1 && keT <= K - 1) {
 #pragma unroll
             for (int k = 0; k < K - 1; ++k) {
@@ -388,6 +396,7 @@ __device__ __forceinline__ void transport_passes(const FrameParams& f, int M, fl
                 for (int c = 0; c < NF; ++c) W[c][k] = sel2(p, p, W[c][k - 1], W[c][k]);
             }
         }
+#endif
         // ================= row pass (beta_2, reading 3)
         if (!(dbg & 128)) {
             // run-end rows to the exchange buffer: [comp][warp][end][lane] float2
@@ -526,7 +535,8 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
                       (blockIdx.x == 0 && blockIdx.y == 5) || (blockIdx.x == gridDim.x - 1 && blockIdx.y == gridDim.y - 1));
 #define SF_TICK() do { if (tim) { __syncthreads(); if (tid == 0) T_[nT_] = clock64(); ++nT_; } } while (0)
     SF_TICK();
-    unsigned long long gt0_ = 0, gt1_ = 0, gte_ = 0;  // dbg 2048: globaltimer at entry / griddep release / e planes in / exit
+    unsigned long long gt0_ = 0, gt1_ = 0, gte_ = 0, gtt_ = 0;  // dbg 2048: globaltimer at entry / griddep release /
+    // e planes in (after the replica fix-up) / transport done / exit
     if (dbg & 2048) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt0_));
     // ---------------- staging: e1 / e2 planes (transport), Y and depth (update)
     uint64_t* const bars = reinterpret_cast<uint64_t*>(sm + 8 * P + C::XRF);
@@ -629,7 +639,6 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
     if (a.tma && !(dbg & 4)) {
         mbar_wait(&bars[0], 0);
         mbar_wait(&bars[1], 0);
-        if (dbg & 2048) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gte_));
         if (edgeC || edgeR) {  // replica cells next to grid edges take the edge cell's e (reading 10)
             __syncthreads();
             if (cmin > 0 || cmax < RW - 1)
@@ -647,19 +656,21 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
                 }
             __syncthreads();
         }
+        if (dbg & 2048) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gte_));
     } else {
         cp_async_wait<1>();  // own e cells landed (each thread reads only what it copied until the 1st barrier)
     }
 
     if (!(dbg & 1))
     {
-        if (edgeC || edgeR || f.imu)
+        if (edgeC || edgeR || f.imu || (dbg & 4096))
             transport_passes<K, NWY, RULE, CLAMP, 4, true, true>(f, a.M, W, SX, SY, SZ, mx, Es, XB0, lane, wy, cmin,
                                                                  cmax, rmin, rmax, dbg);
         else
             transport_passes<K, NWY, RULE, CLAMP, 4, false, false>(f, a.M, W, SX, SY, SZ, mx, Es, XB0, lane, wy,
                                                                    cmin, cmax, rmin, rmax, dbg);
     }
+    if (dbg & 2048) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gtt_));
     const float U = f.U;
 
     // ---------------- flags from tile cells (exact at every pass); |u_hat| before the clamp
@@ -967,7 +978,7 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
     if ((dbg & 2048) && tid == 0) {
         unsigned long long t2_;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t2_));
-        printf("SFGT %d %d %llu %llu %llu %llu\n", blockIdx.x, blockIdx.y, gt0_, gt1_, t2_, gte_);
+        printf("SFGT %d %d %llu %llu %llu %llu %llu\n", blockIdx.x, blockIdx.y, gt0_, gt1_, t2_, gte_, gtt_);
     }
     const unsigned any = __reduce_or_sync(FULL, fl);
     if (lane == 0 && any) atomicOr(a.flags, any);
