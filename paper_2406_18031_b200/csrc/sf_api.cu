@@ -178,7 +178,7 @@ extern "C" sf_status sf_create(const sf_config* cfg, const float* geometry, sf_c
     bool ok = cudaMalloc(&c->G0, npix * sizeof(float4)) == cudaSuccess &&
               cudaMalloc(&c->G1, npix * sizeof(float4)) == cudaSuccess &&
               cudaMalloc(&c->G2, npix * sizeof(float4)) == cudaSuccess &&
-              cudaMalloc(&c->E, 6 * npix * sizeof(float)) == cudaSuccess &&
+              cudaMalloc(&c->E, 6 * (size_t)sf_ew(f.W) * sf_eh(f.H) * sizeof(float)) == cudaSuccess &&
               cudaMalloc(&c->state[0], nall * sizeof(float4)) == cudaSuccess &&
               cudaMalloc(&c->state[1], nall * sizeof(float4)) == cudaSuccess &&
               cudaMalloc(&c->pred, nall * sizeof(float4)) == cudaSuccess &&

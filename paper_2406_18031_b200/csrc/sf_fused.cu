@@ -536,13 +536,13 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
 #define SF_TICK() do { if (tim) { __syncthreads(); if (tid == 0) T_[nT_] = clock64(); ++nT_; } } while (0)
     SF_TICK();
     unsigned long long gt0_ = 0, gt1_ = 0, gte_ = 0, gtt_ = 0;  // dbg 2048: globaltimer at entry / griddep release /
-    // e planes in (after the replica fix-up) / transport done / exit
+    // e planes in / transport done / exit
     if (dbg & 2048) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt0_));
     // ---------------- staging: e1 / e2 planes (transport), Y and depth (update)
     uint64_t* const bars = reinterpret_cast<uint64_t*>(sm + 8 * P + C::XRF);
     if (a.tma) {
         // TMA: one thread issues three bulk tensor copies of the whole region (out-of-range cells
-        // arrive as zeros; the replica cells next to grid edges are fixed up below)
+        // arrive as zeros; the replica e cells next to grid edges come from E's padding)
         if (tid == 0) {
             mbar_init(&bars[0], 1);
             mbar_init(&bars[1], 1);
@@ -552,25 +552,27 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
         __syncthreads();
         if (tid == 0 && !(dbg & 4)) {  // geometry: independent of the previous frame
             mbar_expect_tx(&bars[0], 3u * P * 4u);
-            tma_load_3d(Es, &a.tmE, gj0, gi0, 0, &bars[0]);
+            tma_load_3d(Es, &a.tmE, gj0 + SF_EPAD, gi0 + SF_EPAD, 0, &bars[0]);
             mbar_expect_tx(&bars[1], 3u * P * 4u);
-            tma_load_3d(Es + 3 * P, &a.tmE, gj0, gi0, 3, &bars[1]);
+            tma_load_3d(Es + 3 * P, &a.tmE, gj0 + SF_EPAD, gi0 + SF_EPAD, 3, &bars[1]);
         }
     } else {
         const bool pair = !edgeC && (f.W & 1) == 0;  // both cells contiguous and 8-byte aligned
+        const int EW = sf_ew(f.W);
+        const size_t EP = (size_t)EW * sf_eh(f.H);  // padded e planes: clamped cell (i, j) at (i + EPAD, j + EPAD)
 #pragma unroll
         for (int k = 0; k < K; ++k) {
             const int r = r0 + k;
-            const size_t gr = (size_t)iclamp(gi0 + r, 0, f.H - 1) * f.W;
+            const size_t gr = (size_t)(iclamp(gi0 + r, 0, f.H - 1) + SF_EPAD) * EW + SF_EPAD;
             const size_t ga = gr + iclamp(gj0 + c0, 0, f.W - 1), gb = gr + iclamp(gj0 + c0 + 1, 0, f.W - 1);
 #pragma unroll
             for (int p = 0; p < 6; ++p) {
                 float* dst = Es + p * P + r * RW + c0;
                 if (pair) {
-                    cp_async8(dst, a.E + p * HW + ga);
+                    cp_async8(dst, a.E + p * EP + ga);
                 } else {
-                    cp_async4(dst, a.E + p * HW + ga);
-                    cp_async4(dst + 1, a.E + p * HW + gb);
+                    cp_async4(dst, a.E + p * EP + ga);
+                    cp_async4(dst + 1, a.E + p * EP + gb);
                 }
             }
         }
@@ -639,23 +641,7 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
     if (a.tma && !(dbg & 4)) {
         mbar_wait(&bars[0], 0);
         mbar_wait(&bars[1], 0);
-        if (edgeC || edgeR) {  // replica cells next to grid edges take the edge cell's e (reading 10)
-            __syncthreads();
-            if (cmin > 0 || cmax < RW - 1)
-                for (int t = tid; t < 6 * RH; t += NT) {
-                    float* row = Es + (t / RH) * P + (t % RH) * RW;
-                    if (cmin > 0) row[cmin - 1] = row[cmin];
-                    if (cmax < RW - 1) row[cmax + 1] = row[cmax];
-                }
-            __syncthreads();
-            if (rmin > 0 || rmax < RH - 1)
-                for (int t = tid; t < 6 * RW; t += NT) {
-                    float* col = Es + (t / RW) * P + (t % RW);
-                    if (rmin > 0) col[(rmin - 1) * RW] = col[rmin * RW];
-                    if (rmax < RH - 1) col[(rmax + 1) * RW] = col[rmax * RW];
-                }
-            __syncthreads();
-        }
+        // (replica e cells next to grid edges arrive with the load: padded E, reading 10)
         if (dbg & 2048) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gte_));
     } else {
         cp_async_wait<1>();  // own e cells landed (each thread reads only what it copied until the 1st barrier)
@@ -1037,21 +1023,23 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_low(const __grid_constant__ Low
         __syncthreads();
         if (tid == 0) {
             mbar_expect_tx(&bars[0], 3u * P * 4u);
-            tma_load_3d(Es, &a.tmE, gj0, gi0, 0, &bars[0]);
+            tma_load_3d(Es, &a.tmE, gj0 + SF_EPAD, gi0 + SF_EPAD, 0, &bars[0]);
             mbar_expect_tx(&bars[1], 3u * P * 4u);
-            tma_load_3d(Es + 3 * P, &a.tmE, gj0, gi0, 3, &bars[1]);
+            tma_load_3d(Es + 3 * P, &a.tmE, gj0 + SF_EPAD, gi0 + SF_EPAD, 3, &bars[1]);
         }
     } else {
+        const int EW = sf_ew(f.W);
+        const size_t EP = (size_t)EW * sf_eh(f.H);  // padded e planes: clamped cell (i, j) at (i + EPAD, j + EPAD)
 #pragma unroll
         for (int k = 0; k < K; ++k) {
             const int r = r0 + k;
-            const size_t gr = (size_t)iclamp(gi0 + r, 0, f.H - 1) * f.W;
+            const size_t gr = (size_t)(iclamp(gi0 + r, 0, f.H - 1) + SF_EPAD) * EW + SF_EPAD;
             const size_t ga = gr + iclamp(gj0 + c0, 0, f.W - 1), gb = gr + iclamp(gj0 + c0 + 1, 0, f.W - 1);
 #pragma unroll
             for (int p = 0; p < 6; ++p) {
                 float* dst = Es + p * P + r * RW + c0;
-                cp_async4(dst, a.E + p * HW + ga);
-                cp_async4(dst + 1, a.E + p * HW + gb);
+                cp_async4(dst, a.E + p * EP + ga);
+                cp_async4(dst + 1, a.E + p * EP + gb);
             }
         }
         cp_async_commit();
@@ -1093,22 +1081,7 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_low(const __grid_constant__ Low
     } else {
         cp_async_wait<0>();
     }
-    if (cmin > 0 || cmax < RW - 1 || rmin > 0 || rmax < RH - 1) {  // replica e cells (reading 10)
-        __syncthreads();
-        if (cmin > 0 || cmax < RW - 1)
-            for (int t = tid; t < 6 * RH; t += C::NT) {
-                float* row = Es + (t / RH) * P + (t % RH) * RW;
-                if (cmin > 0) row[cmin - 1] = row[cmin];
-                if (cmax < RW - 1) row[cmax + 1] = row[cmax];
-            }
-        __syncthreads();
-        if (rmin > 0 || rmax < RH - 1)
-            for (int t = tid; t < 6 * RW; t += C::NT) {
-                float* col = Es + (t / RW) * P + (t % RW);
-                if (rmin > 0) col[(rmin - 1) * RW] = col[rmin * RW];
-                if (rmax < RH - 1) col[(rmax + 1) * RW] = col[rmax * RW];
-            }
-    }
+    // (replica e cells next to grid edges arrive with the load: padded E, reading 10)
     __syncthreads();
     transport_passes<K, NWY, RULE, CLAMP, 8>(f, a.M, W, SX, SY, SZ, mx, Es, XB0, lane, wy, cmin, cmax, rmin, rmax, 0,
                                              Ss);
@@ -1280,7 +1253,7 @@ cudaError_t launch_cfg(sf_ctx* c, const float* Y, const float* D) {
             }();
             a.dbg_skip = dbg_env;
         }
-        a.tma = !no_tma() && encode3d(&a.tmE, c->E, f.W, f.H, 6, FC::RW, FC::RH, 3) &&
+        a.tma = !no_tma() && encode3d(&a.tmE, c->E, sf_ew(f.W), sf_eh(f.H), 6, FC::RW, FC::RH, 3) &&
                 encode3d(&a.tmY, Y, f.W, f.H, f.B, FC::RW, FC::RH, 1) &&
                 encode3d(&a.tmD, D, f.W, f.H, f.B, FC::RW, FC::RH, 1);
         a.fin = src;
@@ -1351,7 +1324,7 @@ cudaError_t launch_low(sf_ctx* c) {
         a.R = (a.M + 3) & ~3;
         a.TW = LC::RW - 2 * a.R;
         a.TH = LC::RH - 2 * a.R;
-        a.tma = !no_tma() && encode3d(&a.tmE, c->E, f.W, f.H, 6, LC::RW, LC::RH, 3);
+        a.tma = !no_tma() && encode3d(&a.tmE, c->E, sf_ew(f.W), sf_eh(f.H), 6, LC::RW, LC::RH, 3);
         a.finA = srcA;
         a.finW = srcW;
         const bool last = ((L - 1 - l) & 1) == 0;

@@ -22,12 +22,23 @@ __global__ void k_geometry(const float* __restrict__ g10, float4* G0, float4* G1
     const float4 e2 = make_float4(__fdiv_rn(g[6], ds), __fdiv_rn(g[7], ds), __fdiv_rn(g[8], ds), 0.0f);
     G1[p] = e1;
     G2[p] = e2;
-    E[p] = e1.x;
-    E[(size_t)n + p] = e1.y;
-    E[2 * (size_t)n + p] = e1.z;
-    E[3 * (size_t)n + p] = e2.x;
-    E[4 * (size_t)n + p] = e2.y;
-    E[5 * (size_t)n + p] = e2.z;
+}
+
+// The padded e planes (sf_internal.cuh SF_EPAD): cell (i, j) of [H + 2 EPAD][W + 2 EPAD] holds e of
+// the clamped grid cell (i - EPAD, j - EPAD).
+__global__ void k_epad(const float4* __restrict__ G1, const float4* __restrict__ G2, float* E, int H, int W) {
+    const int EW = sf_ew(W), EH = sf_eh(H);
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= EW * EH) return;
+    const int i = iclamp(q / EW - SF_EPAD, 0, H - 1), j = iclamp(q % EW - SF_EPAD, 0, W - 1);
+    const size_t pe = (size_t)EW * EH, p = (size_t)i * W + j;
+    const float4 e1 = G1[p], e2 = G2[p];
+    E[q] = e1.x;
+    E[pe + q] = e1.y;
+    E[2 * pe + q] = e1.z;
+    E[3 * pe + q] = e2.x;
+    E[4 * pe + q] = e2.y;
+    E[5 * pe + q] = e2.z;
 }
 
 // ------------------------------------------------------------------ transport pass (P1-P4)
@@ -338,6 +349,8 @@ __global__ void k_pack(const float* __restrict__ w, const float* __restrict__ rh
 cudaError_t sf_launch_geometry(sf_ctx* c, const float* g10) {
     const int n = c->fp.H * c->fp.W;
     k_geometry<<<(n + 255) / 256, 256, 0, c->stream>>>(g10, c->G0, c->G1, c->G2, c->E, n);
+    const int ne = sf_ew(c->fp.W) * sf_eh(c->fp.H);
+    k_epad<<<(ne + 255) / 256, 256, 0, c->stream>>>(c->G1, c->G2, c->E, c->fp.H, c->fp.W);
     return cudaGetLastError();
 }
 
