@@ -133,14 +133,20 @@ __device__ __forceinline__ void edge_fill(float* p0, float* p1, float* p2, int r
         p1[to] = p1[from];
         if (NP > 2) p2[to] = p2[from];
     };
+    // one band: empty bands are skipped before any index arithmetic (block-uniform test)
+    auto band = [&](int r0, int r1, int c0, int c1) {
+        const int nc = c1 - c0 + 1, nr = r1 - r0 + 1;
+        if (nc <= 0 || nr <= 0) return;
 #pragma unroll 1
-    SF_FOR_RECT(r, c, ra, min(rb, rmin - 1), ca, cb, NT, tid) cp(r, c);
-#pragma unroll 1
-    SF_FOR_RECT(r, c, max(ra, rmax + 1), rb, ca, cb, NT, tid) cp(r, c);
-#pragma unroll 1
-    SF_FOR_RECT(r, c, max(ra, rmin), min(rb, rmax), ca, min(cb, cmin - 1), NT, tid) cp(r, c);
-#pragma unroll 1
-    SF_FOR_RECT(r, c, max(ra, rmin), min(rb, rmax), max(ca, cmax + 1), cb, NT, tid) cp(r, c);
+        for (int t = tid; t < nc * nr; t += NT) {
+            const int q = t / nc;
+            cp(r0 + q, c0 + t - q * nc);
+        }
+    };
+    band(ra, min(rb, rmin - 1), ca, cb);
+    band(max(ra, rmax + 1), rb, ca, cb);
+    band(max(ra, rmin), min(rb, rmax), ca, min(cb, cmin - 1));
+    band(max(ra, rmin), min(rb, rmax), max(ca, cmax + 1), cb);
 }
 
 struct FusedArgs {
@@ -311,6 +317,9 @@ __device__ __forceinline__ void transport_passes(const FrameParams& f, int M, fl
     const bool in1 = !EDGE || c0 + 1 <= cmax;                  // cell 1 inside the grid (for the flag max)
 #endif
     const int keT = rmin - r0, keB = rmax - r0;                // edge rows in this thread's run
+    // warp-uniform (a vote result) so the refresh branches below need no reconvergence regions
+    const bool doT = __all_sync(FULL, repT && keT >= 1 && keT <= K - 1);
+    const bool doB = __all_sync(FULL, repB && keB >= 0 && keB <= K - 2);
 
     // dominant flow of both cells -> flag max, clamp, (|u_hat0|, |u_hat1|)
     // (the clamp keeps the sign since U > 0, and |clamp(u, -U, U)| = min(|u|, U) -- also for a
@@ -380,7 +389,7 @@ __device__ __forceinline__ void transport_passes(const FrameParams& f, int M, fl
 #endif
         // row replicas inside this thread's run <- their edge rows (before the row pass reads)
 #ifndef SF_EXP_NO_ROWREP
-        if (repT && keT >= 1 && keT <= K - 1) {
+        if (doT) {
 #pragma unroll
             for (int k = 0; k < K - 1; ++k) {
                 const bool p = (keT - 1 - k) == 0;
@@ -388,7 +397,7 @@ __device__ __forceinline__ void transport_passes(const FrameParams& f, int M, fl
                 for (int c = 0; c < NF; ++c) W[c][k] = sel2(p, p, W[c][k + 1], W[c][k]);
             }
         }
-        if (repB && keB >= 0 && keB <= K - 2) {
+        if (doB) {
 #pragma unroll
             for (int k = K - 1; k >= 1; --k) {
                 const bool p = (keB + 1 - k) == 0;
