@@ -465,8 +465,8 @@ __device__ __forceinline__ void transport_passes(const FrameParams& f, int M, fl
                 bb[c] = W[c][K - 1];
             }
             // neighbour run ends; at an edge row on a run boundary the replica is the row itself.
-            // Select form: the neighbour warp's entry (clamped warp index) and the e planes one row
-            // outside the run (in bounds of shared memory for the first / last warp) are always read.
+            // Select form: the neighbour warp's entry and the e planes one row outside the run are
+            // always read (warp index and row clamped to the region).
             {
                 const bool useT = wy > 0 && !(repT && keT == 0), useB = wy < NWY - 1 && !(repB && keB == K - 1);
                 const int wt = wy > 0 ? wy - 1 : 0, wb = wy < NWY - 1 ? wy + 1 : NWY - 1;
@@ -476,7 +476,9 @@ __device__ __forceinline__ void transport_passes(const FrameParams& f, int M, fl
                     tn[c] = XB[((c * NWY + wt) * 2 + 1) * 32 + lane];
                     bn[c] = XB[((c * NWY + wb) * 2 + 0) * 32 + lane];
                 }
-                const int it = (r0 - 1) * RW + c0, ibb = (r0 + K) * RW + c0;
+                // (rows clamped to the region: the first / last warp's unused read stays off Y's plane,
+                //  which the Y / depth loads may still be writing)
+                const int it = (wy > 0 ? r0 - 1 : r0) * RW + c0, ibb = (wy < NWY - 1 ? r0 + K : r0 + K - 1) * RW + c0;
                 const float2 vtn = dot2(*reinterpret_cast<const float2*>(Es + 3 * P + it),
                                         *reinterpret_cast<const float2*>(Es + 4 * P + it),
                                         *reinterpret_cast<const float2*>(Es + 5 * P + it), tn[0], tn[1], tn[2]);
