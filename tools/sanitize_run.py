@@ -1,6 +1,6 @@
 #!/usr/bin/env python3
 """Small workloads for compute-sanitizer (tools/gpu_sanitize.sh): the fused and per-pass H = 1
-paths on a ragged multi-CTA grid (interior, edge and corner CTAs), the pyramid, the input
+paths on ragged multi-CTA grids (interior, edge and corner CTAs; cp.async and TMA staging), the pyramid, the input
 mapping and the evaluation -- each compared with the oracle so a run is also a parity check."""
 import os
 import sys
@@ -45,7 +45,8 @@ def pyramid(frames=3):
 if __name__ == "__main__":
     which = sys.argv[1:] or ["fused", "passes", "pyramid"]
     if "fused" in which:
-        h1(sf.SF_KERNEL_FUSED, 150, 130)
+        h1(sf.SF_KERNEL_FUSED, 150, 130)  # W % 4 != 0: cp.async staging
+        h1(sf.SF_KERNEL_FUSED, 150, 136)  # W % 4 == 0: TMA staging (racecheck does not see TMA writes)
     if "passes" in which:
         h1(sf.SF_KERNEL_PASSES, 150, 130)
     if "pyramid" in which:
