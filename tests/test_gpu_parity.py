@@ -104,9 +104,11 @@ def test_predict_only_ragged_random_state(kernel):
     assert sf.sf_status_flags(m.ctx)[1] == o.flags
 
 
-@pytest.mark.parametrize("variant", ["printed", "noclamp", "S0", "S3", "inverse_input", "invalid_depth", "N1", "tiny"])
+@pytest.mark.parametrize("variant", ["printed", "noclamp", "S0", "S3", "inverse_input", "invalid_depth", "N1", "tiny",
+                                     "far_depth", "huge_gamma3"])
 def test_variants(variant):
-    """Options and degenerate cases, 6 frames each, bitwise."""
+    """Options and degenerate cases, 6 frames each, bitwise.  far_depth / huge_gamma3 put reciprocal
+    inputs above 2^126, outside rcp_fast's exact range, so the kernels' exact fallback paths run."""
     seq = sfgen.config_sequence(1, frames=6)
     p = seq.params
     Y, D = seq.Y.copy(), seq.depth.copy()
@@ -128,6 +130,10 @@ def test_variants(variant):
         D[:, :, 60:] = np.inf
     elif variant == "N1":
         kw["max_flow"] = 0.75
+    elif variant == "far_depth":
+        D[:, 5:10, 5:12] = np.float32(1e38)  # valid depth, 1/lambda = 1e-38 (normal)
+    elif variant == "huge_gamma3":
+        kw["gamma"] = (p.gamma[0], p.gamma[1], 1e38, p.gamma[3], p.gamma[4])  # LDL^T pivots ~ 1e38
     elif variant == "tiny":
         g = grid.gnomonic(2, 3, 40.0)
         rng = np.random.default_rng(1)
