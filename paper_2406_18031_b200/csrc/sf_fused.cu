@@ -745,22 +745,30 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
         SF_TICK();
         bool okall = true;  // every reciprocal below took rcp_fast's exact range
         {
-            // rhohat plane + horizontal brightness taps on the solve region +-2 rows, +-1 cols
+            // rhohat plane + horizontal brightness taps on the solve region +-2 rows, +-1 cols, two
+            // horizontally adjacent cells per item (8-byte aligned pairs from an even column; the taps as
+            // f32x2, each lane the scalar tap order).  A pair may add one cell on either side of the
+            // range: its values are never read (inputs there are in the plane / filled bands).
+            const int ca = (clo - 1) & ~1, npc = (chi + 1 - ca) / 2 + 1;
+            auto ld2 = [&](const float* pl, int i) { return *reinterpret_cast<const float2*>(pl + i); };
 #pragma unroll 2
-            SF_FOR_RECT(r, c, rlo - 2, rhi + 2, clo - 1, chi + 1, NT, tid) {
-                const int idx = r * RW + c;
-                const float d = Ds[idx];
-                bool ok = true;
-                const float rh = f.is_inv ? d : rcp_fast(d, ok);
-                const bool valid = depth_valid(d, f.is_inv);
-                RHs[idx] = valid ? rh : qnan;
-                okall = okall && (ok || !valid);
-                const float x0 = Ys[idx - 2], x1 = Ys[idx - 1], x2 = Ys[idx], x3 = Ys[idx + 1], x4 = Ys[idx + 2];
-                HG[idx] = tap_g(x0, x1, x2, x3, x4);
-                HH[idx] = tap_h(x0, x1, x2, x3, x4);
-                if (r >= R && r < R + TH && c >= R && c < R + TW && r >= rmin && r <= rmax && c >= cmin &&
-                    c <= cmax && gi0 + r >= f.fr0 && gi0 + r < f.fr1 && !isfinite(x2))
-                    fl |= SF_FLAG_NONFINITE;
+            SF_FOR_RECT(r, pc, rlo - 2, rhi + 2, 0, npc - 1, NT, tid) {
+                const int c = ca + 2 * pc, idx = r * RW + c;
+                const float2 d = ld2(Ds, idx);
+                bool ok0 = true, ok1 = true;
+                const float rh0 = f.is_inv ? d.x : rcp_fast(d.x, ok0), rh1 = f.is_inv ? d.y : rcp_fast(d.y, ok1);
+                const bool v0 = depth_valid(d.x, f.is_inv), v1 = depth_valid(d.y, f.is_inv);
+                *reinterpret_cast<float2*>(RHs + idx) = make_float2(v0 ? rh0 : qnan, v1 ? rh1 : qnan);
+                okall = okall && (ok0 || !v0) && (ok1 || !v1);
+                const float2 ya = ld2(Ys, idx - 2), yb = ld2(Ys, idx), yc = ld2(Ys, idx + 2);
+                const float2 x0 = ya, x1 = make_float2(ya.y, yb.x), x2 = yb, x3 = make_float2(yb.y, yc.x), x4 = yc;
+                *reinterpret_cast<float2*>(HG + idx) = tap2_g(x0, x1, x2, x3, x4);
+                *reinterpret_cast<float2*>(HH + idx) = tap2_h(x0, x1, x2, x3, x4);
+                if (r >= R && r < R + TH && r >= rmin && r <= rmax && gi0 + r >= f.fr0 && gi0 + r < f.fr1) {
+                    if (c >= R && c < R + TW && c >= cmin && c <= cmax && !isfinite(yb.x)) fl |= SF_FLAG_NONFINITE;
+                    if (c + 1 >= R && c + 1 < R + TW && c + 1 >= cmin && c + 1 <= cmax && !isfinite(yb.y))
+                        fl |= SF_FLAG_NONFINITE;
+                }
             }
         }
         if (__syncthreads_or(!okall)) {  // (never for depths in [2^-126, 2^126)): exact reciprocals
