@@ -136,3 +136,23 @@ def test_pyramid_accuracy(pyr_run):
     """The two-level filter tracks the ground truth: after 40 frames the RMSE is
     below 25 % of the zero-flow error."""
     assert pyr_run["rmse"][-1] < 0.25 * pyr_run["zero"], (pyr_run["rmse"][-1], pyr_run["zero"])
+
+
+def test_pyramid_increment_update_depth_term():
+    """Bottom-level increment update [dU] (eq:cost_bottom; reading 28): a uniform
+    inverse-depth change on a static FLAT scene is explained by the normal component of the
+    increment alone -- m = ds^2 rhohat s (no rho gradient) and c_rho = ds^2 (rhohat - rho^{k+}), so
+    for a dominant gamma2 dw_z = rho^{k+}/rhohat - 1 (the E_rho closed form of L572-574 applied to
+    dw with prior dw^{k+} = 0).  The top level recovers the same rate, and w = up(w^2) + dw."""
+    H = W = 16
+    g1, g2 = grid.flat(H, W, 2.0 ** -6), grid.flat(H // 2, W // 2, 2.0 ** -5)
+    p = Params(max_flow=2.0, gamma=(0.0, 1e14, 1.0, 1.0, 0.0), smooth_iters=0)
+    po = oracle.PyramidOracle(g1, g2, p, precision="f64", smooth_top=0)
+    Y = np.zeros((H, W), np.float32)
+    po.step(Y, np.full((H, W), 2.0, np.float32))  # rho = 0.5 at both levels, w = 0
+    po.step(Y, np.full((H, W), 1.6, np.float32))
+    rate = 0.5 * float(np.float32(1.6)) - 1.0
+    assert np.allclose(po.dw[..., 2], rate, atol=1e-6) and np.abs(po.dw[..., :2]).max() < 1e-12
+    assert np.allclose(po.w2[..., 2], rate, atol=1e-6)
+    assert np.allclose(po.w[..., 2], 2 * rate, atol=2e-6)
+    assert np.allclose(po.rho, 1.0 / float(np.float32(1.6)), rtol=1e-14)  # gamma5 = 0: the measurement
