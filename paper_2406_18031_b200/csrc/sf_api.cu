@@ -52,6 +52,8 @@ static sf_status validate(const sf_config* c) {
     return SF_OK;
 }
 
+static void async_teardown(sf_ctx* c);
+
 static void free_ctx(sf_ctx* c) {
     if (!c) return;
     void* ptrs[] = {c->G0, c->G1, c->G2, c->E, c->state[0], c->state[1], c->pred, c->tmp, c->tmp2,
@@ -68,17 +70,7 @@ static void free_ctx(sf_ctx* c) {
     if (c->async_ready) {
         cudaStreamSynchronize(c->s_in);
         cudaStreamSynchronize(c->s_out);
-        for (int i = 0; i < 2; ++i) {
-            cudaFree(c->aY[i]);
-            cudaFree(c->aD[i]);
-            cudaFree(c->aw[i]);
-            cudaFree(c->ar[i]);
-            cudaEventDestroy(c->ev_in[i]);
-            cudaEventDestroy(c->ev_done[i]);
-            cudaEventDestroy(c->ev_out[i]);
-        }
-        cudaStreamDestroy(c->s_in);
-        cudaStreamDestroy(c->s_out);
+        async_teardown(c);
     }
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
     free(c);
@@ -123,15 +115,19 @@ static sf_status create_top(sf_ctx* c, const sf_config* cfg, const float* geomet
 }
 
 extern "C" sf_status sf_create(const sf_config* cfg, const float* geometry, sf_ctx** out) {
+    SF_NVTX("sf_create");
     if (!cfg || !out) return SF_E_DATA;
     *out = nullptr;
     sf_status st = validate(cfg);
     if (st != SF_OK) return st;
     if (!geometry) return SF_E_DATA;
-    if (cudaSetDevice(cfg->device) != cudaSuccess) return SF_E_CUDA;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || cfg->device < 0 || cfg->device >= ndev) return SF_E_CUDA;
+    SfDeviceGuard guard(cfg->device);  // the caller's current device is restored on return
     sf_ctx* c = (sf_ctx*)calloc(1, sizeof(sf_ctx));
     if (!c) return SF_E_CUDA;
     c->cfg = *cfg;
+    c->device = cfg->device;
     FrameParams& f = c->fp;
     f.H = cfg->height;
     f.W = cfg->width;
@@ -239,13 +235,17 @@ extern "C" sf_status sf_create(const sf_config* cfg, const float* geometry, sf_c
 }
 
 extern "C" void sf_destroy(sf_ctx* c) {
+    SF_NVTX("sf_destroy");
     if (!c) return;
+    SF_DEVICE_GUARD(c);
     cudaStreamSynchronize(c->stream);
     free_ctx(c);
 }
 
 extern "C" sf_status sf_predict(sf_ctx* c) {
+    SF_NVTX("sf_predict");
     if (!c) return SF_E_DATA;
+    SF_DEVICE_GUARD(c);
     if (c->levels == 2) return SF_E_UNSUPPORTED;
     if (!c->initialized || c->pending) return SF_E_STATE;
     SF_TRY(sf_launch_predict_passes(c));
@@ -254,7 +254,9 @@ extern "C" sf_status sf_predict(sf_ctx* c) {
 }
 
 extern "C" sf_status sf_update(sf_ctx* c, const float* Y, const float* D) {
+    SF_NVTX("sf_update");
     if (!c || !Y || !D) return SF_E_DATA;
+    SF_DEVICE_GUARD(c);
     if (c->levels == 2) return SF_E_UNSUPPORTED;
     if (!c->initialized) {
         SF_TRY(sf_launch_update_passes(c, Y, D, true));
@@ -304,7 +306,9 @@ static sf_status pyr_step(sf_ctx* c, const float* Y, const float* D) {
 }
 
 extern "C" sf_status sf_step(sf_ctx* c, const float* Y, const float* D) {
+    SF_NVTX("sf_step");
     if (!c || !Y || !D) return SF_E_DATA;
+    SF_DEVICE_GUARD(c);
     if (c->levels == 2) return pyr_step(c, Y, D);
     if (!c->initialized) return sf_update(c, Y, D);
     if (c->pending) return SF_E_STATE;
@@ -319,12 +323,23 @@ extern "C" sf_status sf_step(sf_ctx* c, const float* Y, const float* D) {
 }
 
 extern "C" sf_status sf_step_host(sf_ctx* c, const float* Yh, const float* Dh, float* wh, float* rh) {
+    SF_NVTX("sf_step_host");
     if (!c || !Yh || !Dh) return SF_E_DATA;
+    SF_DEVICE_GUARD(c);
     const size_t n = (size_t)c->fp.B * c->fp.H * c->fp.W;
-    if (!c->hY) {
-        if (cudaMalloc(&c->hY, n * sizeof(float)) != cudaSuccess || cudaMalloc(&c->hD, n * sizeof(float)) != cudaSuccess ||
-            cudaMalloc(&c->hw, 3 * n * sizeof(float)) != cudaSuccess || cudaMalloc(&c->hr, n * sizeof(float)) != cudaSuccess)
-            return SF_E_CUDA;
+    if (!c->hY) {  // staging buffers, committed only when all four allocations succeed
+        float* b[4] = {nullptr, nullptr, nullptr, nullptr};
+        const size_t sz[4] = {n, n, 3 * n, n};
+        for (int i = 0; i < 4; ++i)
+            if (cudaMalloc(&b[i], sz[i] * sizeof(float)) != cudaSuccess) {
+                for (int j = 0; j < 4; ++j)
+                    if (b[j]) cudaFree(b[j]);
+                return SF_E_CUDA;
+            }
+        c->hY = b[0];
+        c->hD = b[1];
+        c->hw = b[2];
+        c->hr = b[3];
     }
     SF_TRY(cudaMemcpyAsync(c->hY, Yh, n * sizeof(float), cudaMemcpyHostToDevice, c->stream));
     SF_TRY(cudaMemcpyAsync(c->hD, Dh, n * sizeof(float), cudaMemcpyHostToDevice, c->stream));
@@ -345,30 +360,52 @@ extern "C" sf_status sf_step_host(sf_ctx* c, const float* Yh, const float* Dh, f
 // Pipelined host-buffer frames: frame k's input copies (stream s_in), step + unpack (the
 // context stream) and output copies (stream s_out) overlap frame k-1's output copies and
 // frame k+1's input copies; slot k % 2 holds the device staging of frame k.
+static void async_teardown(sf_ctx* c) {
+    for (int i = 0; i < 2; ++i) {
+        if (c->aY[i]) cudaFree(c->aY[i]);
+        if (c->aD[i]) cudaFree(c->aD[i]);
+        if (c->aw[i]) cudaFree(c->aw[i]);
+        if (c->ar[i]) cudaFree(c->ar[i]);
+        if (c->ev_in[i]) cudaEventDestroy(c->ev_in[i]);
+        if (c->ev_done[i]) cudaEventDestroy(c->ev_done[i]);
+        if (c->ev_out[i]) cudaEventDestroy(c->ev_out[i]);
+        c->aY[i] = c->aD[i] = c->aw[i] = c->ar[i] = nullptr;
+        c->ev_in[i] = c->ev_done[i] = c->ev_out[i] = nullptr;
+    }
+    if (c->s_in) cudaStreamDestroy(c->s_in);
+    if (c->s_out) cudaStreamDestroy(c->s_out);
+    c->s_in = c->s_out = nullptr;
+}
+
 static sf_status async_setup(sf_ctx* c) {
     const size_t n = (size_t)c->fp.B * c->fp.H * c->fp.W;
-    for (int i = 0; i < 2; ++i) {
-        if (cudaMalloc(&c->aY[i], n * sizeof(float)) != cudaSuccess || cudaMalloc(&c->aD[i], n * sizeof(float)) != cudaSuccess ||
-            cudaMalloc(&c->aw[i], 3 * n * sizeof(float)) != cudaSuccess ||
-            cudaMalloc(&c->ar[i], n * sizeof(float)) != cudaSuccess ||
-            cudaEventCreateWithFlags(&c->ev_in[i], cudaEventDisableTiming) != cudaSuccess ||
-            cudaEventCreateWithFlags(&c->ev_done[i], cudaEventDisableTiming) != cudaSuccess ||
-            cudaEventCreateWithFlags(&c->ev_out[i], cudaEventDisableTiming) != cudaSuccess)
-            return SF_E_CUDA;
-        // "previous use finished" is true initially
-        if (cudaEventRecord(c->ev_done[i], c->stream) != cudaSuccess || cudaEventRecord(c->ev_out[i], c->stream) != cudaSuccess)
-            return SF_E_CUDA;
+    bool ok = true;
+    for (int i = 0; i < 2 && ok; ++i) {
+        ok = cudaMalloc(&c->aY[i], n * sizeof(float)) == cudaSuccess && cudaMalloc(&c->aD[i], n * sizeof(float)) == cudaSuccess &&
+             cudaMalloc(&c->aw[i], 3 * n * sizeof(float)) == cudaSuccess &&
+             cudaMalloc(&c->ar[i], n * sizeof(float)) == cudaSuccess &&
+             cudaEventCreateWithFlags(&c->ev_in[i], cudaEventDisableTiming) == cudaSuccess &&
+             cudaEventCreateWithFlags(&c->ev_done[i], cudaEventDisableTiming) == cudaSuccess &&
+             cudaEventCreateWithFlags(&c->ev_out[i], cudaEventDisableTiming) == cudaSuccess &&
+             // "previous use finished" is true initially
+             cudaEventRecord(c->ev_done[i], c->stream) == cudaSuccess && cudaEventRecord(c->ev_out[i], c->stream) == cudaSuccess;
     }
-    if (cudaStreamCreateWithFlags(&c->s_in, cudaStreamNonBlocking) != cudaSuccess ||
-        cudaStreamCreateWithFlags(&c->s_out, cudaStreamNonBlocking) != cudaSuccess)
+    ok = ok && cudaStreamCreateWithFlags(&c->s_in, cudaStreamNonBlocking) == cudaSuccess &&
+         cudaStreamCreateWithFlags(&c->s_out, cudaStreamNonBlocking) == cudaSuccess;
+    if (!ok) {  // nothing half-made survives: the next call retries from scratch
+        cudaStreamSynchronize(c->stream);
+        async_teardown(c);
         return SF_E_CUDA;
+    }
     c->async_ready = true;
     c->slot = 0;
     return SF_OK;
 }
 
 extern "C" sf_status sf_step_host_async(sf_ctx* c, const float* Yh, const float* Dh, float* wh, float* rh) {
+    SF_NVTX("sf_step_host_async");
     if (!c || !Yh || !Dh) return SF_E_DATA;
+    SF_DEVICE_GUARD(c);
     if (!c->async_ready) {
         sf_status st = async_setup(c);
         if (st != SF_OK) return st;
@@ -404,7 +441,9 @@ extern "C" sf_status sf_step_host_async(sf_ctx* c, const float* Yh, const float*
 }
 
 extern "C" sf_status sf_wait(sf_ctx* c) {
+    SF_NVTX("sf_wait");
     if (!c) return SF_E_DATA;
+    SF_DEVICE_GUARD(c);
     if (c->async_ready) {
         SF_TRY(cudaStreamSynchronize(c->s_in));
         SF_TRY(cudaStreamSynchronize(c->s_out));
@@ -414,7 +453,9 @@ extern "C" sf_status sf_wait(sf_ctx* c) {
 }
 
 extern "C" sf_status sf_get_fields(sf_ctx* c, int32_t which, float* w, float* rho, float* yhat) {
+    SF_NVTX("sf_get_fields");
     if (!c) return SF_E_DATA;
+    SF_DEVICE_GUARD(c);
     if (!c->initialized) return SF_E_STATE;
     const size_t n = (size_t)c->fp.B * c->fp.H * c->fp.W;
     if (c->levels == 2) {
@@ -437,7 +478,9 @@ extern "C" sf_status sf_get_fields(sf_ctx* c, int32_t which, float* w, float* rh
 }
 
 extern "C" sf_status sf_set_fields(sf_ctx* c, const float* w, const float* rho, const float* yhat) {
+    SF_NVTX("sf_set_fields");
     if (!c || !w || !rho) return SF_E_DATA;
+    SF_DEVICE_GUARD(c);
     if (c->levels == 2) return SF_E_UNSUPPORTED;
     const size_t n = (size_t)c->fp.B * c->fp.H * c->fp.W;
     SF_TRY(sf_launch_pack(c, w, rho, c->state[c->cur]));
@@ -451,7 +494,9 @@ extern "C" sf_status sf_set_fields(sf_ctx* c, const float* w, const float* rho, 
 }
 
 extern "C" sf_status sf_status_flags(sf_ctx* c, uint32_t* flags, int32_t clear) {
+    SF_NVTX("sf_status_flags");
     if (!c || !flags) return SF_E_DATA;
+    SF_DEVICE_GUARD(c);
     unsigned h = 0, ht = 0;
     SF_TRY(cudaMemcpyAsync(&h, c->flags, sizeof(unsigned), cudaMemcpyDeviceToHost, c->stream));
     if (c->top) SF_TRY(cudaMemcpyAsync(&ht, c->top->flags, sizeof(unsigned), cudaMemcpyDeviceToHost, c->stream));
@@ -473,10 +518,15 @@ extern "C" sf_status sf_set_motion(sf_ctx* c, const float* omega, const float* a
         f.imu = 0;
         return SF_OK;
     }
+    float om[3], ac[3];  // validated before anything is committed (a failure leaves the context unchanged)
     for (int k = 0; k < 3; ++k) {
-        f.om[k] = omega ? omega[k] : 0.0f;
-        f.ac[k] = accel ? accel[k] : 0.0f;
-        if (!isfinite(f.om[k]) || !isfinite(f.ac[k])) return SF_E_CONFIG;
+        om[k] = omega ? omega[k] : 0.0f;
+        ac[k] = accel ? accel[k] : 0.0f;
+        if (!isfinite(om[k]) || !isfinite(ac[k])) return SF_E_CONFIG;
+    }
+    for (int k = 0; k < 3; ++k) {
+        f.om[k] = om[k];
+        f.ac[k] = ac[k];
     }
     f.imu = 1;
     return SF_OK;

@@ -51,7 +51,9 @@ static bool compatible(const sf_ctx* a, const sf_ctx* b) {
 }
 
 extern "C" sf_status sf_halo_exchange_peer(sf_ctx* c, const sf_ctx* up, const sf_ctx* down) {
+    SF_NVTX("sf_halo_exchange_peer");
     if (!c) return SF_E_DATA;
+    SF_DEVICE_GUARD(c);
     if (!c->initialized) return SF_E_STATE;
     if (c->pending) return SF_E_STATE;
     if (c->ext_begin < c->own_begin) {  // top halo rows [ext_begin, own_begin) live in `up`
@@ -129,7 +131,9 @@ extern "C" void sf_nccl_comm_destroy(void* comm) {
 // rank+1, and receives its own halo rows from them.  Band heights >= halo (sf_band_partition), so
 // the rows a neighbour needs are always inside one band; both sides use the same halo size.
 extern "C" sf_status sf_halo_exchange_nccl(sf_ctx* c, void* comm, int32_t rank, int32_t nranks) {
+    SF_NVTX("sf_halo_exchange_nccl");
     if (!c || !comm) return SF_E_DATA;
+    SF_DEVICE_GUARD(c);
     if (!c->initialized || c->pending) return SF_E_STATE;
     NcclApi& n = nccl();
     if (!n.ok) return SF_E_NCCL;

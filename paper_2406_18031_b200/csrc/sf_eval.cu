@@ -77,7 +77,9 @@ constexpr int SF_EVAL_BLOCKS = 296;  // 2 x 148 SMs
 }  // namespace
 
 extern "C" sf_status sf_flow_px(sf_ctx* c, float* tangent, float* normal) {
+    SF_NVTX("sf_flow_px");
     if (!c) return SF_E_DATA;
+    SF_DEVICE_GUARD(c);
     if (!c->initialized) return SF_E_STATE;
     const FrameParams& f = c->fp;
     const size_t HW = (size_t)f.H * f.W, n = HW * f.B;
@@ -91,7 +93,9 @@ extern "C" sf_status sf_flow_px(sf_ctx* c, float* tangent, float* normal) {
 
 extern "C" sf_status sf_eval(sf_ctx* c, const float* w_gt, float* rmse, double* aae_deg, double* mean_rmse,
                              double* mean_aae) {
+    SF_NVTX("sf_eval");
     if (!c || !w_gt) return SF_E_DATA;
+    SF_DEVICE_GUARD(c);
     if (!c->initialized) return SF_E_STATE;
     const FrameParams& f = c->fp;
     const size_t HW = (size_t)f.H * f.W;

@@ -154,6 +154,7 @@ struct FusedArgs {
     CUtensorMap tmY;    // [B][H][W] brightness, box 64 x 72 x 1
     CUtensorMap tmD;    // [B][H][W] depth, box 64 x 72 x 1
     int tma;            // 1: stage e / Y / depth with TMA (needs W % 4 == 0, 16-byte aligned bases)
+    int y16;            // 1: Y and depth bases 16-byte aligned (the cp.async fallback may copy 16 bytes)
     int dbg_skip;       // timing experiments only (SF_DEBUG_SKIP): 1 = skip transport, 2 = skip update,
                         // 4 = no e TMA, 8 = no Y/depth TMA, 16 = no field / s loads, 32 = exit at entry,
                         // 64 = no column passes, 128 = no row passes, 256 = print phase clocks of CTA (6,5),
@@ -591,7 +592,7 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
         griddep_wait();  // inputs / state of this frame may come from the preceding kernel
         if (dbg & 2048) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt1_));
         if (a.upd) {
-            if (!edgeC && !edgeR && (f.W & 3) == 0 && (gj0 & 3) == 0) {
+            if (a.y16 && !edgeC && !edgeR && (f.W & 3) == 0 && (gj0 & 3) == 0) {
                 for (int idx = tid; idx < P / 4; idx += NT) {
                     const int r = idx / (RW / 4), c = (idx % (RW / 4)) * 4;
                     const size_t g = plane + (size_t)(gi0 + r) * f.W + (gj0 + c);
@@ -1275,6 +1276,7 @@ cudaError_t launch_cfg(sf_ctx* c, const float* Y, const float* D) {
         a.tma = !no_tma() && encode3d(&a.tmE, c->E, sf_ew(f.W), sf_eh(f.H), 6, FC::RW, FC::RH, 3) &&
                 encode3d(&a.tmY, Y, f.W, f.H, f.B, FC::RW, FC::RH, 1) &&
                 encode3d(&a.tmD, D, f.W, f.H, f.B, FC::RW, FC::RH, 1);
+        a.y16 = ((reinterpret_cast<uintptr_t>(Y) | reinterpret_cast<uintptr_t>(D)) & 15) == 0;
         a.fin = src;
         a.sk = c->state[c->cur];
         a.fout = upd ? c->state[1 - c->cur] : bufs[l & 1];

@@ -45,7 +45,9 @@ static sf_status make_map_params(int32_t cam_height, int32_t cam_width, const fl
 
 extern "C" sf_status sf_map_inputs(sf_ctx* c, const float* Ycam, const float* Zcam, int32_t cam_height,
                                    int32_t cam_width, const float* K, const float* Rcg, float* Y, float* D) {
+    SF_NVTX("sf_map_inputs");
     if (!c || !Ycam || !Zcam || !K || !Y || !D) return SF_E_DATA;
+    SF_DEVICE_GUARD(c);
     MapParams m;
     sf_status st = make_map_params(cam_height, cam_width, K, Rcg, &m);
     if (st != SF_OK) return st;
@@ -62,14 +64,21 @@ extern "C" sf_status sf_map_inputs(sf_ctx* c, const float* Ycam, const float* Zc
 // the per-cell gathers lengthen the one-wave kernel's prologue.)
 extern "C" sf_status sf_step_camera(sf_ctx* c, const float* Ycam, const float* Zcam, int32_t cam_height,
                                     int32_t cam_width, const float* K, const float* Rcg) {
+    SF_NVTX("sf_step_camera");
     if (!c || !Ycam || !Zcam || !K) return SF_E_DATA;
+    SF_DEVICE_GUARD(c);
     MapParams m;
     sf_status st = make_map_params(cam_height, cam_width, K, Rcg, &m);
     if (st != SF_OK) return st;
     const size_t n = (size_t)c->fp.B * c->fp.H * c->fp.W;
-    if (!c->mY) {
-        SF_TRY(cudaMalloc(&c->mY, n * sizeof(float)));
-        SF_TRY(cudaMalloc(&c->mD, n * sizeof(float)));
+    if (!c->mY) {  // committed only when both allocations succeed
+        float *y = nullptr, *d = nullptr;
+        if (cudaMalloc(&y, n * sizeof(float)) != cudaSuccess || cudaMalloc(&d, n * sizeof(float)) != cudaSuccess) {
+            if (y) cudaFree(y);
+            return SF_E_CUDA;
+        }
+        c->mY = y;
+        c->mD = d;
     }
     st = sf_map_inputs(c, Ycam, Zcam, cam_height, cam_width, K, Rcg, c->mY, c->mD);
     if (st != SF_OK) return st;

@@ -26,3 +26,24 @@ def test_graft_entry_has_build_and_smoke():
     sys.path.insert(0, ROOT)
     import __graft_entry__ as g
     assert callable(g.build) and callable(g.smoke)
+
+
+def test_reference_arm_config_matches_gpu_arm():
+    """Both arms print the same config dict for the same workload (the driver compares them)."""
+    sys.path.insert(0, ROOT)
+    import bench
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps", "1",
+                        "--warmup", "3"], capture_output=True, text=True, timeout=600, cwd=ROOT)
+    d = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][-1])
+    assert d["config"] == bench.workload_config(2, 1, 1, 1, None, False)
+    assert d["warmup"] == 3 and d["steps"] == 1
+
+
+def test_cpu_all_cores_aggregate():
+    """The all-cores CPU aggregate (independent sequences, one oracle process per core)."""
+    sys.path.insert(0, ROOT)
+    import bench
+    import sfgen
+    seq = sfgen.config_sequence(1, frames=3)
+    out = bench.cpu_all_cores(seq, t1=0.01, budget_s=0.05)
+    assert out["cores"] >= 1 and out["value"] > 0 and out["kind"] == "oracle"
