@@ -10,7 +10,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-SOURCES = ["sf_api.cu", "sf_passes.cu", "sf_fused.cu", "sf_band.cu", "sf_eval.cu", "sf_pyramid.cu", "sf_map.cu"]
+SOURCES = ["sf_api.cu", "sf_passes.cu", "sf_fused.cu", "sf_band.cu", "sf_eval.cu", "sf_pyramid.cu", "sf_map.cu", "sf_update.cu"]
 LIB = os.path.join(HERE, "libsf.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [

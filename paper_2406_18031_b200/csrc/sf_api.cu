@@ -221,6 +221,7 @@ extern "C" sf_status sf_create(const sf_config* cfg, const float* geometry, sf_c
         }
         // bottom level: fused prediction unless the pass kernels are requested; update on passes
         c->low_fused = cfg->kernel != SF_KERNEL_PASSES && sf_low_fused_supported(c);
+        c->upd_fused = cfg->kernel != SF_KERNEL_PASSES && sf_update_fused_supported(c);
         c->kernel = c->low_fused ? SF_KERNEL_FUSED : SF_KERNEL_PASSES;
         *out = c;
         return SF_OK;
@@ -248,7 +249,7 @@ extern "C" sf_status sf_predict(sf_ctx* c) {
     SF_DEVICE_GUARD(c);
     if (c->levels == 2) return SF_E_UNSUPPORTED;
     if (!c->initialized || c->pending) return SF_E_STATE;
-    SF_TRY(sf_launch_predict_passes(c));
+    SF_TRY(c->kernel == SF_KERNEL_FUSED ? sf_launch_predict_fused(c) : sf_launch_predict_passes(c));
     c->pending = true;
     return SF_OK;
 }
@@ -264,7 +265,11 @@ extern "C" sf_status sf_update(sf_ctx* c, const float* Y, const float* D) {
         return SF_OK;
     }
     if (!c->pending) return SF_E_STATE;
-    SF_TRY(sf_launch_update_passes(c, Y, D, false));
+    if (c->kernel == SF_KERNEL_FUSED)
+        SF_TRY(sf_launch_update_fused(c, Y, D, c->pred, reinterpret_cast<const float*>(c->state[c->cur]) + 3, 4,
+                                      c->yhat[c->cur], 1, c->state[1 - c->cur], c->yhat[1 - c->cur]));
+    else
+        SF_TRY(sf_launch_update_passes(c, Y, D, false));
     c->cur = 1 - c->cur;
     c->pending = false;
     return SF_OK;
@@ -537,8 +542,8 @@ extern "C" int32_t sf_kernel_in_use(const sf_ctx* c) { return c ? c->kernel : 0;
 extern "C" int32_t sf_launches_per_step(const sf_ctx* c) {
     if (!c) return 0;
     if (c->levels == 2)  // down2 + top + bottom prediction + update + S box + up2
-        return 1 + sf_launches_per_step(c->top) + (c->low_fused ? sf_low_fused_launches(c) : 2 * c->fp.N) + 1 +
-               c->fp.S + 1;
+        return 1 + sf_launches_per_step(c->top) + (c->low_fused ? sf_low_fused_launches(c) : 2 * c->fp.N) +
+               (c->upd_fused ? 1 : 1 + c->fp.S) + 1;
     if (c->kernel == SF_KERNEL_FUSED) return sf_fused_launches(c);
     return 2 * c->fp.N + 1 + c->fp.S;
 }

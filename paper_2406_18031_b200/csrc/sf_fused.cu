@@ -25,97 +25,17 @@
 #include <stdio.h>
 #include <stdlib.h>
 
+#include <string.h>
+
 #include <mutex>
 
-#include "sf_internal.cuh"
+#include "sf_pair.cuh"
 
 namespace {
 
-constexpr unsigned FULL = 0xffffffffu;
-
-// ---- paired float32 ops (sm_100a f32x2; each lane op is the IEEE float32 op)
-__device__ __forceinline__ float2 sub2(float2 a, float2 b) {
-    float2 d;
-    asm("{.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
-        "sub.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;}"
-        : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
-    return d;
-}
-__device__ __forceinline__ float2 add2(float2 a, float2 b) {
-    float2 d;
-    asm("{.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
-        "add.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;}"
-        : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
-    return d;
-}
-__device__ __forceinline__ float2 mul2(float2 a, float2 b) {
-    float2 d;
-    asm("{.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
-        "mul.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;}"
-        : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
-    return d;
-}
-__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
-    float2 d;
-    asm("{.reg .b64 ra, rb, rc, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
-        "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;}"
-        : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
-    return d;
-}
-
-__device__ __forceinline__ void cp_async4(float* sdst, const float* gsrc) {
-    const unsigned s = (unsigned)__cvta_generic_to_shared(sdst);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gsrc));
-}
-__device__ __forceinline__ void cp_async8(float* sdst, const float* gsrc) {
-    const unsigned s = (unsigned)__cvta_generic_to_shared(sdst);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gsrc));
-}
-__device__ __forceinline__ void cp_async16(float* sdst, const float* gsrc) {
-    const unsigned s = (unsigned)__cvta_generic_to_shared(sdst);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gsrc));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
-
-// ---- programmatic dependent launch (griddepcontrol; no-ops without the launch attribute)
-__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
-__device__ __forceinline__ void griddep_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;\n" ::); }
-
-// ---- mbarrier + TMA (cp.async.bulk.tensor) helpers
-__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
-        "r"(phase)
-        : "memory");
-}
-__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int x, int y, int z, uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n" ::
-            "r"(smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
-        : "memory");
-}
+using namespace sfp;
 
 
-// Iterate the cells of the rectangle [r0, r1] x [c0, c1] with NT threads, row-major, full lane
-// utilisation and no per-iteration integer division.
-#define SF_FOR_RECT(r, c, R0, R1, C0, C1, NT, tid)                                                  \
-    for (int nc_ = (C1) - (C0) + 1, dr_ = (NT) / nc_, dc_ = (NT) % nc_, r = (R0) + (tid) / nc_,   \
-             c = (C0) + (tid) % nc_;                                                             \
-         nc_ > 0 && r <= (R1); r += dr_ + ((c + dc_ > (C1)) ? 1 : 0), c = (c + dc_ > (C1)) ? c + dc_ - nc_ : c + dc_)
 
 // Replicate-border fill (reading 10) of the out-of-grid cells of the rectangle [ra, rb] x [ca, cb]
 // of NP shared planes: each takes the value of its clamped in-grid cell.  Only the out-of-grid
@@ -189,84 +109,6 @@ struct Cfg {
     static constexpr size_t SMEM = sizeof(float) * (8 * (size_t)P + XRF) + 64;  // + mbarriers
 };
 
-// Cell-paired helpers: every float2 holds one quantity of the thread's two cells (cell 0, cell 1),
-// so the per-cell arithmetic runs as f32x2 ops with no operand regrouping.
-// dot2 = fma(az, z, fma(ay, y, ax x)) per cell (the order of xdot3).
-__device__ __forceinline__ float2 dot2(float2 ax, float2 ay, float2 az, float2 x, float2 y, float2 z) {
-    return fma2(az, z, fma2(ay, y, mul2(ax, x)));
-}
-// f* = fma(-dt, fma(|u_hat|, f - f_up, f q), f) per cell -- equal (up to the sign of a zero) to the
-// literal fma(-dt, fma(u_hat, D, f q), f) with D the upwind difference, because
-// |u_hat| (f - f_up) and u_hat D are the same exact product.
-__device__ __forceinline__ float2 tr2(float2 v, float2 fu, float2 A, float2 Q, float2 T) {
-    return fma2(T, fma2(A, sub2(v, fu), mul2(v, Q)), v);
-}
-__device__ __forceinline__ float2 sel2(bool p0, bool p1, float2 a, float2 b) {
-    return make_float2(p0 ? a.x : b.x, p1 ? a.y : b.y);
-}
-
-// Cell-paired update arithmetic (the order of sf_internal.cuh's tap_g / tap_h / ls_solve3 per
-// lane of the pair; reciprocals stay scalar __frcp_rn).
-__device__ __forceinline__ float2 bc2(float x) { return make_float2(x, x); }
-__device__ __forceinline__ float2 neg2(float2 a) { return make_float2(-a.x, -a.y); }
-__device__ __forceinline__ float2 tap2_g(float2 x0, float2 x1, float2 x2, float2 x3, float2 x4) {
-    float2 a = mul2(bc2(SF_G0), x0);
-    a = fma2(bc2(SF_G1), x1, a);
-    a = fma2(bc2(SF_G2), x2, a);
-    a = fma2(bc2(SF_G1), x3, a);
-    return fma2(bc2(SF_G0), x4, a);
-}
-__device__ __forceinline__ float2 tap2_h(float2 x0, float2 x1, float2 x2, float2 x3, float2 x4) {
-    float2 a = mul2(bc2(SF_H0), x0);
-    a = fma2(bc2(SF_H1), x1, a);
-    a = fma2(bc2(0.0f), x2, a);
-    a = fma2(bc2(SF_H3), x3, a);
-    return fma2(bc2(SF_H4), x4, a);
-}
-template <bool FAST>
-__device__ __forceinline__ float2 rcp2(float2 a, bool& ok) {
-    return make_float2(rcp_rn<FAST>(a.x, ok), rcp_rn<FAST>(a.y, ok));
-}
-template <bool FAST>
-__device__ __forceinline__ void ls_solve3x2_t(const float2 g[3], const float2 m[3], float2 cY, float2 cr,
-                                              const float2 wp[3], float g1, float2 g2, float g3, float2 x[3], bool& ok) {
-    float2 g1g[3], g2m[3];
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-        g1g[a] = mul2(bc2(g1), g[a]);
-        g2m[a] = mul2(g2, m[a]);
-    }
-    const float2 G3 = bc2(g3);
-    const float2 A00 = add2(fma2(g2m[0], m[0], mul2(g1g[0], g[0])), G3);
-    const float2 A10 = fma2(g2m[1], m[0], mul2(g1g[1], g[0]));
-    const float2 A11 = add2(fma2(g2m[1], m[1], mul2(g1g[1], g[1])), G3);
-    const float2 A20 = fma2(g2m[2], m[0], mul2(g1g[2], g[0]));
-    const float2 A21 = fma2(g2m[2], m[1], mul2(g1g[2], g[1]));
-    const float2 A22 = add2(fma2(g2m[2], m[2], mul2(g1g[2], g[2])), G3);
-    float2 b[3];
-#pragma unroll
-    for (int a = 0; a < 3; ++a) b[a] = fma2(neg2(g2m[a]), cr, fma2(neg2(g1g[a]), cY, mul2(G3, wp[a])));
-    const float2 r0 = rcp2<FAST>(A00, ok);
-    const float2 l10 = mul2(A10, r0), l20 = mul2(A20, r0);
-    const float2 d1 = fma2(neg2(l10), A10, A11);
-    const float2 r1 = rcp2<FAST>(d1, ok);
-    const float2 t = fma2(neg2(l20), A10, A21);
-    const float2 l21 = mul2(t, r1);
-    const float2 dd2 = fma2(neg2(l21), t, fma2(neg2(l20), A20, A22));
-    const float2 r2 = rcp2<FAST>(dd2, ok);
-    const float2 y1 = fma2(neg2(l10), b[0], b[1]);
-    const float2 y2 = fma2(neg2(l21), y1, fma2(neg2(l20), b[0], b[2]));
-    x[2] = mul2(y2, r2);
-    x[1] = fma2(neg2(l21), x[2], mul2(y1, r1));
-    x[0] = fma2(neg2(l20), x[2], fma2(neg2(l10), x[1], mul2(b[0], r0)));
-}
-// fast reciprocals; the whole solve is redone with __frcp_rn if an input left the exact range
-__device__ __forceinline__ void ls_solve3x2(const float2 g[3], const float2 m[3], float2 cY, float2 cr,
-                                            const float2 wp[3], float g1, float2 g2, float g3, float2 x[3]) {
-    bool ok = true;
-    ls_solve3x2_t<true>(g, m, cY, cr, wp, g1, g2, g3, x, ok);
-    if (!ok) ls_solve3x2_t<false>(g, m, cY, cr, wp, g1, g2, g3, x, ok);
-}
 
 // The transport: M substeps of a column pass then a row pass on the thread's
 // 2 x K cells, held cell-paired: W[0..2][k] = w (x, y, z), W[3][k] = rho, each a float2 over the
@@ -278,17 +120,27 @@ __device__ __forceinline__ void ls_solve3x2(const float2 g[3], const float2 m[3]
 // dependency cone, like any cut edge.
 // EDGE = false (interior CTAs, no grid edge in the region) and IMU = false compile the edge
 // replicas and the inertial stage out, so the substep loop is straight-line code between barriers.
-template <int K, int NWY, int RULE, bool CLAMP, int NF = 4, bool EDGE = true, bool IMU = true>
+// EREG: the lane's e1 / e2 (ER[0..2] = e1.xyz, ER[3..5] = e2.xyz, cell-paired) are held in
+// registers instead of being read from the shared e planes each pass, and the run-end rows' v is
+// exchanged through the row buffer (as a fifth component) instead of being recomputed from e2.
+template <int K, int NWY, int RULE, bool CLAMP, int NF = 4, bool EDGE = true, bool IMU = true, bool EREG = false>
 __device__ __forceinline__ void transport_passes(const FrameParams& f, int M, float2 (&W)[NF][K], const float2 (&SX)[K],
                                                  const float2 (&SY)[K], const float2 (&SZ)[K], float (&mx)[K],
                                                  const float* Es, float2* XB0, int lane, int wy, int cmin, int cmax,
-                                                 int rmin, int rmax, int dbg, const float* Ss = nullptr) {
+                                                 int rmin, int rmax, int dbg, const float* Ss = nullptr,
+                                                 const float2 (*ER)[K] = nullptr) {
     using C = Cfg<K, NWY>;
     constexpr int RW = C::RW, P = C::P, RH = C::RH;
     // NF = 4: (w, rho), all dilated.  NF = 8 (pyramid bottom level): (w, dw, rho, Yhat), the last
     // one without dilation (eq:img_propagation_low)
     constexpr int ND = NF == 8 ? 7 : NF;
-    constexpr int XBS = NF * NWY * 2 * 32;  // float2 slots of one row-exchange buffer
+    constexpr int NX = EREG ? NF + 1 : NF;  // row-buffer components (+ v with EREG)
+    constexpr int XBS = NX * NWY * 2 * 32;  // float2 slots of one row-exchange buffer
+    const int c0_ = 2 * lane, r0_ = K * wy;
+    auto e1v = [&](int k, int q) -> float2 {  // component q of (e1, e2) at the lane's row k
+        if (EREG) return ER[q][k];
+        return *reinterpret_cast<const float2*>(Es + q * P + (r0_ + k) * RW + c0_);
+    };
     // NF = 4: two buffers (substep parity); NF = 8: one buffer (shared memory is short) and a
     // second barrier per substep after the neighbour rows are read
     constexpr int NXB = NF == 8 ? 1 : 2;
@@ -339,11 +191,7 @@ __device__ __forceinline__ void transport_passes(const FrameParams& f, int M, fl
         if (!(dbg & 64))
 #pragma unroll
         for (int k = 0; k < K; ++k) {
-            const int ib = (r0 + k) * RW + c0;
-            const float2 ex = *reinterpret_cast<const float2*>(Es + ib);
-            const float2 ey = *reinterpret_cast<const float2*>(Es + P + ib);
-            const float2 ez = *reinterpret_cast<const float2*>(Es + 2 * P + ib);
-            const float2 u = dot2(ex, ey, ez, W[0][k], W[1][k], W[2][k]);
+            const float2 u = dot2(e1v(k, 0), e1v(k, 1), e1v(k, 2), W[0][k], W[1][k], W[2][k]);
             const float uL = __shfl_up_sync(FULL, u.y, 1);    // lane-1's cell 1 = left of cell 0
             const float uR = __shfl_down_sync(FULL, u.x, 1);  // lane+1's cell 0 = right of cell 1
             bool p0, p1;
@@ -418,11 +266,10 @@ __device__ __forceinline__ void transport_passes(const FrameParams& f, int M, fl
             }
             float2 v[K];
 #pragma unroll
-            for (int k = 0; k < K; ++k) {
-                const int ib = (r0 + k) * RW + c0;
-                v[k] = dot2(*reinterpret_cast<const float2*>(Es + 3 * P + ib),
-                            *reinterpret_cast<const float2*>(Es + 4 * P + ib),
-                            *reinterpret_cast<const float2*>(Es + 5 * P + ib), W[0][k], W[1][k], W[2][k]);
+            for (int k = 0; k < K; ++k) v[k] = dot2(e1v(k, 3), e1v(k, 4), e1v(k, 5), W[0][k], W[1][k], W[2][k]);
+            if (EREG) {  // the run ends' v for the neighbour warps
+                XB[((NF * NWY + wy) * 2 + 0) * 32 + lane] = v[0];
+                XB[((NF * NWY + wy) * 2 + 1) * 32 + lane] = v[K - 1];
             }
             // row k in place from its upwind values fu (selected from the pre-pass rows k-1 / k+1)
             auto row_update = [&](int k, float2 vm, float2 vp, const float2 (&fm)[NF], const float2 (&fp)[NF]) {
@@ -479,13 +326,19 @@ __device__ __forceinline__ void transport_passes(const FrameParams& f, int M, fl
                 }
                 // (rows clamped to the region: the first / last warp's unused read stays off Y's plane,
                 //  which the Y / depth loads may still be writing)
-                const int it = (wy > 0 ? r0 - 1 : r0) * RW + c0, ibb = (wy < NWY - 1 ? r0 + K : r0 + K - 1) * RW + c0;
-                const float2 vtn = dot2(*reinterpret_cast<const float2*>(Es + 3 * P + it),
-                                        *reinterpret_cast<const float2*>(Es + 4 * P + it),
-                                        *reinterpret_cast<const float2*>(Es + 5 * P + it), tn[0], tn[1], tn[2]);
-                const float2 vbn = dot2(*reinterpret_cast<const float2*>(Es + 3 * P + ibb),
-                                        *reinterpret_cast<const float2*>(Es + 4 * P + ibb),
-                                        *reinterpret_cast<const float2*>(Es + 5 * P + ibb), bn[0], bn[1], bn[2]);
+                float2 vtn, vbn;
+                if (EREG) {  // the neighbours' own v of those rows (the same bits as recomputing it)
+                    vtn = XB[((NF * NWY + wt) * 2 + 1) * 32 + lane];
+                    vbn = XB[((NF * NWY + wb) * 2 + 0) * 32 + lane];
+                } else {
+                    const int it = (wy > 0 ? r0 - 1 : r0) * RW + c0, ibb = (wy < NWY - 1 ? r0 + K : r0 + K - 1) * RW + c0;
+                    vtn = dot2(*reinterpret_cast<const float2*>(Es + 3 * P + it),
+                               *reinterpret_cast<const float2*>(Es + 4 * P + it),
+                               *reinterpret_cast<const float2*>(Es + 5 * P + it), tn[0], tn[1], tn[2]);
+                    vbn = dot2(*reinterpret_cast<const float2*>(Es + 3 * P + ibb),
+                               *reinterpret_cast<const float2*>(Es + 4 * P + ibb),
+                               *reinterpret_cast<const float2*>(Es + 5 * P + ibb), bn[0], bn[1], bn[2]);
+                }
 #pragma unroll
                 for (int c = 0; c < NF; ++c) {
                     t[c] = sel2(useT, useT, tn[c], t[c]);
@@ -990,6 +843,161 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_fused(const __grid_constant__ F
     if (lane == 0 && any) atomicOr(a.flags, any);
 }
 
+// ================================================================== transport-only kernel (split step)
+// The prediction P1-P5 alone: M substeps on a RW x RH region with the halo R = M (rounded up to
+// 4) -- the update's 2S box halo is not carried through the transport (it is recomputed by the
+// update kernel, sf_update.cu, on its own tiles).  Same arithmetic and register layout as k_fused's
+// transport; writes (w*, rho*) of the tile.
+template <int K, int NWY, bool EREG = false>
+struct TransCfg {
+    static constexpr int RW = 64, RH = K * NWY, P = RW * RH, NT = 32 * NWY;
+    // floats: 2 row-exchange buffers of float2 slots, 4 components (+ v with EREG)
+    static constexpr int XBF = 2 * (EREG ? 5 : 4) * NWY * 2 * 32 * 2;
+    static constexpr size_t SMEM = sizeof(float) * (6 * (size_t)P + XBF) + 64;  // e planes | XB | bars
+};
+
+// EREG: e1 / e2 of the lane's cells held in registers for the whole frame (transport_passes).
+template <int K, int NWY, int RULE, bool CLAMP, bool EREG>
+__global__ void __launch_bounds__(32 * NWY, 1) k_trans(const __grid_constant__ FusedArgs a) {
+    using C = TransCfg<K, NWY, EREG>;
+    constexpr int RW = C::RW, RH = C::RH, P = C::P;
+    extern __shared__ __align__(1024) float4 smem4[];
+    float* const sm = reinterpret_cast<float*>(smem4);
+    float* const Es = sm;
+    float2* const XB0 = reinterpret_cast<float2*>(sm + 6 * P);
+    uint64_t* const bars = reinterpret_cast<uint64_t*>(sm + 6 * P + C::XBF);
+    const FrameParams& f = a.f;
+    const int tid = threadIdx.x, lane = tid & 31, wy = tid >> 5;
+    const int c0 = 2 * lane, r0 = K * wy;
+    const int b = blockIdx.z, R = a.R, TH = a.TH, TW = a.TW;
+    const int gi0 = blockIdx.y * TH - R, gj0 = blockIdx.x * TW - R;
+    const int cmin = max(0, -gj0), cmax = min(RW - 1, f.W - 1 - gj0);
+    const int rmin = max(0, -gi0), rmax = min(RH - 1, f.H - 1 - gi0);
+    const bool edge = cmin > 0 || cmax < RW - 1 || rmin > 0 || rmax < RH - 1;  // block-uniform
+    const size_t HW = (size_t)f.H * f.W, plane = (size_t)b * HW;
+    SF_PROF_DECL(a.dbg_skip & 8192);
+    SF_PROF();
+    // ---- the update kernel's inputs Y and depth (a.Y / a.D, 16-byte aligned; null when no update
+    // follows): each CTA prefetches its share of the frame into L2, so that the update kernel's
+    // loads hit L2 (a hint: L2 is the point of coherence, so it may run before the wait)
+    if (a.Y && tid == 0) {
+        const size_t bytes = (size_t)f.B * HW * sizeof(float) & ~(size_t)15;
+        const size_t ncta = (size_t)gridDim.x * gridDim.y * gridDim.z;
+        const size_t cta = blockIdx.x + (size_t)gridDim.x * (blockIdx.y + (size_t)gridDim.y * blockIdx.z);
+        const size_t chunk = ((bytes + ncta - 1) / ncta + 15) & ~(size_t)15, off = cta * chunk;
+        if (off < bytes) {
+            const unsigned n = (unsigned)min(chunk, bytes - off);
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(reinterpret_cast<const char*>(a.Y) + off), "r"(n)
+                         : "memory");
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(reinterpret_cast<const char*>(a.D) + off), "r"(n)
+                         : "memory");
+        }
+    }
+    // ---- e planes: TMA (geometry, independent of the previous kernel) or cp.async
+    if (a.tma) {
+        if (tid == 0) {
+            mbar_init(&bars[0], 1);
+            mbar_init(&bars[1], 1);
+            asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        }
+        __syncthreads();
+        if (tid == 0) {
+            mbar_expect_tx(&bars[0], 3u * P * 4u);
+            tma_load_3d(Es, &a.tmE, gj0 + SF_EPAD, gi0 + SF_EPAD, 0, &bars[0]);
+            mbar_expect_tx(&bars[1], 3u * P * 4u);
+            tma_load_3d(Es + 3 * P, &a.tmE, gj0 + SF_EPAD, gi0 + SF_EPAD, 3, &bars[1]);
+        }
+    } else {
+        const int EW = sf_ew(f.W);
+        const size_t EP = (size_t)EW * sf_eh(f.H);  // padded e planes: clamped cell (i, j) at (i + EPAD, j + EPAD)
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const int r = r0 + k;
+            const size_t gr = (size_t)(iclamp(gi0 + r, 0, f.H - 1) + SF_EPAD) * EW + SF_EPAD;
+            const size_t ga = gr + iclamp(gj0 + c0, 0, f.W - 1), gb = gr + iclamp(gj0 + c0 + 1, 0, f.W - 1);
+#pragma unroll
+            for (int p = 0; p < 6; ++p) {
+                float* dst = Es + p * P + r * RW + c0;
+                cp_async4(dst, a.E + p * EP + ga);
+                cp_async4(dst + 1, a.E + p * EP + gb);
+            }
+        }
+        cp_async_commit();
+    }
+    // ---- own directions s -> registers (geometry), then the fields once the previous kernel is done
+    float2 W[4][K];
+    float2 SX[K], SY[K], SZ[K];
+    float mx[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        const size_t gr = (size_t)iclamp(gi0 + r0 + k, 0, f.H - 1) * f.W;
+        const size_t ga = gr + iclamp(gj0 + c0, 0, f.W - 1), gb = gr + iclamp(gj0 + c0 + 1, 0, f.W - 1);
+        const float4 sa = __ldg(a.G0 + ga), sb = __ldg(a.G0 + gb);
+        SX[k] = make_float2(sa.x, sb.x);
+        SY[k] = make_float2(sa.y, sb.y);
+        SZ[k] = make_float2(sa.z, sb.z);
+        mx[k] = 0.0f;
+    }
+    griddep_wait();
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        const size_t gr = (size_t)iclamp(gi0 + r0 + k, 0, f.H - 1) * f.W;
+        const size_t ga = gr + iclamp(gj0 + c0, 0, f.W - 1), gb = gr + iclamp(gj0 + c0 + 1, 0, f.W - 1);
+        const float4 fa = a.fin[plane + ga], fb = a.fin[plane + gb];
+        W[0][k] = make_float2(fa.x, fb.x);
+        W[1][k] = make_float2(fa.y, fb.y);
+        W[2][k] = make_float2(fa.z, fb.z);
+        W[3][k] = make_float2(fa.w, fb.w);
+    }
+    griddep_launch_dependents();  // the update kernel's CTAs may start their geometry loads
+    SF_PROF();  // 0: prologue (s, griddep, fields)
+    if (a.tma) {
+        mbar_wait(&bars[0], 0);
+        mbar_wait(&bars[1], 0);
+    } else {
+        cp_async_wait<0>();
+    }
+    SF_PROF();  // 1: e planes landed
+    float2 ER[EREG ? 6 : 1][K];
+    if (EREG) {
+#pragma unroll
+        for (int q = 0; q < (EREG ? 6 : 1); ++q)
+#pragma unroll
+            for (int k = 0; k < K; ++k) ER[q][k] = *reinterpret_cast<const float2*>(Es + q * P + (r0 + k) * RW + c0);
+    }
+    if (edge || f.imu)
+        transport_passes<K, NWY, RULE, CLAMP, 4, true, true, EREG>(f, a.M, W, SX, SY, SZ, mx, Es, XB0, lane, wy, cmin,
+                                                                   cmax, rmin, rmax, 0, nullptr, ER);
+    else
+        transport_passes<K, NWY, RULE, CLAMP, 4, false, false, EREG>(f, a.M, W, SX, SY, SZ, mx, Es, XB0, lane, wy,
+                                                                     cmin, cmax, rmin, rmax, 0, nullptr, ER);
+    SF_PROF();  // 2: transport
+    // ---- flags from tile cells (exact at every pass; |u_hat| before the clamp) and the tile store
+    unsigned fl = 0;
+    const bool t0 = c0 >= R && c0 < R + TW && c0 >= cmin && c0 <= cmax;
+    const bool t1 = c0 + 1 >= R && c0 + 1 < R + TW && c0 + 1 >= cmin && c0 + 1 <= cmax;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        const int r = r0 + k;
+        if (r >= R && r < R + TH && r >= rmin && r <= rmax) {
+            if (t0 && gi0 + r >= f.fr0 && gi0 + r < f.fr1) {  // (R, TW even: the pair is in or out together)
+                if (CLAMP) {
+                    if (mx[k] > f.U) fl |= SF_FLAG_CLAMPED;
+                } else if (xmul(f.dt, mx[k]) > 1.0f) {
+                    fl |= SF_FLAG_CFL;
+                }
+            }
+            const size_t g = plane + (size_t)(gi0 + r) * f.W + (gj0 + c0);
+            if (t0) a.fout[g] = make_float4(W[0][k].x, W[1][k].x, W[2][k].x, W[3][k].x);
+            if (t1) a.fout[g + 1] = make_float4(W[0][k].y, W[1][k].y, W[2][k].y, W[3][k].y);
+        }
+    }
+    SF_PROF();  // 3: store
+    SF_PROF_PRINT("trans");
+    const unsigned any = __reduce_or_sync(FULL, fl);
+    if (lane == 0 && any) atomicOr(a.flags, any);
+}
+
 // ================================================================== pyramid bottom level (NEXT #1)
 // Fused prediction [P_[]] of the bottom level: M substeps of the 8-field transport (w, dw, rho,
 // Yhat advected by the reconstructed w; readings 26-27) for one tile, fields in registers
@@ -1256,6 +1264,16 @@ bool encode3d_raw(CUtensorMap* m, const float* base, int W, int H, int d2, int R
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+}  // namespace
+
+// TMA / PDL switches shared with sf_update.cu
+bool sf_tma_encode3d(CUtensorMap* m, const float* base, int W, int H, int d2, int RW, int RH, int bz) {
+    return !no_tma() && encode3d(m, base, W, H, d2, RW, RH, bz);
+}
+bool sf_pdl_enabled() { return !no_pdl(); }
+
+namespace {
+
 template <int K, int NWY>
 cudaError_t launch_cfg(sf_ctx* c, const float* Y, const float* D) {
     using FC = Cfg<K, NWY>;
@@ -1378,21 +1396,134 @@ cudaError_t launch_low(sf_ctx* c) {
     return cudaSuccess;
 }
 
+// Split step (default): ceil(N / 8) transport launches (k_trans, halo R = M) + one update launch
+// (k_upd, sf_update.cu).  SF_FUSED_MODE=mono selects the single-launch k_fused (halo M + 2S).
+// SF_TRANS_CFG picks the transport region shape (rows x warps) and where e1 / e2 live: 0 = 7 x 8
+// with e in registers (default), 1 = 7 x 8 with e read from shared memory, 2 = 4 x 14 (shared) --
+// all 64 x 56 regions.
+bool fused_mono() {
+    static const bool v = [] {
+        const char* e = getenv("SF_FUSED_MODE");
+        return e && e[0] == 'm';
+    }();
+    return v;
+}
+int trans_cfg() {
+    static const int v = [] {
+        const char* e = getenv("SF_TRANS_CFG");
+        return e ? atoi(e) : 0;
+    }();
+    return v;
+}
+
+template <int K, int NWY, bool EREG>
+bool prepare_trans() {
+    using TC = TransCfg<K, NWY, EREG>;
+    const void* fns[] = {(const void*)k_trans<K, NWY, SF_DOM_LARGEST, true, EREG>,
+                         (const void*)k_trans<K, NWY, SF_DOM_LARGEST, false, EREG>,
+                         (const void*)k_trans<K, NWY, SF_DOM_PRINTED, true, EREG>,
+                         (const void*)k_trans<K, NWY, SF_DOM_PRINTED, false, EREG>};
+    for (const void* fn : fns)
+        if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TC::SMEM) != cudaSuccess)
+            return false;
+    return true;
+}
+
+// Transport launches l = 0..L-1 (M <= 8 substeps each, halo R = M rounded up to 4); the last one
+// writes c->pred, earlier ones alternate through c->tmp / c->tmp2.
+template <int K, int NWY, bool EREG>
+cudaError_t launch_trans(sf_ctx* c, const float* Y, const float* D) {
+    using TC = TransCfg<K, NWY, EREG>;
+    const FrameParams& f = c->fp;
+    const int L = (f.N + MMAX - 1) / MMAX;
+    const float4* src = c->state[c->cur];
+    for (int l = 0; l < L; ++l) {
+        FusedArgs a;
+        memset(&a, 0, sizeof(a));
+        a.M = (l < L - 1) ? MMAX : f.N - MMAX * (L - 1);
+        a.R = (a.M + 3) & ~3;
+        a.TW = TC::RW - 2 * a.R;
+        a.TH = TC::RH - 2 * a.R;
+        a.tma = !no_tma() && encode3d(&a.tmE, c->E, sf_ew(f.W), sf_eh(f.H), 6, TC::RW, TC::RH, 3);
+        a.fin = src;
+        a.fout = (l == L - 1) ? c->pred : (((L - 1 - l) & 1) ? c->tmp : c->tmp2);
+        const bool pf = l == 0 && Y && D && ((reinterpret_cast<uintptr_t>(Y) | reinterpret_cast<uintptr_t>(D)) & 15) == 0;
+        a.Y = pf ? Y : nullptr;  // L2 prefetch of the update's inputs by the first launch
+        a.D = pf ? D : nullptr;
+        a.G0 = c->G0;
+        a.E = c->E;
+        a.flags = c->flags;
+        a.f = f;
+        {
+            static const int dbg_env = [] {
+                const char* e = getenv("SF_DEBUG_SKIP");
+                return e ? atoi(e) : 0;
+            }();
+            a.dbg_skip = dbg_env;
+        }
+        const dim3 grid((f.W + a.TW - 1) / a.TW, (f.H + a.TH - 1) / a.TH, f.B);
+        void (*kern)(FusedArgs) =
+            f.rule == SF_DOM_PRINTED
+                ? (f.clamp ? k_trans<K, NWY, SF_DOM_PRINTED, true, EREG> : k_trans<K, NWY, SF_DOM_PRINTED, false, EREG>)
+                : (f.clamp ? k_trans<K, NWY, SF_DOM_LARGEST, true, EREG> : k_trans<K, NWY, SF_DOM_LARGEST, false, EREG>);
+        cudaLaunchConfig_t lc = {};
+        lc.gridDim = grid;
+        lc.blockDim = dim3(TC::NT);
+        lc.dynamicSmemBytes = TC::SMEM;
+        lc.stream = c->stream;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = no_pdl() ? 0 : 1;
+        lc.attrs = at;
+        lc.numAttrs = 1;
+        cudaError_t e = cudaLaunchKernelEx(&lc, kern, a);
+        if (e == cudaSuccess) e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+        src = a.fout;
+    }
+    return cudaSuccess;
+}
+
 }  // namespace
 
 bool sf_fused_supported(const sf_ctx* c) {
+    // (sf_predict / sf_update on a fused context run k_trans / k_upd in either mode)
+    if ((c->fp.N + MMAX - 1) / MMAX > 8 || !sf_update_fused_supported(c)) return false;
+    bool ok;
+    switch (trans_cfg()) {
+        case 1: ok = prepare_trans<7, 8, false>(); break;
+        case 2: ok = prepare_trans<4, 14, false>(); break;
+        default: ok = prepare_trans<7, 8, true>(); break;
+    }
+    if (!ok || !fused_mono()) return ok;
     const Plan p = make_plan(c->fp);
-    if (p.launches > 8) return false;
     for (int l = 0; l < p.launches; ++l)
         if (64 - 2 * p.R[l] < 8 || 72 - 2 * p.R[l] < 8) return false;
     // opt in to the large dynamic shared-memory carve-out (one CTA per SM)
     return fused_cfg() == 1 ? prepare_cfg<4, 18>() : prepare_cfg<6, 12>();
 }
 
-int sf_fused_launches(const sf_ctx* c) { return make_plan(c->fp).launches; }
+int sf_fused_launches(const sf_ctx* c) {
+    if (fused_mono()) return make_plan(c->fp).launches;
+    return (c->fp.N + MMAX - 1) / MMAX + 1;
+}
+
+// The prediction alone (k_trans launches) into c->pred: sf_predict on the fused path.  Y / D
+// (nullable): the next update's inputs, prefetched into L2 by the transport.
+cudaError_t sf_launch_predict_fused(sf_ctx* c, const float* Y, const float* D) {
+    switch (trans_cfg()) {
+        case 1: return launch_trans<7, 8, false>(c, Y, D);
+        case 2: return launch_trans<4, 14, false>(c, Y, D);
+        default: return launch_trans<7, 8, true>(c, Y, D);
+    }
+}
 
 cudaError_t sf_launch_fused_step(sf_ctx* c, const float* Y, const float* D) {
-    return fused_cfg() == 1 ? launch_cfg<4, 18>(c, Y, D) : launch_cfg<6, 12>(c, Y, D);
+    if (fused_mono()) return fused_cfg() == 1 ? launch_cfg<4, 18>(c, Y, D) : launch_cfg<6, 12>(c, Y, D);
+    cudaError_t e = sf_launch_predict_fused(c, Y, D);
+    if (e != cudaSuccess) return e;
+    return sf_launch_update_fused(c, Y, D, c->pred, reinterpret_cast<const float*>(c->state[c->cur]) + 3, 4,
+                                  c->yhat[c->cur], 1, c->state[1 - c->cur], c->yhat[1 - c->cur]);
 }
 
 bool sf_low_fused_supported(const sf_ctx* c) {

@@ -428,6 +428,9 @@ cudaError_t sf_launch_update_low(sf_ctx* c, const float* Y, const float* D, bool
         return cudaGetLastError();
     }
     float4* nxt = c->state[1 - c->cur];
+    if (c->upd_fused)  // one tiled launch (sf_update.cu): references rho^{k+} = pred.w, Yhat^{k+} = Wpred.w
+        return sf_launch_update_fused(c, Y, D, c->pred, reinterpret_cast<const float*>(c->pred) + 3, 4,
+                                      reinterpret_cast<const float*>(c->Wpred) + 3, 4, nxt, c->yhat[0]);
     float4* solved = f.S > 0 ? c->tmp : nxt;
     k_update<<<g, blk, 0, c->stream>>>(Y, D, c->pred, c->pred, reinterpret_cast<const float*>(c->Wpred) + 3, 4,
                                        c->yhat[0], solved, c->G0, c->G1, c->G2, f, c->flags);

@@ -1,0 +1,465 @@
+// sf_update.cu -- the update step U1-U5 as ONE tiled kernel per frame: brightness
+// model (eq:img_model), inverse-depth model (eq:dominant_b1/b2), the per-
+// pixel 3x3 LS (eq:LS_update), S passes of the 5x5 box (reading 13) and the
+// inverse-depth fusion (eq:cost_invdepth).  Same bits as sf_passes.cu's k_update +
+// S x k_box.
+//
+// Layout.  A CTA owns an output tile TH x TW and works on shared planes
+// of PH x PW cells: the tile plus a margin of MR = h + 2 rows and MG >= h + 3 columns (h = 2S,
+// MG a multiple of 4 so the box's 16-byte accesses stay aligned).  The box passes need w_LS on the
+// tile +- h, so the LS is solved there (the solve region, SR); the models need Y on SR +- 2 and the
+// depth on SR +- 1.  Y and depth are loaded with replicate-clamped indices (reading 10), so the
+// models need no edge logic; the box's out-of-grid window cells are filled with their clamped
+// in-grid cell (edge CTAs only).
+//   stage 0: Y, depth -> planes (two TMA tensor copies of the whole plane, issued before the wait
+//            on the transport kernel: they are the caller's inputs, and the transport kernel has
+//            prefetched them into L2; edge CTAs then replace the zero-filled out-of-grid cells by
+//            their clamped cell; cp.async with clamped indices without TMA); the first solve
+//            item's global inputs fetched;
+//   stage 1: rhohat plane (NaN = invalid) + horizontal taps HG = hz(g, Y), HH = hz(h, Y);
+//   stage 2: per SR pair of cells: vertical taps -> Yhat', beta_1, beta_2; rho one-sided
+//            differences; ghat, m; c_Y, c_rho; LDL^T solve -> w_LS planes; Yhat^{k+1} of tile cells
+//            stored; the next item's global inputs (w^{k+}, s, e1, e2, references) fetched one
+//            item ahead;
+//   stage 3: S box passes, each separable in two sweeps over the shared planes (horizontal
+//            5-sums of the window rows, then vertical 5-sums / 25), one 4-column quad per item;
+//   stage 4: rho fusion and the coalesced store of (w^{k+1}, rho^{k+1}) for the tile.
+// The top level (H = 1) and the pyramid's bottom level [dU] (reading 28: references Yhat^{k+},
+// rho^{k+} instead of Yhat^k, rho^k) run the same kernel with different reference pointers.
+#include <stdint.h>
+#include <stdlib.h>
+
+#include "sf_pair.cuh"
+
+namespace {
+
+using namespace sfp;
+
+struct UpdArgs {
+    CUtensorMap tmY;           // [B][H][W] brightness, box PW x PH x 1 (valid when tma)
+    CUtensorMap tmD;           // [B][H][W] depth, box PW x PH x 1
+    int tma;
+    const float4* pred;        // [B][H][W] (w^{k+}, rho^{k+})
+    const float* rref;         // rho reference of c_rho, element p at rref[p * rs]
+    const float* yref;         // Yhat reference of c_Y, element p at yref[p * ys]
+    int rs, ys;
+    const float* Y;            // [B][H][W] brightness
+    const float* D;            // [B][H][W] depth (or inverse depth)
+    const float4* G0;          // (s, d2)
+    const float4* G1;          // (e1, ds)
+    const float4* G2;          // (e2, 0)
+    float4* out;               // (w^{k+1}, rho^{k+1})
+    float* yout;               // Yhat^{k+1}
+    unsigned* flags;
+    FrameParams f;
+    int TH, TW, h, MR, MG, PH, PW, P;  // P: plane stride (PH * PW rounded up to 32 floats)
+    int dbg;                           // SF_DEBUG_SKIP (debug builds only): 8192 = phase profile
+};
+
+// 14 warps, one CTA per SM (<= 146 registers); the 48 x 40 tile's 1344 solve pairs are exactly 3
+// per thread
+constexpr int UPD_NT = 448;
+
+// Replicate fill (reading 10) of the out-of-grid cells of [ra, rb] x [ca, cb] (clipped to the
+// plane) in NP planes (p, p + P, ...) of row stride PW: each takes the value of its clamped
+// in-grid cell.
+template <int NP>
+__device__ __forceinline__ void fill_planes(float* p, int P, int PW, int PH, int ra, int rb, int ca, int cb, int rmin,
+                                            int rmax, int cmin, int cmax, int tid) {
+    ra = max(ra, 0);
+    rb = min(rb, PH - 1);
+    ca = max(ca, 0);
+    cb = min(cb, PW - 1);
+    auto band = [&](int r0, int r1, int c0, int c1) {
+        const int nc = c1 - c0 + 1, nr = r1 - r0 + 1;
+        if (nc <= 0 || nr <= 0) return;
+#pragma unroll 1
+        for (int t = tid; t < nc * nr; t += UPD_NT) {
+            const int q = t / nc, r = r0 + q, c = c0 + t - q * nc;
+            const int from = iclamp(r, rmin, rmax) * PW + iclamp(c, cmin, cmax), to = r * PW + c;
+#pragma unroll
+            for (int q = 0; q < NP; ++q) p[q * P + to] = p[q * P + from];
+        }
+    };
+    band(ra, min(rb, rmin - 1), ca, cb);            // rows above the grid (with corners)
+    band(max(ra, rmax + 1), rb, ca, cb);            // rows below
+    band(max(ra, rmin), min(rb, rmax), ca, min(cb, cmin - 1));  // left columns
+    band(max(ra, rmin), min(rb, rmax), max(ca, cmax + 1), cb);  // right columns
+}
+
+// The global inputs of one solve item (a horizontal pair of SR cells).
+struct SolveIn {
+    float4 wa, wb;   // pred: (w^{k+}, rho^{k+})
+    float4 sa, sb;   // G0: (s, d2)
+    float4 ea, eb;   // G1: e1
+    float4 fa, fb;   // G2: e2
+    float2 y, rk;    // Yhat and rho references
+};
+
+__global__ void __launch_bounds__(UPD_NT, 1) k_upd(const __grid_constant__ UpdArgs a) {
+    extern __shared__ __align__(1024) float sm[];  // TMA destinations: 128-byte aligned planes
+    const FrameParams& f = a.f;
+    const int tid = threadIdx.x;
+    const int PH = a.PH, PW = a.PW, P = a.P, h = a.h, MR = a.MR, MG = a.MG, TH = a.TH, TW = a.TW;
+    float* const Ys = sm;          // Y; after the models: rho^{k+} of the SR cells (RP)
+    float* const RHs = sm + P;     // depth -> rhohat (NaN = invalid), read by the fusion
+    float* const HG = sm + 2 * P;  // horizontal g-taps of Y
+    float* const HH = sm + 3 * P;  // horizontal h-taps of Y
+    float* const F0 = sm + 4 * P;  // 3 planes: w_LS, smoothed in place by the box passes
+    float* const F1 = sm + 7 * P;  // 3 planes: the box's horizontal sums
+    float* const RP = Ys;
+    uint64_t* const bar = reinterpret_cast<uint64_t*>(sm + 10 * P);
+    const int b = blockIdx.z;
+    const int i0 = blockIdx.y * TH, j0 = blockIdx.x * TW;
+    const int oi = i0 - MR, oj = j0 - MG;  // global cell of plane cell (0, 0)
+    // in-grid part of the plane (also the replicate-clamp bounds), plane coordinates
+    const int rmin = max(0, -oi), rmax = min(PH - 1, f.H - 1 - oi);
+    const int cmin = max(0, -oj), cmax = min(PW - 1, f.W - 1 - oj);
+    const size_t HW = (size_t)f.H * f.W, pl = (size_t)b * HW;
+    const int lc0 = MG - h - 2, ncl = TW + 2 * h + 4;  // columns of Y used: SR +- 2 (depth: SR +- 1)
+    SF_PROF_DECL(a.dbg & 8192);
+    SF_PROF();
+
+    // ---------------- stage 0: Y and depth (caller inputs, prefetched into L2 by the transport
+    // kernel): the whole plane by TMA, or the used columns by cp.async with clamped indices
+    if (a.tma) {
+        if (tid == 0) {
+            mbar_init(bar, 1);
+            asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+            mbar_expect_tx(bar, 2u * PH * PW * 4u);
+            tma_load_3d(Ys, &a.tmY, oj, oi, b, bar);
+            tma_load_3d(RHs, &a.tmD, oj, oi, b, bar);
+        }
+    } else {
+        SF_FOR_RECT(r, c, 0, PH - 1, lc0, lc0 + ncl - 1, UPD_NT, tid) {
+            const size_t g = pl + (size_t)iclamp(oi + r, 0, f.H - 1) * f.W + iclamp(oj + c, 0, f.W - 1);
+            cp_async4(Ys + r * PW + c, a.Y + g);
+            cp_async4(RHs + r * PW + c, a.D + g);
+        }
+        cp_async_commit();
+    }
+
+    // solve region (in-grid), its pair grid, and the first item's global inputs (geometry now,
+    // the transported fields once the transport kernel has completed).  Fetches are branch-free
+    // (a thread past the region re-fetches the region's last row) so that no in-flight load is
+    // copied between registers before its first use.
+    const int srl = max(MR - h, rmin), srh = min(MR + TH + h - 1, rmax);
+    const int scl = max(MG - h, cmin), sch = min(MG + TW + h - 1, cmax);  // scl even (MG - h even, or the grid's column 0)
+    const int np = (sch - scl + 2) >> 1;
+    const int pdr = UPD_NT / np, pdc = UPD_NT % np;
+    int rn = srl + tid / np, pn = tid % np;
+    SolveIn nx;
+    auto fetch_geo = [&](int r, int pc, SolveIn& q) {
+        r = min(r, srh);
+        const int c = scl + 2 * pc, c1 = min(c + 1, sch);
+        const size_t ga = (size_t)(oi + r) * f.W + (oj + c), gb = (size_t)(oi + r) * f.W + (oj + c1);
+        q.sa = __ldg(a.G0 + ga);
+        q.sb = __ldg(a.G0 + gb);
+        q.ea = __ldg(a.G1 + ga);
+        q.eb = __ldg(a.G1 + gb);
+        q.fa = __ldg(a.G2 + ga);
+        q.fb = __ldg(a.G2 + gb);
+    };
+    auto fetch_fld = [&](int r, int pc, SolveIn& q) {
+        r = min(r, srh);
+        const int c = scl + 2 * pc, c1 = min(c + 1, sch);
+        const size_t ga = pl + (size_t)(oi + r) * f.W + (oj + c), gb = pl + (size_t)(oi + r) * f.W + (oj + c1);
+        q.wa = a.pred[ga];
+        q.wb = a.pred[gb];
+        q.y = make_float2(a.yref[ga * a.ys], a.yref[gb * a.ys]);
+        q.rk = make_float2(a.rref[ga * a.rs], a.rref[gb * a.rs]);
+    };
+    fetch_geo(rn, pn, nx);
+    griddep_wait();  // w^{k+} and the references come from the preceding kernels
+    griddep_launch_dependents();
+    SF_PROF();  // 0: stage-0 issue + griddep
+    fetch_fld(rn, pn, nx);
+    if (a.tma) {
+        mbar_wait(bar, 0);
+        if (rmin > 0 || rmax < PH - 1 || cmin > 0 || cmax < PW - 1) {  // out-of-grid cells arrived as zeros
+            __syncthreads();
+            fill_planes<2>(Ys, P, PW, PH, 0, PH - 1, 0, PW - 1, rmin, rmax, cmin, cmax, tid);
+        }
+    } else {
+        cp_async_wait<0>();
+    }
+    __syncthreads();
+    SF_PROF();  // 1: Y / depth landed (+ edge fill)
+
+    // ---------------- stage 1: rhohat + horizontal brightness taps, pairs of cells
+    const float qnan = __int_as_float(0x7fffffff);
+    unsigned fl = 0;
+    bool okall = true;  // every reciprocal took rcp_fast's exact range
+    const int tr0 = max(MR, rmin), tr1 = min(MR + TH - 1, rmax);  // tile rows / columns in the grid
+    const int tc0 = max(MG, cmin), tc1 = min(MG + TW - 1, cmax);
+    {
+        auto ld2 = [&](const float* p, int i) { return *reinterpret_cast<const float2*>(p + i); };
+#pragma unroll 1
+        SF_FOR_RECT(r, pc, 0, PH - 1, 0, (ncl >> 1) - 1, UPD_NT, tid) {
+            const int c = lc0 + 2 * pc, idx = r * PW + c;
+            const float2 d = ld2(RHs, idx);
+            bool ok0 = true, ok1 = true;
+            const float rh0 = f.is_inv ? d.x : rcp_fast(d.x, ok0), rh1 = f.is_inv ? d.y : rcp_fast(d.y, ok1);
+            const bool v0 = depth_valid(d.x, f.is_inv), v1 = depth_valid(d.y, f.is_inv);
+            *reinterpret_cast<float2*>(RHs + idx) = make_float2(v0 ? rh0 : qnan, v1 ? rh1 : qnan);
+            okall = okall && (ok0 || !v0) && (ok1 || !v1);
+            if (c >= MG - h && c < MG + TW + h) {  // HG / HH on the SR columns
+                const float2 ya = ld2(Ys, idx - 2), yb = ld2(Ys, idx), yc = ld2(Ys, idx + 2);
+                const float2 x1 = make_float2(ya.y, yb.x), x3 = make_float2(yb.y, yc.x);
+                *reinterpret_cast<float2*>(HG + idx) = tap2_g(ya, x1, yb, x3, yc);
+                *reinterpret_cast<float2*>(HH + idx) = tap2_h(ya, x1, yb, x3, yc);
+                if (r >= tr0 && r <= tr1 && oi + r >= f.fr0 && oi + r < f.fr1) {  // Y of tile cells finite
+                    if (c >= tc0 && c <= tc1 && !isfinite(yb.x)) fl |= SF_FLAG_NONFINITE;
+                    if (c + 1 >= tc0 && c + 1 <= tc1 && !isfinite(yb.y)) fl |= SF_FLAG_NONFINITE;
+                }
+            }
+        }
+    }
+    if (__syncthreads_or(!okall)) {  // (never for depths in [2^-126, 2^126)): exact reciprocals
+#pragma unroll 1
+        SF_FOR_RECT(r, c, 0, PH - 1, lc0, lc0 + ncl - 1, UPD_NT, tid) {
+            // the depth itself is gone: recompute from the global input (replicate-clamped)
+            const size_t g = pl + (size_t)iclamp(oi + r, 0, f.H - 1) * f.W + iclamp(oj + c, 0, f.W - 1);
+            const float d = a.D[g];
+            RHs[r * PW + c] = depth_valid(d, f.is_inv) ? rho_hat(d, f.is_inv) : qnan;
+        }
+        __syncthreads();
+    }
+
+    SF_PROF();  // 2: models
+    // ---------------- stage 2: per-pixel LS on SR, a horizontal pair of cells per item
+    {
+        auto ld2 = [&](const float* p, int i) { return *reinterpret_cast<const float2*>(p + i); };
+#pragma unroll 1
+        while (rn <= srh) {
+            const int r = rn, c = scl + 2 * pn;
+            const SolveIn cu = nx;
+            rn += pdr + ((pn + pdc >= np) ? 1 : 0);
+            pn = (pn + pdc >= np) ? pn + pdc - np : pn + pdc;
+            fetch_geo(rn, pn, nx);
+            fetch_fld(rn, pn, nx);
+            const bool full = c + 1 <= sch;
+            const int idx = r * PW + c;  // even: 8-byte aligned pairs (a ragged pair's second cell is unused)
+            const float2 g0 = ld2(HG, idx - 2 * PW), g1 = ld2(HG, idx - PW), g2 = ld2(HG, idx), g3 = ld2(HG, idx + PW),
+                         g4 = ld2(HG, idx + 2 * PW);
+            const float2 h0 = ld2(HH, idx - 2 * PW), h1 = ld2(HH, idx - PW), h2 = ld2(HH, idx), h3 = ld2(HH, idx + PW),
+                         h4 = ld2(HH, idx + 2 * PW);
+            const float2 yh = tap2_g(g0, g1, g2, g3, g4);  // Yhat^{k+1}
+            const float2 be1 = tap2_g(h0, h1, h2, h3, h4);
+            const float2 be2 = tap2_h(g0, g1, g2, g3, g4);
+            const float2 rc = ld2(RHs, idx), ru = ld2(RHs, idx - PW), rd = ld2(RHs, idx + PW);
+            const float rl = RHs[idx - 1], rr = RHs[idx + 2];
+            const bool vc0 = !isnan(rc.x), vc1 = !isnan(rc.y);
+            const float2 rh = make_float2(vc0 ? rc.x : 0.0f, vc1 ? rc.y : 0.0f);
+            // eq:dominant_b1 / b2 per cell (the pair's cells are each other's row neighbour)
+            const float2 br1 = make_float2(pick_side(rh.x, vc0, rl, !isnan(rl), rc.y, vc1),
+                                           pick_side(rh.y, vc1, rc.x, vc0, rr, !isnan(rr)));
+            const float2 br2 = make_float2(pick_side(rh.x, vc0, ru.x, !isnan(ru.x), rd.x, !isnan(rd.x)),
+                                           pick_side(rh.y, vc1, ru.y, !isnan(ru.y), rd.y, !isnan(rd.y)));
+            const float2 d2 = make_float2(cu.sa.w, cu.sb.w);
+            const float2 e1a[3] = {make_float2(cu.ea.x, cu.eb.x), make_float2(cu.ea.y, cu.eb.y),
+                                   make_float2(cu.ea.z, cu.eb.z)};
+            const float2 e2a[3] = {make_float2(cu.fa.x, cu.fb.x), make_float2(cu.fa.y, cu.fb.y),
+                                   make_float2(cu.fa.z, cu.fb.z)};
+            const float2 sp[3] = {make_float2(cu.sa.x, cu.sb.x), make_float2(cu.sa.y, cu.sb.y),
+                                  make_float2(cu.sa.z, cu.sb.z)};
+            float2 gh[3], m[3];
+            const float2 d2r = mul2(d2, rh);
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+                gh[q] = mul2(d2, fma2(e2a[q], be2, mul2(e1a[q], be1)));
+                const float2 drq = mul2(d2, fma2(e2a[q], br2, mul2(e1a[q], br1)));
+                m[q] = fma2(d2r, sp[q], drq);
+            }
+            const float2 cY = mul2(d2, sub2(yh, cu.y));   // eq:img_cost_top
+            const float2 cr = mul2(d2, sub2(rh, cu.rk));  // eq:invdepth_cost_top
+            const float2 wp[3] = {make_float2(cu.wa.x, cu.wb.x), make_float2(cu.wa.y, cu.wb.y),
+                                  make_float2(cu.wa.z, cu.wb.z)};
+            float2 x[3];
+            ls_solve3x2(gh, m, cY, cr, wp, f.g1, make_float2(vc0 ? f.g2 : 0.0f, vc1 ? f.g2 : 0.0f), f.g3, x);
+            *reinterpret_cast<float2*>(F0 + idx) = x[0];  // (a ragged pair's second cell: out of the grid, unused)
+            *reinterpret_cast<float2*>(F0 + P + idx) = x[1];
+            *reinterpret_cast<float2*>(F0 + 2 * P + idx) = x[2];
+            *reinterpret_cast<float2*>(RP + idx) = make_float2(cu.wa.w, cu.wb.w);
+            if (r >= tr0 && r <= tr1) {  // tile cells: Yhat^{k+1}, non-finite solve flag
+                const size_t g = pl + (size_t)(oi + r) * f.W + (oj + c);
+                const bool in0 = c >= tc0 && c <= tc1, in1 = full && c + 1 >= tc0 && c + 1 <= tc1;
+                if (in0) a.yout[g] = yh.x;
+                if (in1) a.yout[g + 1] = yh.y;
+                const bool bad = (in0 && !(isfinite(x[0].x) && isfinite(x[1].x) && isfinite(x[2].x))) ||
+                                 (in1 && !(isfinite(x[0].y) && isfinite(x[1].y) && isfinite(x[2].y)));
+                if (bad && oi + r >= f.fr0 && oi + r < f.fr1) fl |= SF_FLAG_NONFINITE;
+            }
+        }
+    }
+
+    SF_PROF();  // 3: solve
+    // ---------------- stage 3: S x 5x5 box (reading 13): horizontal 5-sums left to right
+    // (F0 -> F1), then vertical 5-sums top to bottom / 25 (F1 -> F0: the pass's input is dead by
+    // then), so the smoothed field stays in F0.  Items are one component's 4-column quad of one row
+    // (16-byte shared accesses, consecutive quads on consecutive lanes: conflict-free); div25 is
+    // the IEEE quotient.
+    const bool edge = i0 - h < 0 || i0 + TH + h > f.H || j0 - h < 0 || j0 + TW + h > f.W;  // SR leaves the grid
+    const int S = f.S;
+    const float2 y25 = make_float2(0.04f, 0.04f), m25 = make_float2(-25.0f, -25.0f);
+#pragma unroll 1
+    for (int it = 0; it < S; ++it) {
+        const int mo = 2 * (S - 1 - it);  // this pass's output: tile +- mo, in the grid
+        const int or0 = max(MR - mo, rmin), or1 = min(MR + TH + mo - 1, rmax);
+        const int oc0 = max(MG - mo, cmin), oc1 = min(MG + TW + mo - 1, cmax);
+        const int bc0 = oc0 & ~3, nbc = (oc1 - bc0) / 4 + 1;  // 16-byte aligned quads over [oc0, oc1]
+        __syncthreads();
+        if (edge) {
+            fill_planes<3>(F0, P, PW, PH, or0 - 2, or1 + 2, oc0 - 2, oc1 + 2, rmin, rmax, cmin, cmax, tid);
+            __syncthreads();
+        }
+        // horizontal sums of the window rows (quads reading columns c-2 .. c+5; columns outside the
+        // window feed only unstored outputs)
+#pragma unroll 1
+        SF_FOR_RECT(r, bq, or0 - 2, or1 + 2, 0, 3 * nbc - 1, UPD_NT, tid) {
+            const int q = (bq >= nbc) + (bq >= 2 * nbc), c = bc0 + 4 * (bq - q * nbc);
+            const float* row = F0 + q * P + r * PW + c - 2;
+            const float2 xa = *reinterpret_cast<const float2*>(row);
+            const float4 xb = *reinterpret_cast<const float4*>(row + 2);
+            const float2 xc = *reinterpret_cast<const float2*>(row + 6);
+            const float2 xab = make_float2(xa.y, xb.x), xbb = make_float2(xb.y, xb.z), xbc = make_float2(xb.w, xc.x);
+            const float2 xlo = make_float2(xb.x, xb.y), xhi = make_float2(xb.z, xb.w);
+            // sums of columns (c + j - 2 .. c + j + 2), j = 0..3, paired: ((((x0 + x1) + x2) + x3) + x4)
+            const float2 s0 = add2(add2(add2(add2(xa, xab), xlo), xbb), xhi);
+            const float2 s1 = add2(add2(add2(add2(xlo, xbb), xhi), xbc), xc);
+            *reinterpret_cast<float4*>(F1 + q * P + r * PW + c) = make_float4(s0.x, s0.y, s1.x, s1.y);
+        }
+        __syncthreads();
+#pragma unroll 1
+        SF_FOR_RECT(r, bq, or0, or1, 0, 3 * nbc - 1, UPD_NT, tid) {
+            const int q = (bq >= nbc) + (bq >= 2 * nbc), c = bc0 + 4 * (bq - q * nbc);
+            const float* col = F1 + q * P + (r - 2) * PW + c;
+            float4 v4[5];
+#pragma unroll
+            for (int i = 0; i < 5; ++i) v4[i] = *reinterpret_cast<const float4*>(col + i * PW);
+            float o[4];
+#pragma unroll
+            for (int jp = 0; jp < 2; ++jp) {
+                auto lo = [&](const float4& x) { return jp ? make_float2(x.z, x.w) : make_float2(x.x, x.y); };
+                const float2 v = add2(add2(add2(add2(lo(v4[0]), lo(v4[1])), lo(v4[2])), lo(v4[3])), lo(v4[4]));
+                const float2 qq = mul2(v, y25);
+                const float2 q1 = fma2(fma2(qq, m25, v), y25, qq);
+                o[2 * jp] = isfinite(v.x) ? q1.x : qq.x;
+                o[2 * jp + 1] = isfinite(v.y) ? q1.y : qq.y;
+            }
+            *reinterpret_cast<float4*>(F0 + q * P + r * PW + c) = make_float4(o[0], o[1], o[2], o[3]);
+        }
+    }
+    float* const src = F0;
+    __syncthreads();
+    SF_PROF();  // 4: box
+
+    // ---------------- stage 4: rho fusion and the store of the tile
+    const float kap = f.kappa;
+#pragma unroll 1
+    SF_FOR_RECT(r, c, tr0, tr1, tc0, tc1, UPD_NT, tid) {
+        const int idx = r * PW + c;
+        const float rh = RHs[idx], rp = RP[idx];
+        const bool v = !isnan(rh);
+        const float rn1 = xfma(v ? kap : 0.0f, xsub(v ? rh : 0.0f, rp), rp);
+        if (!isfinite(rn1) && oi + r >= f.fr0 && oi + r < f.fr1) fl |= SF_FLAG_NONFINITE;
+        a.out[pl + (size_t)(oi + r) * f.W + (oj + c)] = make_float4(src[idx], src[P + idx], src[2 * P + idx], rn1);
+    }
+    SF_PROF();  // 5: fusion + store
+    SF_PROF_PRINT("upd");
+    const unsigned any = __reduce_or_sync(FULL, fl);
+    if ((tid & 31) == 0 && any) atomicOr(a.flags, any);
+}
+
+// Tile shapes tried by the launcher (TW a multiple of 4).
+struct TileOpt {
+    int TW, TH;
+};
+constexpr TileOpt kTiles[] = {{64, 48}, {48, 40}, {32, 32}, {32, 16}, {16, 16}};
+
+bool plan_tiles(const FrameParams& f, int h, UpdArgs& a, size_t& smem) {
+    int sms = 148;
+    {
+        int dev = 0;
+        if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const int MR = h + 2, MG = (h + 6) & ~3;  // MG >= h + 3, a multiple of 4
+    long long best = -1;
+    for (const TileOpt& t : kTiles) {
+        const int PW = t.TW + 2 * MG, PH = t.TH + 2 * MR, P = (PW * PH + 31) & ~31;  // 128-byte aligned planes
+        const size_t bytes = sizeof(float) * 10 * (size_t)P + 64;
+        if (bytes > 227 * 1024) continue;
+        const long long tiles = (long long)((f.W + t.TW - 1) / t.TW) * ((f.H + t.TH - 1) / t.TH) * f.B;
+        const long long waves = (tiles + sms - 1) / sms;
+        const long long cost = waves * (long long)(t.TW + 2 * h + 4) * (t.TH + 2 * h + 4);  // plane work per SM
+        if (best < 0 || cost < best) {
+            best = cost;
+            a.TW = t.TW;
+            a.TH = t.TH;
+            a.MR = MR;
+            a.MG = MG;
+            a.PW = PW;
+            a.PH = PH;
+            a.P = P;
+            smem = bytes;
+        }
+    }
+    return best >= 0;
+}
+
+}  // namespace
+
+// Supported when the box halo fits the planes (S <= 8).
+bool sf_update_fused_supported(const sf_ctx* c) {
+    if (c->fp.S > 8) return false;
+    UpdArgs a;
+    size_t smem = 0;
+    if (!plan_tiles(c->fp, 2 * c->fp.S, a, smem)) return false;
+    return cudaFuncSetAttribute(k_upd, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) == cudaSuccess;
+}
+
+// One update: pred (w^{k+}, rho^{k+}) + references + (Y, depth) -> out (state k+1), yout.
+cudaError_t sf_launch_update_fused(sf_ctx* c, const float* Y, const float* D, const float4* pred, const float* rref,
+                                   int rs, const float* yref, int ys, float4* out, float* yout) {
+    const FrameParams& f = c->fp;
+    UpdArgs a;
+    size_t smem = 0;
+    a.h = 2 * f.S;
+    if (!plan_tiles(f, a.h, a, smem)) return cudaErrorInvalidConfiguration;
+    a.tma = sf_tma_encode3d(&a.tmY, Y, f.W, f.H, f.B, a.PW, a.PH, 1) &&
+            sf_tma_encode3d(&a.tmD, D, f.W, f.H, f.B, a.PW, a.PH, 1);
+    a.pred = pred;
+    a.rref = rref;
+    a.rs = rs;
+    a.yref = yref;
+    a.ys = ys;
+    a.Y = Y;
+    a.D = D;
+    a.G0 = c->G0;
+    a.G1 = c->G1;
+    a.G2 = c->G2;
+    a.out = out;
+    a.yout = yout;
+    a.flags = c->flags;
+    a.f = f;
+    {
+        static const int dbg_env = [] {
+            const char* e = getenv("SF_DEBUG_SKIP");
+            return e ? atoi(e) : 0;
+        }();
+        a.dbg = dbg_env;
+    }
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3((f.W + a.TW - 1) / a.TW, (f.H + a.TH - 1) / a.TH, f.B);
+    lc.blockDim = dim3(UPD_NT);
+    lc.dynamicSmemBytes = smem;
+    lc.stream = c->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL behind the transport kernel
+    at[0].val.programmaticStreamSerializationAllowed = sf_pdl_enabled() ? 1 : 0;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&lc, k_upd, a);
+    if (e == cudaSuccess) e = cudaGetLastError();
+    return e;
+}

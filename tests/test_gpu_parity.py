@@ -298,11 +298,12 @@ def test_config4_batch64_full_size():
 
 @pytest.mark.parametrize("H,W,N,S,B", [(97, 131, 3, 2, 1), (150, 61, 8, 2, 2), (200, 170, 11, 1, 1),
                                        (64, 300, 5, 0, 1), (33, 33, 1, 3, 3), (72, 64, 8, 2, 1),
-                                       (300, 257, 17, 2, 1), (5, 7, 2, 2, 2)])
-def test_fused_equals_passes_random_states(H, W, N, S, B):
-    """The fused, temporally blocked kernel (tiles + halos, 1 launch per 8 substeps) gives the
-    per-pass kernels' bits on random states over ragged grids, batches and substep counts
-    (tile edges, grid edges, partial tiles, N > 8 multi-launch, S = 0), 3 frames each."""
+                                       (300, 257, 17, 2, 1), (5, 7, 2, 2, 2), (130, 190, 4, 4, 1)])
+def test_random_states_vs_oracle(H, W, N, S, B):
+    """Both GPU paths -- the tiled kernels (transport tiles + halos, 1 launch per 8 substeps, the
+    update tiles) and the per-pass kernels -- against the float32 ORACLE, element by element, on
+    random states over ragged grids, batches and substep counts (tile edges, grid edges, partial
+    tiles, N > 8 multi-launch, S = 0 .. 4), every one of 3 frames; flags equal."""
     sf = _sf()
     g = grid.gnomonic(H, W, 80.0)
     rng = np.random.default_rng(H * 7 + W)
@@ -314,36 +315,63 @@ def test_fused_equals_passes_random_states(H, W, N, S, B):
     Ys = rng.uniform(0.1, 0.9, (3, B, H, W)).astype(np.float32)
     Ds = rng.uniform(1.0, 9.0, (3, B, H, W)).astype(np.float32)
     Ds[:, :, ::7, ::5] = np.nan
+    os_ = [oracle.Oracle(g, p, "f32") for _ in range(B)]
+    for b, o in enumerate(os_):
+        o.set_state(w[b], rho[b], yh[b])
     ms = {}
     for kern in ("passes", "fused"):
         m = sf.StructureFlow(g, p, batch=B, kernel=_kernel_id(kern))
         assert m.kernel == _kernel_id(kern)
         m.set_fields(_dev(w), _dev(rho), _dev(yh))
-        for k in range(3):
-            m.step(_dev(Ys[k]), _dev(Ds[k]))
         ms[kern] = m
-    a, b = _fields(ms["passes"]), _fields(ms["fused"])
-    for name, x, y in zip(("w", "rho", "yhat"), a, b):
-        assert_parity(y, x, name)
-    assert sf.sf_status_flags(ms["passes"].ctx)[1] == sf.sf_status_flags(ms["fused"].ctx)[1]
+    for k in range(3):
+        for b, o in enumerate(os_):
+            o.step(Ys[k][b], Ds[k][b])
+        for kern, m in ms.items():
+            m.step(_dev(Ys[k]), _dev(Ds[k]))
+            got = _fields(m)
+            for b, o in enumerate(os_):
+                for name, x, y in zip(("w", "rho", "yhat"), got, (o.w, o.rho, o.yhat)):
+                    assert_parity(x[b], y, f"{kern} {name}[{b}] frame {k}")
+    want = 0
+    for o in os_:
+        want |= o.flags
+    for kern, m in ms.items():
+        assert sf.sf_status_flags(m.ctx)[1] == want, kern
 
 
-def test_fused_equals_passes_on_bench_ring():
-    """The bench workload (configs[1] scene, frames replayed from a ring with a wrap-around
-    jump back to frame 0): fused and per-pass kernels stay bit-identical, flags included."""
+def test_bench_ring_vs_oracle():
+    """The bench workload (configs[1] scene, frames replayed from a ring with a wrap-around jump
+    back to frame 0), 40 steps: both GPU paths equal the float32 oracle every 4 steps, flags
+    included."""
     sf = _sf()
     seq = sfgen.config_sequence(2, frames=16)
     ms = {k: sf.StructureFlow(seq.geom, seq.params, kernel=_kernel_id(k)) for k in ("passes", "fused")}
+    o = oracle.Oracle(seq.geom, seq.params, "f32")
     Yd = [_dev(y) for y in seq.Y]
     Dd = [_dev(d) for d in seq.depth]
     for i in range(40):
         for m in ms.values():
             m.step(Yd[i % 16], Dd[i % 16])
-        if i % 8 == 7:
-            a, b = _fields(ms["passes"]), _fields(ms["fused"])
-            for name, x, y in zip(("w", "rho", "yhat"), a, b):
-                assert_parity(y, x, f"{name} step {i}")
-            assert sf.sf_status_flags(ms["passes"].ctx)[1] == sf.sf_status_flags(ms["fused"].ctx)[1], i
+        o.step(seq.Y[i % 16], seq.depth[i % 16])
+        if i % 4 == 3:
+            for kern, m in ms.items():
+                for name, x, y in zip(("w", "rho", "yhat"), _fields(m), (o.w, o.rho, o.yhat)):
+                    assert_parity(x[0], y, f"{kern} {name} step {i}")
+                assert sf.sf_status_flags(m.ctx)[1] == o.flags, (kern, i)
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_config2_clamp_active_100_frames(kernel):
+    """configs[1] at full size with max_flow = 1.5 px (N = 2) against the scene's flows of up to
+    ~2.1 px/frame: the advection clamp (reading 12) engages (from frame 3).  Every one of 100 frames bitwise
+    against the float32 oracle; the sticky flags are non-zero (CLAMPED) and equal."""
+    sf = _sf()
+    seq = sfgen.config_sequence(2, frames=100)
+    p = seq.params
+    p4 = Params(max_flow=1.5, gamma=p.gamma, smooth_iters=p.smooth_iters)
+    m, o = run_pair(seq, 100, kernel, params=p4, check_every=1, tol_final=1e-3)
+    assert o.flags & sf.SF_FLAG_CLAMPED, o.flags
 
 
 @pytest.mark.parametrize("kernel", KERNELS)

@@ -1,0 +1,12 @@
+# Transport variants: GPU suite on the default, then per-variant phase profiles and benches.
+set -x
+SF_BUILD_DEBUG=1 python -c "import __graft_entry__ as g; g.build()" 2>&1 | tail -1
+for cfg in 0 1 2; do
+  SF_TRANS_CFG=$cfg SF_DEBUG_SKIP=8192 timeout 300 python tools/ktime.py --frames 12 --ring 8 2>&1 | grep SFPROF | tail -4
+done
+python -c "import __graft_entry__ as g; g.build(); g.smoke()" 2>&1 | tail -1
+for cfg in 0 1 2; do
+  SF_TRANS_CFG=$cfg timeout 300 python bench.py --steps 2000 --warmup 20 --no-cpu-baseline 2>&1 | tail -1 > gpurun_out/bench_t$cfg.json
+  python -c "import json; d=json.load(open('gpurun_out/bench_t$cfg.json')); print('BENCH cfg $cfg', d['value'], d['ms_per_step']*1e3)"
+done
+timeout 1200 python -m pytest tests -m gpu -q -x 2>&1 | tail -4
