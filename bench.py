@@ -425,6 +425,23 @@ def run_sf(args):
     total_ms = float(t.item())
     st, flags = sf.sf_status_flags(m.ctx)
 
+    # ---- per-kernel durations (fused H = 1): frames through sf_step_timed, CUDA events on the context
+    # stream between the transport (k_trans) and the update (k_upd); the roofline's dominant kernel
+    ktimes = None
+    if m.kernel == sf.SF_KERNEL_FUSED and levels == 1 and cam is None:
+        tp, tu = [], []
+        with torch.cuda.stream(s):
+            for i in range(max(20, min(args.steps, 200))):
+                k = frame_of(state["i"])
+                state["i"] += 1
+                a_ms, b_ms = sf.sf_step_timed(m.ctx, Yd[k].data_ptr(), Dd[k].data_ptr())
+                if i >= 5:
+                    tp.append(a_ms)
+                    tu.append(b_ms)
+        ktimes = {"k_trans_ms": statistics.mean(tp), "k_upd_ms": statistics.mean(tu), "frames": len(tp),
+                  "note": "sf_step_timed: CUDA events around each kernel on the context stream (no "
+                          "programmatic-launch overlap across the events), after the timed region"}
+
     # ---- end to end through the host-buffer C-ABI call (pinned host memory), same metric
     e2e_steps = max(3, min(args.steps, 400))
     Yp = torch.empty((ring, B, H, W), dtype=torch.float32, pin_memory=True)
@@ -476,19 +493,41 @@ def run_sf(args):
         sm_max = pk.get("sm_max_mhz", 1965.0)
         alu_peak = SMS * FP32_LANES_PER_SM * sm_max * 1e6 / 1e12  # TFLOP/s-equivalent FP32 lane-ops
         alu = ops / (mean_ms / 1e3) / 1e12
-        kname = "k_fused" if m.kernel == sf.SF_KERNEL_FUSED else "whole step (2N+1+S per-pass kernels)"
-        if levels == 2:
-            kname = "whole step (top level fused + bottom-level pass kernels)"
-        tr = ncu_traffic() if (m.kernel == sf.SF_KERNEL_FUSED and levels == 1) else None
-        roof = {"bound": "alu", "achieved": alu, "peak": alu_peak, "unit": "TFLOP/s", "frac": alu / alu_peak,
-                "traffic": tr["bytes_per_launch"] if tr else None,
-                "traffic_source": (tr["source"] + " (ncu --set full, cache-flushed replay)") if tr else None,
-                "kernel": kname, "launches_per_step": launches,
-                "algo_ops_per_launch": ops / max(1, launches),
-                "peak_source": f"148 SMs x 128 FP32 lanes x {sm_max:.0f} MHz (DESIGN.md section 8)",
-                "hbm_view": {"achieved_gbs": gbs, "peak_gbs": hbm_peak, "frac": gbs / hbm_peak,
-                             "algo_bytes_per_step": algo_bytes,
-                             "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in pk else "fallback"}}
+        step_view = {"achieved": alu, "frac": alu / alu_peak, "ops_per_step": ops,
+                     "note": "all algorithmic FP32 ops of the step / the device-timed step"}
+        if ktimes:
+            # dominant kernel: the transport (2N passes x 26 ops/px) over its
+            # event-timed duration; the update kernel's view beside it
+            t_ops = 26 * 2 * params.N * B * H * W
+            u_ops = (109 + 27 * params.smooth_iters) * B * H * W
+            t_alu = t_ops / (ktimes["k_trans_ms"] / 1e3) / 1e12
+            u_alu = u_ops / (ktimes["k_upd_ms"] / 1e3) / 1e12
+            tr = ncu_traffic("k_trans")
+            roof = {"bound": "alu", "achieved": t_alu, "peak": alu_peak, "unit": "TFLOP/s", "frac": t_alu / alu_peak,
+                    "traffic": tr["bytes_per_launch"] if tr else None,
+                    "traffic_source": (tr["source"] + " (ncu --set full, cache-flushed replay)") if tr else None,
+                    "kernel": "k_trans", "launches_per_step": (params.N + 7) // 8,
+                    "algo_ops_per_launch": t_ops / ((params.N + 7) // 8),
+                    "kernel_ms": ktimes["k_trans_ms"], "kernel_times": ktimes,
+                    "peak_source": f"148 SMs x 128 FP32 lanes x {sm_max:.0f} MHz (DESIGN.md section 8)",
+                    "update_kernel": {"kernel": "k_upd", "achieved": u_alu, "frac": u_alu / alu_peak,
+                                      "ops_per_launch": u_ops, "kernel_ms": ktimes["k_upd_ms"]},
+                    "step_view": step_view,
+                    "hbm_view": {"achieved_gbs": gbs, "peak_gbs": hbm_peak, "frac": gbs / hbm_peak,
+                                 "algo_bytes_per_step": algo_bytes,
+                                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in pk else "fallback"}}
+        else:
+            kname = "whole step (2N+1+S per-pass kernels)" if m.kernel != sf.SF_KERNEL_FUSED else "whole step"
+            if levels == 2:
+                kname = "whole step (top level fused + bottom-level kernels)"
+            roof = {"bound": "alu", "achieved": alu, "peak": alu_peak, "unit": "TFLOP/s", "frac": alu / alu_peak,
+                    "traffic": None, "traffic_source": None, "kernel": kname, "launches_per_step": launches,
+                    "algo_ops_per_launch": ops / max(1, launches),
+                    "peak_source": f"148 SMs x 128 FP32 lanes x {sm_max:.0f} MHz (DESIGN.md section 8)",
+                    "step_view": step_view,
+                    "hbm_view": {"achieved_gbs": gbs, "peak_gbs": hbm_peak, "frac": gbs / hbm_peak,
+                                 "algo_bytes_per_step": algo_bytes,
+                                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in pk else "fallback"}}
         out = {"metric": METRIC, "value": value, "unit": "Hz", "n_gpus": world, "steps": args.steps,
                "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
                "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",

@@ -240,6 +240,33 @@ sf_status sf_halo_exchange_peer(sf_ctx* ctx, const sf_ctx* up, const sf_ctx* dow
  * sf_nccl_comm_init (or any communicator of the same NCCL library).  Errors: SF_E_NCCL. */
 sf_status sf_halo_exchange_nccl(sf_ctx* ctx, void* nccl_comm, int32_t rank, int32_t nranks);
 
+/* ---- per-substep banded exchange (the north star's banded split) --------
+ * A band context created with band_own_begin / band_own_end and 2 halo rows on every cut side
+ * (sf_band_partition(..., sf_band_halo_substep(cfg), ...)) runs a frame with the halo rows
+ * refreshed at each point that reads across a row boundary: after every column pass (1 row of
+ * (w*, rho*), before the row pass) and before every box pass (2 rows of w) --
+ * N + S exchanges per frame instead of sf_halo_exchange_*'s one deep exchange.  Transport and box
+ * run on the per-pass kernels; Y / depth cover the band's rows (halo included).  The owned rows
+ * equal a whole-grid context's bit for bit.
+ * The transport is the caller's: xfer(user, send_up, recv_up, send_down, recv_down, n_up, n_down)
+ * is called once per batch member at every exchange point; send_* point at the rows to send to the
+ * neighbour above / below, recv_* at the rows to fill from it (n_* floats each; NULL / 0 where
+ * the band has no neighbour on that side).  host_staged = 1: the pointers are pinned host memory
+ * (libsf copies the rows out before and in after the call, synchronously); 0: device pointers
+ * into the context's buffers, the callee enqueues the transfer in the context stream's order.
+ * xfer returns 0 on success.  Errors: SF_E_DATA, SF_E_STATE, SF_E_CONFIG (halo rows missing or a
+ * band thinner than 4 rows), SF_E_UNSUPPORTED (pyramid), SF_E_NCCL (xfer failed), SF_E_CUDA. */
+typedef int32_t (*sf_halo_xfer_fn)(void* user, const float* send_up, float* recv_up, const float* send_down,
+                                   float* recv_down, size_t n_up, size_t n_down);
+int32_t sf_band_halo_substep(const sf_config* cfg);
+sf_status sf_step_banded(sf_ctx* ctx, const float* Y_dev, const float* depth_dev, sf_halo_xfer_fn xfer, void* user,
+                         int32_t host_staged);
+/* The same over NCCL (band index == rank): every exchange is an ncclGroup of ncclSend / ncclRecv
+ * with ranks rank - 1 and rank + 1; the row pass's inner rows run while the transport exchange is
+ * in flight on a side stream (interior first), the rows next to the cut edges after it. */
+sf_status sf_step_banded_nccl(sf_ctx* ctx, const float* Y_dev, const float* depth_dev, void* nccl_comm, int32_t rank,
+                              int32_t nranks);
+
 /* NCCL plumbing (libnccl.so.2 is loaded at first use): rank 0 makes a 128-byte unique id, the
  * caller broadcasts it (e.g. torch.distributed), every rank creates its communicator. */
 sf_status sf_nccl_unique_id(char id[128]);
@@ -251,6 +278,16 @@ int32_t sf_kernel_in_use(const sf_ctx* ctx);
 
 /* Number of kernel launches one sf_step issues (for the bench's gpu_launches count). */
 int32_t sf_launches_per_step(const sf_ctx* ctx);
+
+/* Per-kernel timing of one frame (measurement hook): sf_step's kernels on
+ * the context stream with CUDA events between the prediction (the k_trans launches) and the
+ * update (k_upd): *ms_predict / *ms_update receive the two durations in milliseconds (the event
+ * between them also removes the programmatic-launch overlap of the two kernels; a short device
+ * spin queued first keeps host launch latency out of the timings).  Y / depth as in
+ * sf_step.  Synchronises the stream.  Fused H = 1 contexts with a pending-free, initialised state
+ * only; errors: SF_E_DATA (null pointer), SF_E_STATE, SF_E_UNSUPPORTED (passes kernels, pyramid),
+ * SF_E_CUDA. */
+sf_status sf_step_timed(sf_ctx* ctx, const float* Y_dev, const float* depth_dev, float* ms_predict, float* ms_update);
 
 /* Static description of a status code. */
 const char* sf_error_string(sf_status s);

@@ -26,7 +26,7 @@ EXPORTS = ("sf_config_default", "sf_create", "sf_destroy", "sf_predict", "sf_upd
            "sf_get_fields", "sf_set_fields", "sf_status_flags", "sf_kernel_in_use", "sf_launches_per_step",
            "sf_error_string", "sf_band_halo", "sf_band_partition", "sf_halo_exchange_peer", "sf_halo_exchange_nccl",
            "sf_nccl_unique_id", "sf_nccl_comm_init", "sf_nccl_comm_destroy", "sf_flow_px", "sf_eval", "sf_map_inputs", "sf_set_motion", "sf_step_host_async", "sf_wait",
-           "sf_step_camera")
+           "sf_step_camera", "sf_step_timed", "sf_band_halo_substep", "sf_step_banded", "sf_step_banded_nccl")
 
 
 class sf_config(C.Structure):
@@ -43,6 +43,11 @@ class SFError(RuntimeError):
     def __init__(self, status: int, where: str):
         super().__init__(f"{where}: {sf_error_string(status)} (status {status})")
         self.status = status
+
+
+# sf_halo_xfer_fn (include/sf.h): (user, send_up, recv_up, send_down, recv_down, n_up, n_down) -> 0
+HALO_XFER_FN = C.CFUNCTYPE(C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t,
+                           C.c_size_t)
 
 
 def _load():
@@ -83,11 +88,15 @@ def _load():
     lib.sf_step_host_async.argtypes = [P, P, P, P, P]
     lib.sf_wait.argtypes = [P]
     lib.sf_step_camera.argtypes = [P, P, P, C.c_int32, C.c_int32, P, P]
+    lib.sf_step_timed.argtypes = [P, P, P, C.POINTER(C.c_float), C.POINTER(C.c_float)]
+    lib.sf_band_halo_substep.argtypes = [C.POINTER(sf_config)]
+    lib.sf_step_banded.argtypes = [P, P, P, HALO_XFER_FN, P, C.c_int32]
+    lib.sf_step_banded_nccl.argtypes = [P, P, P, P, C.c_int32, C.c_int32]
     for name in ("sf_create", "sf_predict", "sf_update", "sf_step", "sf_step_host", "sf_get_fields",
                  "sf_set_fields", "sf_status_flags", "sf_kernel_in_use", "sf_launches_per_step", "sf_band_halo",
                  "sf_band_partition", "sf_halo_exchange_peer", "sf_halo_exchange_nccl", "sf_nccl_unique_id",
                  "sf_nccl_comm_init", "sf_flow_px", "sf_eval", "sf_map_inputs", "sf_set_motion", "sf_step_host_async", "sf_wait",
-           "sf_step_camera"):
+           "sf_step_camera", "sf_step_timed", "sf_band_halo_substep", "sf_step_banded", "sf_step_banded_nccl"):
         getattr(lib, name).restype = C.c_int
     return lib
 
@@ -208,6 +217,41 @@ def sf_kernel_in_use(ctx: int) -> int:
 
 def sf_launches_per_step(ctx: int) -> int:
     return _lib.sf_launches_per_step(C.c_void_p(ctx))
+
+
+def sf_band_halo_substep(cfg) -> int:
+    return _lib.sf_band_halo_substep(C.byref(cfg))
+
+
+def sf_step_banded(ctx: int, Y_ptr: int, D_ptr: int, xfer, host_staged: int = 1) -> None:
+    """One frame of a band context with the per-substep halo exchange through the caller's
+    transport `xfer(send_up, recv_up, send_down, recv_down, n_up, n_down)` (addresses as ints,
+    None where there is no neighbour; host pointers when host_staged)."""
+    def _cb(user, su, ru, sd, rd, nu, nd):
+        try:
+            xfer(su, ru, sd, rd, nu, nd)
+            return 0
+        except Exception:  # reported as SF_E_NCCL by the library
+            import traceback
+            traceback.print_exc()
+            return 1
+    fn = HALO_XFER_FN(_cb)
+    _check(_lib.sf_step_banded(C.c_void_p(ctx), C.c_void_p(Y_ptr), C.c_void_p(D_ptr), fn, None, int(host_staged)),
+           "sf_step_banded")
+
+
+def sf_step_banded_nccl(ctx: int, Y_ptr: int, D_ptr: int, comm: int, rank: int, nranks: int) -> None:
+    _check(_lib.sf_step_banded_nccl(C.c_void_p(ctx), C.c_void_p(Y_ptr), C.c_void_p(D_ptr), C.c_void_p(comm),
+                                    int(rank), int(nranks)), "sf_step_banded_nccl")
+
+
+def sf_step_timed(ctx: int, Y_ptr: int, D_ptr: int):
+    """One fused frame with CUDA events between its prediction and update kernels (sf.h):
+    returns (ms_predict, ms_update)."""
+    a, b = C.c_float(), C.c_float()
+    _check(_lib.sf_step_timed(C.c_void_p(ctx), C.c_void_p(Y_ptr), C.c_void_p(D_ptr), C.byref(a), C.byref(b)),
+           "sf_step_timed")
+    return a.value, b.value
 
 
 def sf_band_halo(cfg: sf_config) -> int:

@@ -56,7 +56,7 @@ static void async_teardown(sf_ctx* c);
 
 static void free_ctx(sf_ctx* c) {
     if (!c) return;
-    void* ptrs[] = {c->G0, c->G1, c->G2, c->E, c->state[0], c->state[1], c->pred, c->tmp, c->tmp2,
+    void* ptrs[] = {c->G0, c->G1, c->G2, c->GS, c->E, c->state[0], c->state[1], c->pred, c->tmp, c->tmp2,
                     c->yhat[0], c->yhat[1], c->HG, c->HH, c->flags, c->hY, c->hD, c->hw, c->hr, c->eval_part,
                     c->Wf[0], c->Wf[1], c->Wpred, c->Wtmp, c->Y2, c->D2, c->mY, c->mD};
     for (void* p : ptrs)
@@ -67,6 +67,13 @@ static void free_ctx(sf_ctx* c) {
     }
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);
     if (c->ev_join) cudaEventDestroy(c->ev_join);
+    if (c->xstream) {
+        cudaStreamSynchronize(c->xstream);
+        cudaStreamDestroy(c->xstream);
+    }
+    if (c->xev[0]) cudaEventDestroy(c->xev[0]);
+    if (c->xev[1]) cudaEventDestroy(c->xev[1]);
+    if (c->xhost) cudaFreeHost(c->xhost);
     if (c->async_ready) {
         cudaStreamSynchronize(c->s_in);
         cudaStreamSynchronize(c->s_out);
@@ -174,6 +181,7 @@ extern "C" sf_status sf_create(const sf_config* cfg, const float* geometry, sf_c
     bool ok = cudaMalloc(&c->G0, npix * sizeof(float4)) == cudaSuccess &&
               cudaMalloc(&c->G1, npix * sizeof(float4)) == cudaSuccess &&
               cudaMalloc(&c->G2, npix * sizeof(float4)) == cudaSuccess &&
+              cudaMalloc(&c->GS, 3 * npix * sizeof(float4)) == cudaSuccess &&
               cudaMalloc(&c->E, 6 * (size_t)sf_ew(f.W) * sf_eh(f.H) * sizeof(float)) == cudaSuccess &&
               cudaMalloc(&c->state[0], nall * sizeof(float4)) == cudaSuccess &&
               cudaMalloc(&c->state[1], nall * sizeof(float4)) == cudaSuccess &&
@@ -325,6 +333,34 @@ extern "C" sf_status sf_step(sf_ctx* c, const float* Y, const float* D) {
     sf_status st = sf_predict(c);
     if (st != SF_OK) return st;
     return sf_update(c, Y, D);
+}
+
+extern "C" sf_status sf_step_timed(sf_ctx* c, const float* Y, const float* D, float* ms_predict, float* ms_update) {
+    SF_NVTX("sf_step_timed");
+    if (!c || !Y || !D || !ms_predict || !ms_update) return SF_E_DATA;
+    SF_DEVICE_GUARD(c);
+    if (c->levels == 2 || c->kernel != SF_KERNEL_FUSED) return SF_E_UNSUPPORTED;
+    if (!c->initialized || c->pending) return SF_E_STATE;
+    cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+    sf_status st = SF_OK;
+    for (int i = 0; i < 3 && st == SF_OK; ++i)
+        if (cudaEventCreate(&ev[i]) != cudaSuccess) st = SF_E_CUDA;
+    // (a 100 us device spin first: the launches below are queued before the GPU reaches them, so the
+    // events time the kernels and not the host's launch latency)
+    if (st == SF_OK &&
+        (sf_launch_spin(c, 100000) != cudaSuccess || cudaEventRecord(ev[0], c->stream) != cudaSuccess ||
+         sf_launch_predict_fused(c, Y, D) != cudaSuccess ||
+         cudaEventRecord(ev[1], c->stream) != cudaSuccess ||
+         sf_launch_update_fused(c, Y, D, c->pred, reinterpret_cast<const float*>(c->state[c->cur]) + 3, 4,
+                                c->yhat[c->cur], 1, c->state[1 - c->cur], c->yhat[1 - c->cur]) != cudaSuccess ||
+         cudaEventRecord(ev[2], c->stream) != cudaSuccess || cudaEventSynchronize(ev[2]) != cudaSuccess ||
+         cudaEventElapsedTime(ms_predict, ev[0], ev[1]) != cudaSuccess ||
+         cudaEventElapsedTime(ms_update, ev[1], ev[2]) != cudaSuccess))
+        st = SF_E_CUDA;
+    if (st == SF_OK) c->cur = 1 - c->cur;
+    for (int i = 0; i < 3; ++i)
+        if (ev[i]) cudaEventDestroy(ev[i]);
+    return st;
 }
 
 extern "C" sf_status sf_step_host(sf_ctx* c, const float* Yh, const float* Dh, float* wh, float* rh) {

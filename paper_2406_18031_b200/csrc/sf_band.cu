@@ -161,3 +161,161 @@ extern "C" sf_status sf_halo_exchange_nccl(sf_ctx* c, void* comm, int32_t rank, 
     }
     return n.GroupEnd() == 0 ? SF_OK : SF_E_NCCL;
 }
+
+// ------------------------------------------------------------------ per-substep exchange
+// The north star's banded split: a band context holds its owned rows plus 2 halo rows on each
+// cut side, and the halo rows are refreshed at every point of the frame that reads across a row
+// boundary -- after each column pass (1 row of (w*, rho*): the row pass reads i +- 1)
+// and before each box pass (2 rows of w: the 5x5 box reads i +- 2).  The transport and
+// the box run on the per-pass kernels over the owned rows (transport) / the band (box); the
+// update's models read the band's own inputs (Y, depth cover the band and its halo rows).
+extern "C" int32_t sf_band_halo_substep(const sf_config* cfg) {
+    (void)cfg;
+    return 2;
+}
+
+namespace {
+// One exchange point: rows of the float4 plane `buf` ([B][H][W], local rows) -- send own rows
+// [lo, lo + r) up and [hi - r, hi) down, receive [lo - r, lo) from up and [hi, hi + r) from down.
+sf_status exchange_rows(sf_ctx* c, float4* buf, int r, sf_halo_xfer_fn xfer, void* user, int host_staged,
+                        cudaStream_t s) {
+    const FrameParams& f = c->fp;
+    const size_t W = (size_t)f.W;
+    const int lo = c->own_begin - c->ext_begin, hi = c->own_end - c->ext_begin;
+    const bool up = lo > 0, dn = hi < f.H;
+    const size_t n = (size_t)r * W * 4;  // floats per segment
+    for (int b = 0; b < f.B; ++b) {
+        float4* base = buf + (size_t)b * f.H * W;
+        float* su = up ? reinterpret_cast<float*>(base + lo * W) : nullptr;
+        float* ru = up ? reinterpret_cast<float*>(base + (lo - r) * W) : nullptr;
+        float* sd = dn ? reinterpret_cast<float*>(base + (hi - r) * W) : nullptr;
+        float* rd = dn ? reinterpret_cast<float*>(base + hi * W) : nullptr;
+        if (!host_staged) {
+            if (xfer(user, su, ru, sd, rd, up ? n : 0, dn ? n : 0) != 0) return SF_E_NCCL;
+            continue;
+        }
+        float* h = c->xhost;  // [send_up | recv_up | send_dn | recv_dn], n floats each
+        if (up && cudaMemcpyAsync(h, su, n * sizeof(float), cudaMemcpyDeviceToHost, s) != cudaSuccess) return SF_E_CUDA;
+        if (dn && cudaMemcpyAsync(h + 2 * n, sd, n * sizeof(float), cudaMemcpyDeviceToHost, s) != cudaSuccess)
+            return SF_E_CUDA;
+        if (cudaStreamSynchronize(s) != cudaSuccess) return SF_E_CUDA;
+        if (xfer(user, up ? h : nullptr, up ? h + n : nullptr, dn ? h + 2 * n : nullptr, dn ? h + 3 * n : nullptr,
+                 up ? n : 0, dn ? n : 0) != 0)
+            return SF_E_NCCL;
+        if (up && cudaMemcpyAsync(ru, h + n, n * sizeof(float), cudaMemcpyHostToDevice, s) != cudaSuccess) return SF_E_CUDA;
+        if (dn && cudaMemcpyAsync(rd, h + 3 * n, n * sizeof(float), cudaMemcpyHostToDevice, s) != cudaSuccess)
+            return SF_E_CUDA;
+        if (cudaStreamSynchronize(s) != cudaSuccess) return SF_E_CUDA;  // the staging is reused next call
+    }
+    return SF_OK;
+}
+
+struct NcclXfer {
+    void* comm;
+    int rank;
+    cudaStream_t stream;
+};
+int32_t nccl_xfer(void* u, const float* su, float* ru, const float* sd, float* rd, size_t nu, size_t nd) {
+    NcclXfer* x = static_cast<NcclXfer*>(u);
+    NcclApi& n = nccl();
+    if (n.GroupStart() != 0) return 1;
+    if (su) {
+        n.Send(su, nu, kNcclFloat32, x->rank - 1, x->comm, x->stream);
+        n.Recv(ru, nu, kNcclFloat32, x->rank - 1, x->comm, x->stream);
+    }
+    if (sd) {
+        n.Send(sd, nd, kNcclFloat32, x->rank + 1, x->comm, x->stream);
+        n.Recv(rd, nd, kNcclFloat32, x->rank + 1, x->comm, x->stream);
+    }
+    return n.GroupEnd() == 0 ? 0 : 1;
+}
+
+sf_status banded_step(sf_ctx* c, const float* Y, const float* D, sf_halo_xfer_fn xfer, void* user, int host_staged,
+                      NcclXfer* nx) {
+    const FrameParams& f = c->fp;
+    const int lo = c->own_begin - c->ext_begin, hi = c->own_end - c->ext_begin;
+    if ((lo > 0 && lo < 2) || (hi < f.H && f.H - hi < 2) || hi - lo < 4) return SF_E_CONFIG;
+    if (host_staged && !c->xhost) {
+        if (cudaMallocHost(&c->xhost, 4 * 2 * (size_t)f.W * 4 * sizeof(float)) != cudaSuccess) {
+            c->xhost = nullptr;
+            return SF_E_CUDA;
+        }
+    }
+    const bool overlap = nx != nullptr;  // device transport: the row pass's inner rows overlap the exchange
+    if (overlap && !c->xstream) {
+        cudaStream_t s = nullptr;
+        cudaEvent_t e0 = nullptr, e1 = nullptr;
+        if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&e0, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&e1, cudaEventDisableTiming) != cudaSuccess) {
+            if (s) cudaStreamDestroy(s);
+            if (e0) cudaEventDestroy(e0);
+            if (e1) cudaEventDestroy(e1);
+            return SF_E_CUDA;
+        }
+        c->xstream = s;
+        c->xev[0] = e0;
+        c->xev[1] = e1;
+    }
+    if (nx) nx->stream = c->xstream;
+    // ---- prediction: N x (column pass, exchange 1 row, row pass), owned rows only
+    const float4* src = c->state[c->cur];
+    for (int n = 0; n < f.N; ++n) {
+        SF_TRY(sf_launch_pass(c, 0, src, c->tmp, lo, hi, c->stream));
+        if (overlap) {
+            SF_TRY(cudaEventRecord(c->xev[0], c->stream));
+            SF_TRY(cudaStreamWaitEvent(c->xstream, c->xev[0], 0));
+            const sf_status st = exchange_rows(c, c->tmp, 1, xfer, user, 0, c->xstream);
+            if (st != SF_OK) return st;
+            SF_TRY(cudaEventRecord(c->xev[1], c->xstream));
+            SF_TRY(sf_launch_pass(c, 1, c->tmp, c->pred, lo + 1, hi - 1, c->stream));  // rows with no halo read
+            SF_TRY(cudaStreamWaitEvent(c->stream, c->xev[1], 0));
+            SF_TRY(sf_launch_pass(c, 1, c->tmp, c->pred, lo, lo + 1, c->stream));
+            SF_TRY(sf_launch_pass(c, 1, c->tmp, c->pred, hi - 1, hi, c->stream));
+        } else {
+            const sf_status st = exchange_rows(c, c->tmp, 1, xfer, user, host_staged, c->stream);
+            if (st != SF_OK) return st;
+            SF_TRY(sf_launch_pass(c, 1, c->tmp, c->pred, lo, hi, c->stream));
+        }
+        src = c->pred;
+    }
+    // ---- update: models + LS + fusion over the band, then S x (exchange 2 rows, box pass)
+    float4* nxt = c->state[1 - c->cur];
+    float4* solved = f.S > 0 ? c->tmp : nxt;
+    SF_TRY(sf_launch_update_solve(c, Y, D, solved));
+    for (int s = 0; s < f.S; ++s) {
+        float4* in = (s & 1) ? c->tmp2 : c->tmp;
+        float4* out = s == f.S - 1 ? nxt : ((s & 1) ? c->tmp : c->tmp2);
+        if (nx) nx->stream = c->stream;
+        const sf_status st = exchange_rows(c, in, 2, xfer, user, host_staged, c->stream);
+        if (st != SF_OK) return st;
+        SF_TRY(sf_launch_box(c, in, out));
+    }
+    c->cur = 1 - c->cur;
+    return SF_OK;
+}
+}  // namespace
+
+extern "C" sf_status sf_step_banded(sf_ctx* c, const float* Y, const float* D, sf_halo_xfer_fn xfer, void* user,
+                                    int32_t host_staged) {
+    SF_NVTX("sf_step_banded");
+    if (!c || !Y || !D || !xfer) return SF_E_DATA;
+    SF_DEVICE_GUARD(c);
+    if (c->levels != 1) return SF_E_UNSUPPORTED;
+    if (!c->initialized) return sf_update(c, Y, D);  // frame 0: pointwise init of the band (exact on owned rows)
+    if (c->pending) return SF_E_STATE;
+    return banded_step(c, Y, D, xfer, user, host_staged ? 1 : 0, nullptr);
+}
+
+extern "C" sf_status sf_step_banded_nccl(sf_ctx* c, const float* Y, const float* D, void* comm, int32_t rank,
+                                         int32_t nranks) {
+    SF_NVTX("sf_step_banded_nccl");
+    if (!c || !Y || !D || !comm || rank < 0 || rank >= nranks) return SF_E_DATA;
+    SF_DEVICE_GUARD(c);
+    if (c->levels != 1) return SF_E_UNSUPPORTED;
+    if (!nccl().ok) return SF_E_NCCL;
+    if (!c->initialized) return sf_update(c, Y, D);
+    if (c->pending) return SF_E_STATE;
+    NcclXfer x{comm, rank, c->stream};
+    return banded_step(c, Y, D, nccl_xfer, &x, 0, &x);
+}

@@ -958,6 +958,11 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_trans(const __grid_constant__ F
         cp_async_wait<0>();
     }
     SF_PROF();  // 1: e planes landed
+#ifdef SF_DEBUG_KNOBS
+    const int kdbg = a.dbg_skip;  // timing experiments: 64 = no column passes, 128 = no row passes
+#else
+    constexpr int kdbg = 0;
+#endif
     float2 ER[EREG ? 6 : 1][K];
     if (EREG) {
 #pragma unroll
@@ -965,12 +970,15 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_trans(const __grid_constant__ F
 #pragma unroll
             for (int k = 0; k < K; ++k) ER[q][k] = *reinterpret_cast<const float2*>(Es + q * P + (r0 + k) * RW + c0);
     }
-    if (edge || f.imu)
+    if (f.imu)  // (the inertial stage only where it is on: it costs registers and scheduling freedom)
         transport_passes<K, NWY, RULE, CLAMP, 4, true, true, EREG>(f, a.M, W, SX, SY, SZ, mx, Es, XB0, lane, wy, cmin,
-                                                                   cmax, rmin, rmax, 0, nullptr, ER);
+                                                                   cmax, rmin, rmax, kdbg, nullptr, ER);
+    else if (edge)
+        transport_passes<K, NWY, RULE, CLAMP, 4, true, false, EREG>(f, a.M, W, SX, SY, SZ, mx, Es, XB0, lane, wy, cmin,
+                                                                    cmax, rmin, rmax, kdbg, nullptr, ER);
     else
         transport_passes<K, NWY, RULE, CLAMP, 4, false, false, EREG>(f, a.M, W, SX, SY, SZ, mx, Es, XB0, lane, wy,
-                                                                     cmin, cmax, rmin, rmax, 0, nullptr, ER);
+                                                                     cmin, cmax, rmin, rmax, kdbg, nullptr, ER);
     SF_PROF();  // 2: transport
     // ---- flags from tile cells (exact at every pass; |u_hat| before the clamp) and the tile store
     unsigned fl = 0;

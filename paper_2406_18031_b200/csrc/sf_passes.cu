@@ -12,7 +12,7 @@ inline dim3 grid_for(const FrameParams& f) { return dim3((f.W + BX - 1) / BX, (f
 
 // ------------------------------------------------------------------ geometry
 // e_k = b_k / ds (IEEE division), d2 = ds * ds (reading 5).
-__global__ void k_geometry(const float* __restrict__ g10, float4* G0, float4* G1, float4* G2, float* E, int n) {
+__global__ void k_geometry(const float* __restrict__ g10, float4* G0, float4* G1, float4* G2, float4* GS, int n) {
     int p = blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= n) return;
     const float* g = g10 + 10 * (size_t)p;
@@ -22,6 +22,9 @@ __global__ void k_geometry(const float* __restrict__ g10, float4* G0, float4* G1
     const float4 e2 = make_float4(__fdiv_rn(g[6], ds), __fdiv_rn(g[7], ds), __fdiv_rn(g[8], ds), 0.0f);
     G1[p] = e1;
     G2[p] = e2;
+    GS[3 * (size_t)p] = G0[p];
+    GS[3 * (size_t)p + 1] = e1;
+    GS[3 * (size_t)p + 2] = e2;
 }
 
 // The padded e planes (sf_internal.cuh SF_EPAD): cell (i, j) of [H + 2 EPAD][W + 2 EPAD] holds e of
@@ -44,12 +47,14 @@ __global__ void k_epad(const float4* __restrict__ G1, const float4* __restrict__
 // ------------------------------------------------------------------ transport pass (P1-P4)
 // AXIS 0: column pass (beta_1, neighbours (i, j+-1), e1).
 // AXIS 1: row pass    (beta_2, neighbours (i+-1, j), e2), P:L674-683 (reading 3).
+// Rows [r0, r1) of the grid (the banded substep exchange updates the rows next to a band's cut
+// edges after the others, sf_band.cu); the whole grid otherwise.
 template <int AXIS>
 __global__ void __launch_bounds__(BX* BY) k_pass(const float4* __restrict__ in, float4* __restrict__ out,
                                                 const float4* __restrict__ G0, const float4* __restrict__ Ge,
-                                                FrameParams f, unsigned* flags) {
-    const int j = blockIdx.x * BX + threadIdx.x, i = blockIdx.y * BY + threadIdx.y, b = blockIdx.z;
-    const bool live = (i < f.H) && (j < f.W);
+                                                FrameParams f, unsigned* flags, int r0, int r1) {
+    const int j = blockIdx.x * BX + threadIdx.x, i = r0 + blockIdx.y * BY + threadIdx.y, b = blockIdx.z;
+    const bool live = (i < r1) && (j < f.W);
     const int ii = live ? i : 0, jj = live ? j : 0;
     int im = ii, ip = ii, jm = jj, jp = jj;
     if (AXIS == 0) {
@@ -348,7 +353,7 @@ __global__ void k_pack(const float* __restrict__ w, const float* __restrict__ rh
 
 cudaError_t sf_launch_geometry(sf_ctx* c, const float* g10) {
     const int n = c->fp.H * c->fp.W;
-    k_geometry<<<(n + 255) / 256, 256, 0, c->stream>>>(g10, c->G0, c->G1, c->G2, c->E, n);
+    k_geometry<<<(n + 255) / 256, 256, 0, c->stream>>>(g10, c->G0, c->G1, c->G2, c->GS, n);
     const int ne = sf_ew(c->fp.W) * sf_eh(c->fp.H);
     k_epad<<<(ne + 255) / 256, 256, 0, c->stream>>>(c->G1, c->G2, c->E, c->fp.H, c->fp.W);
     return cudaGetLastError();
@@ -360,8 +365,8 @@ cudaError_t sf_launch_predict_passes(sf_ctx* c) {
     const dim3 g = grid_for(f), blk(BX, BY);
     const float4* src = c->state[c->cur];
     for (int n = 0; n < f.N; ++n) {
-        k_pass<0><<<g, blk, 0, c->stream>>>(src, c->tmp, c->G0, c->G1, f, c->flags);
-        k_pass<1><<<g, blk, 0, c->stream>>>(c->tmp, c->pred, c->G0, c->G2, f, c->flags);
+        k_pass<0><<<g, blk, 0, c->stream>>>(src, c->tmp, c->G0, c->G1, f, c->flags, 0, f.H);
+        k_pass<1><<<g, blk, 0, c->stream>>>(c->tmp, c->pred, c->G0, c->G2, f, c->flags, 0, f.H);
         src = c->pred;
     }
     return cudaGetLastError();
@@ -385,6 +390,42 @@ cudaError_t sf_launch_update_passes(sf_ctx* c, const float* Y, const float* D, b
         float4* dst = s == f.S - 1 ? nxt : ((s & 1) ? c->tmp : c->tmp2);
         k_box<<<g, blk, 0, c->stream>>>(src, dst, f);
     }
+    return cudaGetLastError();
+}
+
+// Busy-wait ~ns nanoseconds on the device (sf_step_timed queues the timed kernels behind it, so that
+// the CUDA events around them measure device time, not host launch latency).
+__global__ void k_spin(long long ns) {
+    unsigned long long t0, t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    do {
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    } while ((long long)(t - t0) < ns);
+}
+cudaError_t sf_launch_spin(sf_ctx* c, long long ns) {
+    k_spin<<<1, 1, 0, c->stream>>>(ns);
+    return cudaGetLastError();
+}
+
+// ---- building blocks of the banded substep-exchange step (sf_band.cu)
+cudaError_t sf_launch_pass(sf_ctx* c, int axis, const float4* in, float4* out, int r0, int r1, cudaStream_t s) {
+    const FrameParams& f = c->fp;
+    if (r1 <= r0) return cudaSuccess;
+    const dim3 g((f.W + BX - 1) / BX, (r1 - r0 + BY - 1) / BY, f.B), blk(BX, BY);
+    if (axis == 0)
+        k_pass<0><<<g, blk, 0, s>>>(in, out, c->G0, c->G1, f, c->flags, r0, r1);
+    else
+        k_pass<1><<<g, blk, 0, s>>>(in, out, c->G0, c->G2, f, c->flags, r0, r1);
+    return cudaGetLastError();
+}
+cudaError_t sf_launch_update_solve(sf_ctx* c, const float* Y, const float* D, float4* out) {
+    const FrameParams& f = c->fp;
+    k_update<<<grid_for(f), dim3(BX, BY), 0, c->stream>>>(Y, D, c->pred, c->state[c->cur], c->yhat[c->cur], 1,
+                                                          c->yhat[1 - c->cur], out, c->G0, c->G1, c->G2, f, c->flags);
+    return cudaGetLastError();
+}
+cudaError_t sf_launch_box(sf_ctx* c, const float4* in, float4* out) {
+    k_box<<<grid_for(c->fp), dim3(BX, BY), 0, c->stream>>>(in, out, c->fp);
     return cudaGetLastError();
 }
 

@@ -21,8 +21,8 @@
 //            differences; ghat, m; c_Y, c_rho; LDL^T solve -> w_LS planes; Yhat^{k+1} of tile cells
 //            stored; the next item's global inputs (w^{k+}, s, e1, e2, references) fetched one
 //            item ahead;
-//   stage 3: S box passes, each separable in two sweeps over the shared planes (horizontal
-//            5-sums of the window rows, then vertical 5-sums / 25), one 4-column quad per item;
+//   stage 3: S box passes, each a register-tiled separable stencil (one item = one component
+//            of a 4-column x 6-row output block: 10 horizontal 5-sums, sliding vertical 5-sums);
 //   stage 4: rho fusion and the coalesced store of (w^{k+1}, rho^{k+1}) for the tile.
 // The top level (H = 1) and the pyramid's bottom level [dU] (reading 28: references Yhat^{k+},
 // rho^{k+} instead of Yhat^k, rho^k) run the same kernel with different reference pointers.
@@ -45,6 +45,7 @@ struct UpdArgs {
     int rs, ys;
     const float* Y;            // [B][H][W] brightness
     const float* D;            // [B][H][W] depth (or inverse depth)
+    const float4* GS;          // [H][W][3]: (s, d2), (e1, ds), (e2, 0), or null: the separate planes
     const float4* G0;          // (s, d2)
     const float4* G1;          // (e1, ds)
     const float4* G2;          // (e2, 0)
@@ -52,7 +53,8 @@ struct UpdArgs {
     float* yout;               // Yhat^{k+1}
     unsigned* flags;
     FrameParams f;
-    int TH, TW, h, MR, MG, PH, PW, P;  // P: plane stride (PH * PW rounded up to 32 floats)
+    int TH, TW, h, MR, MG, PH, PW, P;  // P: plane stride of Y, rhohat, HG, HH (a multiple of 32 floats)
+    int PF;                            // plane stride of the 6 box planes (= 12 mod 32: bank-spread)
     int dbg;                           // SF_DEBUG_SKIP (debug builds only): 8192 = phase profile
 };
 
@@ -100,15 +102,15 @@ __global__ void __launch_bounds__(UPD_NT, 1) k_upd(const __grid_constant__ UpdAr
     extern __shared__ __align__(1024) float sm[];  // TMA destinations: 128-byte aligned planes
     const FrameParams& f = a.f;
     const int tid = threadIdx.x;
-    const int PH = a.PH, PW = a.PW, P = a.P, h = a.h, MR = a.MR, MG = a.MG, TH = a.TH, TW = a.TW;
+    const int PH = a.PH, PW = a.PW, P = a.P, PF = a.PF, h = a.h, MR = a.MR, MG = a.MG, TH = a.TH, TW = a.TW;
     float* const Ys = sm;          // Y; after the models: rho^{k+} of the SR cells (RP)
     float* const RHs = sm + P;     // depth -> rhohat (NaN = invalid), read by the fusion
     float* const HG = sm + 2 * P;  // horizontal g-taps of Y
     float* const HH = sm + 3 * P;  // horizontal h-taps of Y
-    float* const F0 = sm + 4 * P;  // 3 planes: w_LS, smoothed in place by the box passes
-    float* const F1 = sm + 7 * P;  // 3 planes: the box's horizontal sums
+    float* const F0 = sm + 4 * P;           // 3 planes (stride PF): w_LS, then the box ping
+    float* const F1 = sm + 4 * P + 3 * PF;  // 3 planes: the box pong
     float* const RP = Ys;
-    uint64_t* const bar = reinterpret_cast<uint64_t*>(sm + 10 * P);
+    uint64_t* const bar = reinterpret_cast<uint64_t*>(sm + 4 * P + 6 * PF);
     const int b = blockIdx.z;
     const int i0 = blockIdx.y * TH, j0 = blockIdx.x * TW;
     const int oi = i0 - MR, oj = j0 - MG;  // global cell of plane cell (0, 0)
@@ -151,19 +153,30 @@ __global__ void __launch_bounds__(UPD_NT, 1) k_upd(const __grid_constant__ UpdAr
     SolveIn nx;
     auto fetch_geo = [&](int r, int pc, SolveIn& q) {
         r = min(r, srh);
-        const int c = scl + 2 * pc, c1 = min(c + 1, sch);
-        const size_t ga = (size_t)(oi + r) * f.W + (oj + c), gb = (size_t)(oi + r) * f.W + (oj + c1);
-        q.sa = __ldg(a.G0 + ga);
-        q.sb = __ldg(a.G0 + gb);
-        q.ea = __ldg(a.G1 + ga);
-        q.eb = __ldg(a.G1 + gb);
-        q.fa = __ldg(a.G2 + ga);
-        q.fb = __ldg(a.G2 + gb);
+        const int c = scl + 2 * pc;
+        const size_t cell = (size_t)(oi + r) * f.W + (oj + c), d = c + 1 <= sch ? 1 : 0;  // ragged: the first cell again
+        if (a.GS) {
+            const float4* ga = a.GS + 3 * cell;
+            const float4* gb = ga + 3 * d;
+            q.sa = __ldg(ga);
+            q.ea = __ldg(ga + 1);
+            q.fa = __ldg(ga + 2);
+            q.sb = __ldg(gb);
+            q.eb = __ldg(gb + 1);
+            q.fb = __ldg(gb + 2);
+        } else {
+            q.sa = __ldg(a.G0 + cell);
+            q.sb = __ldg(a.G0 + cell + d);
+            q.ea = __ldg(a.G1 + cell);
+            q.eb = __ldg(a.G1 + cell + d);
+            q.fa = __ldg(a.G2 + cell);
+            q.fb = __ldg(a.G2 + cell + d);
+        }
     };
     auto fetch_fld = [&](int r, int pc, SolveIn& q) {
         r = min(r, srh);
-        const int c = scl + 2 * pc, c1 = min(c + 1, sch);
-        const size_t ga = pl + (size_t)(oi + r) * f.W + (oj + c), gb = pl + (size_t)(oi + r) * f.W + (oj + c1);
+        const int c = scl + 2 * pc;
+        const size_t ga = pl + (size_t)(oi + r) * f.W + (oj + c), gb = ga + (c + 1 <= sch ? 1 : 0);
         q.wa = a.pred[ga];
         q.wb = a.pred[gb];
         q.y = make_float2(a.yref[ga * a.ys], a.yref[gb * a.ys]);
@@ -228,16 +241,17 @@ __global__ void __launch_bounds__(UPD_NT, 1) k_upd(const __grid_constant__ UpdAr
 
     SF_PROF();  // 2: models
     // ---------------- stage 2: per-pixel LS on SR, a horizontal pair of cells per item
+    // The loop is unrolled twice with two input buffers (nx, ny): each item's inputs are fetched
+    // one item ahead straight into the buffer the item will be solved from (no register copies of
+    // in-flight loads).
     {
         auto ld2 = [&](const float* p, int i) { return *reinterpret_cast<const float2*>(p + i); };
-#pragma unroll 1
-        while (rn <= srh) {
-            const int r = rn, c = scl + 2 * pn;
-            const SolveIn cu = nx;
-            rn += pdr + ((pn + pdc >= np) ? 1 : 0);
-            pn = (pn + pdc >= np) ? pn + pdc - np : pn + pdc;
-            fetch_geo(rn, pn, nx);
-            fetch_fld(rn, pn, nx);
+        auto advance = [&](int& r, int& pc) {
+            r += pdr + ((pc + pdc >= np) ? 1 : 0);
+            pc = (pc + pdc >= np) ? pc + pdc - np : pc + pdc;
+        };
+        auto solve_item = [&](int r, int pn_, const SolveIn& cu) {
+            const int c = scl + 2 * pn_;
             const bool full = c + 1 <= sch;
             const int idx = r * PW + c;  // even: 8-byte aligned pairs (a ragged pair's second cell is unused)
             const float2 g0 = ld2(HG, idx - 2 * PW), g1 = ld2(HG, idx - PW), g2 = ld2(HG, idx), g3 = ld2(HG, idx + PW),
@@ -278,8 +292,8 @@ __global__ void __launch_bounds__(UPD_NT, 1) k_upd(const __grid_constant__ UpdAr
             float2 x[3];
             ls_solve3x2(gh, m, cY, cr, wp, f.g1, make_float2(vc0 ? f.g2 : 0.0f, vc1 ? f.g2 : 0.0f), f.g3, x);
             *reinterpret_cast<float2*>(F0 + idx) = x[0];  // (a ragged pair's second cell: out of the grid, unused)
-            *reinterpret_cast<float2*>(F0 + P + idx) = x[1];
-            *reinterpret_cast<float2*>(F0 + 2 * P + idx) = x[2];
+            *reinterpret_cast<float2*>(F0 + PF + idx) = x[1];
+            *reinterpret_cast<float2*>(F0 + 2 * PF + idx) = x[2];
             *reinterpret_cast<float2*>(RP + idx) = make_float2(cu.wa.w, cu.wb.w);
             if (r >= tr0 && r <= tr1) {  // tile cells: Yhat^{k+1}, non-finite solve flag
                 const size_t g = pl + (size_t)(oi + r) * f.W + (oj + c);
@@ -290,18 +304,40 @@ __global__ void __launch_bounds__(UPD_NT, 1) k_upd(const __grid_constant__ UpdAr
                                  (in1 && !(isfinite(x[0].y) && isfinite(x[1].y) && isfinite(x[2].y)));
                 if (bad && oi + r >= f.fr0 && oi + r < f.fr1) fl |= SF_FLAG_NONFINITE;
             }
+        };
+        SolveIn ny;
+        int rm = rn, pm = pn;  // the item after (rn, pn)
+        advance(rm, pm);
+#pragma unroll 1
+        while (rn <= srh) {
+            fetch_geo(rm, pm, ny);
+            fetch_fld(rm, pm, ny);
+            solve_item(rn, pn, nx);
+            if (rm > srh) break;
+            rn = rm;
+            pn = pm;
+            advance(rn, pn);
+            fetch_geo(rn, pn, nx);
+            fetch_fld(rn, pn, nx);
+            solve_item(rm, pm, ny);
+            rm = rn;
+            pm = pn;
+            advance(rm, pm);
         }
     }
 
     SF_PROF();  // 3: solve
-    // ---------------- stage 3: S x 5x5 box (reading 13): horizontal 5-sums left to right
-    // (F0 -> F1), then vertical 5-sums top to bottom / 25 (F1 -> F0: the pass's input is dead by
-    // then), so the smoothed field stays in F0.  Items are one component's 4-column quad of one row
-    // (16-byte shared accesses, consecutive quads on consecutive lanes: conflict-free); div25 is
-    // the IEEE quotient.
+    // ---------------- stage 3: S x 5x5 box (reading 13) as a register-tiled separable
+    // stencil: one item = one component's 4-column quad over 6 output rows, read as a window of 10
+    // rows x 8 columns (8- and 16-byte shared loads) -> horizontal 5-sums left to right of the 10
+    // rows -> vertical 5-sums top to bottom -> / 25 (div25: the IEEE quotient).  The passes
+    // ping-pong between F0 and F1.  Window rows below a pass's last output row (the planes carry
+    // 8 spare rows) and columns outside its window feed only unstored outputs.
     const bool edge = i0 - h < 0 || i0 + TH + h > f.H || j0 - h < 0 || j0 + TW + h > f.W;  // SR leaves the grid
     const int S = f.S;
     const float2 y25 = make_float2(0.04f, 0.04f), m25 = make_float2(-25.0f, -25.0f);
+    float* src = F0;
+    float* dst = F1;
 #pragma unroll 1
     for (int it = 0; it < S; ++it) {
         const int mo = 2 * (S - 1 - it);  // this pass's output: tile +- mo, in the grid
@@ -310,47 +346,48 @@ __global__ void __launch_bounds__(UPD_NT, 1) k_upd(const __grid_constant__ UpdAr
         const int bc0 = oc0 & ~3, nbc = (oc1 - bc0) / 4 + 1;  // 16-byte aligned quads over [oc0, oc1]
         __syncthreads();
         if (edge) {
-            fill_planes<3>(F0, P, PW, PH, or0 - 2, or1 + 2, oc0 - 2, oc1 + 2, rmin, rmax, cmin, cmax, tid);
+            fill_planes<3>(src, PF, PW, PH, or0 - 2, or1 + 2, oc0 - 2, oc1 + 2, rmin, rmax, cmin, cmax, tid);
             __syncthreads();
         }
-        // horizontal sums of the window rows (quads reading columns c-2 .. c+5; columns outside the
-        // window feed only unstored outputs)
 #pragma unroll 1
-        SF_FOR_RECT(r, bq, or0 - 2, or1 + 2, 0, 3 * nbc - 1, UPD_NT, tid) {
-            const int q = (bq >= nbc) + (bq >= 2 * nbc), c = bc0 + 4 * (bq - q * nbc);
-            const float* row = F0 + q * P + r * PW + c - 2;
-            const float2 xa = *reinterpret_cast<const float2*>(row);
-            const float4 xb = *reinterpret_cast<const float4*>(row + 2);
-            const float2 xc = *reinterpret_cast<const float2*>(row + 6);
-            const float2 xab = make_float2(xa.y, xb.x), xbb = make_float2(xb.y, xb.z), xbc = make_float2(xb.w, xc.x);
-            const float2 xlo = make_float2(xb.x, xb.y), xhi = make_float2(xb.z, xb.w);
-            // sums of columns (c + j - 2 .. c + j + 2), j = 0..3, paired: ((((x0 + x1) + x2) + x3) + x4)
-            const float2 s0 = add2(add2(add2(add2(xa, xab), xlo), xbb), xhi);
-            const float2 s1 = add2(add2(add2(add2(xlo, xbb), xhi), xbc), xc);
-            *reinterpret_cast<float4*>(F1 + q * P + r * PW + c) = make_float4(s0.x, s0.y, s1.x, s1.y);
-        }
-        __syncthreads();
-#pragma unroll 1
-        SF_FOR_RECT(r, bq, or0, or1, 0, 3 * nbc - 1, UPD_NT, tid) {
-            const int q = (bq >= nbc) + (bq >= 2 * nbc), c = bc0 + 4 * (bq - q * nbc);
-            const float* col = F1 + q * P + (r - 2) * PW + c;
-            float4 v4[5];
+        SF_FOR_RECT(sg, bq, 0, (or1 - or0) / 6, 0, 3 * nbc - 1, UPD_NT, tid) {
+            // bq = 3 quad + component: with PF = 12 (mod 32) the 8 lanes of a quarter warp hit 8
+            // distinct 16-byte bank groups (bank group of lane l steps by 3 mod 8)
+            const int quad = (bq * 43691) >> 17, q = bq - 3 * quad;  // bq / 3 (exact for bq < 2^15)
+            const int c = bc0 + 4 * quad, r = or0 + 6 * sg;
+            const float* row = src + q * PF + (r - 2) * PW + c - 2;
+            float2 hs[10][2];  // horizontal 5-sums of rows r-2 .. r+7, column pairs (c, c+1) (c+2, c+3)
 #pragma unroll
-            for (int i = 0; i < 5; ++i) v4[i] = *reinterpret_cast<const float4*>(col + i * PW);
-            float o[4];
-#pragma unroll
-            for (int jp = 0; jp < 2; ++jp) {
-                auto lo = [&](const float4& x) { return jp ? make_float2(x.z, x.w) : make_float2(x.x, x.y); };
-                const float2 v = add2(add2(add2(add2(lo(v4[0]), lo(v4[1])), lo(v4[2])), lo(v4[3])), lo(v4[4]));
-                const float2 qq = mul2(v, y25);
-                const float2 q1 = fma2(fma2(qq, m25, v), y25, qq);
-                o[2 * jp] = isfinite(v.x) ? q1.x : qq.x;
-                o[2 * jp + 1] = isfinite(v.y) ? q1.y : qq.y;
+            for (int i = 0; i < 10; ++i, row += PW) {
+                const float2 xa = *reinterpret_cast<const float2*>(row);
+                const float4 xb = *reinterpret_cast<const float4*>(row + 2);
+                const float2 xc = *reinterpret_cast<const float2*>(row + 6);
+                const float2 xab = make_float2(xa.y, xb.x), xbb = make_float2(xb.y, xb.z), xbc = make_float2(xb.w, xc.x);
+                const float2 xlo = make_float2(xb.x, xb.y), xhi = make_float2(xb.z, xb.w);
+                // sums of columns (c + j - 2 .. c + j + 2), j = 0..3, paired: ((((x0 + x1) + x2) + x3) + x4)
+                hs[i][0] = add2(add2(add2(add2(xa, xab), xlo), xbb), xhi);
+                hs[i][1] = add2(add2(add2(add2(xlo, xbb), xhi), xbc), xc);
             }
-            *reinterpret_cast<float4*>(F0 + q * P + r * PW + c) = make_float4(o[0], o[1], o[2], o[3]);
+            float* out = dst + q * PF + r * PW + c;
+#pragma unroll
+            for (int i = 0; i < 6; ++i, out += PW) {
+                float o[4];
+#pragma unroll
+                for (int jp = 0; jp < 2; ++jp) {
+                    const float2 v = add2(add2(add2(add2(hs[i][jp], hs[i + 1][jp]), hs[i + 2][jp]), hs[i + 3][jp]),
+                                          hs[i + 4][jp]);
+                    const float2 qq = mul2(v, y25);
+                    const float2 q1 = fma2(fma2(qq, m25, v), y25, qq);
+                    o[2 * jp] = isfinite(v.x) ? q1.x : qq.x;
+                    o[2 * jp + 1] = isfinite(v.y) ? q1.y : qq.y;
+                }
+                if (r + i <= or1) *reinterpret_cast<float4*>(out) = make_float4(o[0], o[1], o[2], o[3]);
+            }
         }
+        float* tmp = src;
+        src = dst;
+        dst = tmp;
     }
-    float* const src = F0;
     __syncthreads();
     SF_PROF();  // 4: box
 
@@ -363,7 +400,7 @@ __global__ void __launch_bounds__(UPD_NT, 1) k_upd(const __grid_constant__ UpdAr
         const bool v = !isnan(rh);
         const float rn1 = xfma(v ? kap : 0.0f, xsub(v ? rh : 0.0f, rp), rp);
         if (!isfinite(rn1) && oi + r >= f.fr0 && oi + r < f.fr1) fl |= SF_FLAG_NONFINITE;
-        a.out[pl + (size_t)(oi + r) * f.W + (oj + c)] = make_float4(src[idx], src[P + idx], src[2 * P + idx], rn1);
+        a.out[pl + (size_t)(oi + r) * f.W + (oj + c)] = make_float4(src[idx], src[PF + idx], src[2 * PF + idx], rn1);
     }
     SF_PROF();  // 5: fusion + store
     SF_PROF_PRINT("upd");
@@ -386,8 +423,11 @@ bool plan_tiles(const FrameParams& f, int h, UpdArgs& a, size_t& smem) {
     const int MR = h + 2, MG = (h + 6) & ~3;  // MG >= h + 3, a multiple of 4
     long long best = -1;
     for (const TileOpt& t : kTiles) {
-        const int PW = t.TW + 2 * MG, PH = t.TH + 2 * MR, P = (PW * PH + 31) & ~31;  // 128-byte aligned planes
-        const size_t bytes = sizeof(float) * 10 * (size_t)P + 64;
+        // planes of PH rows + 8 spare rows (read by the box's last row segment): Y, rhohat, HG, HH
+        // 128-byte aligned (TMA destinations), the 6 box planes at a stride of 12 (mod 32) floats
+        const int PW = t.TW + 2 * MG, PH = t.TH + 2 * MR, P = (PW * (PH + 8) + 31) & ~31;
+        const int PF = P + 12;
+        const size_t bytes = sizeof(float) * (4 * (size_t)P + 6 * (size_t)PF) + 64;
         if (bytes > 227 * 1024) continue;
         const long long tiles = (long long)((f.W + t.TW - 1) / t.TW) * ((f.H + t.TH - 1) / t.TH) * f.B;
         const long long waves = (tiles + sms - 1) / sms;
@@ -401,6 +441,7 @@ bool plan_tiles(const FrameParams& f, int h, UpdArgs& a, size_t& smem) {
             a.PW = PW;
             a.PH = PH;
             a.P = P;
+            a.PF = PF;
             smem = bytes;
         }
     }
@@ -435,6 +476,7 @@ cudaError_t sf_launch_update_fused(sf_ctx* c, const float* Y, const float* D, co
     a.ys = ys;
     a.Y = Y;
     a.D = D;
+    a.GS = getenv("SF_UPD_GS") ? c->GS : nullptr;  // (A/B switch: interleaved geometry)
     a.G0 = c->G0;
     a.G1 = c->G1;
     a.G2 = c->G2;
