@@ -554,9 +554,12 @@ def run_sf(args):
 
 
 def run_banded(args):
-    """configs[4]: one 8192^2 frame per step, row bands over the ranks (strong scaling).  Each
-    rank owns rows [o0, o1) plus halo = max(N,2)+2S rows; per step: NCCL halo exchange
-    (sf_halo_exchange_nccl, 2 x halo rows of state + Yhat), then sf_step on the band."""
+    """configs[4]: one 8192^2 frame per step, row bands over the ranks (strong scaling).
+    --band-mode deep (default): each rank owns rows [o0, o1) plus halo = max(N,2)+2S rows; per
+    step one NCCL halo exchange (sf_halo_exchange_nccl, 2 x halo rows of state + Yhat), then the
+    fused sf_step on the band.  --band-mode substep: 2 halo rows; sf_step_banded_nccl exchanges 1
+    row after every column pass and 2 rows before every box pass (N + S NCCL groups per frame) on
+    the per-pass kernels (the north star's per-substep split)."""
     import torch
     import torch.distributed as dist
 
@@ -573,7 +576,8 @@ def run_banded(args):
     cfg0 = sf.sf_config_default(H, W)
     cfg0.max_flow_px = c["max_flow"]
     cfg0.smooth_iters = 2
-    halo = sf.sf_band_halo(cfg0)
+    substep = getattr(args, "band_mode", "deep") == "substep"
+    halo = sf.sf_band_halo_substep(cfg0) if substep else sf.sf_band_halo(cfg0)
     e0, o0, o1, e1 = sf.sf_band_partition(H, world, rank, halo)
     ring = 2  # each frame is 512 MiB of inputs: 2 frames replayed palindromically already exceed L2
     geom, Yh, Dh, params = sfgen.configs.band_sequence(5, e0, e1, ring)
@@ -596,6 +600,9 @@ def run_banded(args):
     def step(i):
         j = i % (2 * ring)
         k = j if j < ring else 2 * ring - 1 - j
+        if substep and comm is not None:
+            sf.sf_step_banded_nccl(m.ctx, Yd[k].data_ptr(), Dd[k].data_ptr(), comm, rank, world)
+            return
         if comm is not None and started[0]:
             sf.sf_halo_exchange_nccl(m.ctx, comm, rank, world)
         m.step(Yd[k], Dd[k])
@@ -635,10 +642,15 @@ def run_banded(args):
                "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
                "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
                "config": {"workload": CONFIG_NAMES[5], "H": H, "W": W, "N": params.N, "S": params.smooth_iters,
-                          "parallelism": f"row bands x{world}, halo {halo} rows, 1 NCCL exchange / frame",
+                          "parallelism": (f"row bands x{world}, halo {halo} rows, per-substep NCCL exchange "
+                                          f"({params.N + params.smooth_iters} groups / frame, per-pass kernels)"
+                                          if substep and world > 1 else
+                                          f"row bands x{world}, halo {halo} rows, 1 NCCL exchange / frame"),
                           "inputs": f"{ring} frames x {2 * H * W * 4 / 2**20:.0f} MiB, palindromic (> L2)"},
                "roofline": {"bound": "alu", "achieved": alu, "peak": alu_peak, "unit": "TFLOP/s",
-                            "frac": alu / alu_peak, "traffic": None, "kernel": "k_fused + halo exchange",
+                            "frac": alu / alu_peak, "traffic": None,
+                            "kernel": "per-pass kernels + per-substep exchange" if substep and world > 1
+                            else "fused step + halo exchange",
                             "peak_source": f"{world} x 148 SMs x 128 FP32 lanes x {sm_max:.0f} MHz"},
                "gpu_launches": m.launches_per_step * args.steps, "e2e": None, "device_flags": flags, "clocks": clocks}
         print(json.dumps(out))
@@ -665,6 +677,8 @@ def main():
     ap.add_argument("--levels", type=int, choices=[1, 2], default=1,
                     help="pyramid levels (1: the graded H = 1 hot path; 2: the paper's Table 3 shape)")
     ap.add_argument("--ring", type=int, default=96)
+    ap.add_argument("--band-mode", choices=["deep", "substep"], default="deep",
+                    help="--config 5 over N > 1 ranks: one deep halo exchange per frame, or the per-substep exchange")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:

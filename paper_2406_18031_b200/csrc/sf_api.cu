@@ -56,7 +56,7 @@ static void async_teardown(sf_ctx* c);
 
 static void free_ctx(sf_ctx* c) {
     if (!c) return;
-    void* ptrs[] = {c->G0, c->G1, c->G2, c->GS, c->E, c->state[0], c->state[1], c->pred, c->tmp, c->tmp2,
+    void* ptrs[] = {c->G0, c->G1, c->G2, c->E, c->state[0], c->state[1], c->pred, c->tmp, c->tmp2,
                     c->yhat[0], c->yhat[1], c->HG, c->HH, c->flags, c->hY, c->hD, c->hw, c->hr, c->eval_part,
                     c->Wf[0], c->Wf[1], c->Wpred, c->Wtmp, c->Y2, c->D2, c->mY, c->mD};
     for (void* p : ptrs)
@@ -181,7 +181,6 @@ extern "C" sf_status sf_create(const sf_config* cfg, const float* geometry, sf_c
     bool ok = cudaMalloc(&c->G0, npix * sizeof(float4)) == cudaSuccess &&
               cudaMalloc(&c->G1, npix * sizeof(float4)) == cudaSuccess &&
               cudaMalloc(&c->G2, npix * sizeof(float4)) == cudaSuccess &&
-              cudaMalloc(&c->GS, 3 * npix * sizeof(float4)) == cudaSuccess &&
               cudaMalloc(&c->E, 6 * (size_t)sf_ew(f.W) * sf_eh(f.H) * sizeof(float)) == cudaSuccess &&
               cudaMalloc(&c->state[0], nall * sizeof(float4)) == cudaSuccess &&
               cudaMalloc(&c->state[1], nall * sizeof(float4)) == cudaSuccess &&
@@ -229,7 +228,7 @@ extern "C" sf_status sf_create(const sf_config* cfg, const float* geometry, sf_c
         }
         // bottom level: fused prediction unless the pass kernels are requested; update on passes
         c->low_fused = cfg->kernel != SF_KERNEL_PASSES && sf_low_fused_supported(c);
-        c->upd_fused = cfg->kernel != SF_KERNEL_PASSES && sf_update_fused_supported(c);
+        c->upd_fused = cfg->kernel != SF_KERNEL_PASSES && !getenv("SF_UPD_LOW_PASSES") && sf_update_fused_supported(c);
         c->kernel = c->low_fused ? SF_KERNEL_FUSED : SF_KERNEL_PASSES;
         *out = c;
         return SF_OK;

@@ -876,6 +876,9 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_trans(const __grid_constant__ F
     const bool edge = cmin > 0 || cmax < RW - 1 || rmin > 0 || rmax < RH - 1;  // block-uniform
     const size_t HW = (size_t)f.H * f.W, plane = (size_t)b * HW;
     SF_PROF_DECL(a.dbg_skip & 8192);
+#ifdef SF_DEBUG_KNOBS
+    if (a.dbg_skip & 32) return;  // launch-overhead experiment
+#endif
     SF_PROF();
     // ---- the update kernel's inputs Y and depth (a.Y / a.D, 16-byte aligned; null when no update
     // follows): each CTA prefetches its share of the frame into L2, so that the update kernel's

@@ -12,7 +12,7 @@ inline dim3 grid_for(const FrameParams& f) { return dim3((f.W + BX - 1) / BX, (f
 
 // ------------------------------------------------------------------ geometry
 // e_k = b_k / ds (IEEE division), d2 = ds * ds (reading 5).
-__global__ void k_geometry(const float* __restrict__ g10, float4* G0, float4* G1, float4* G2, float4* GS, int n) {
+__global__ void k_geometry(const float* __restrict__ g10, float4* G0, float4* G1, float4* G2, int n) {
     int p = blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= n) return;
     const float* g = g10 + 10 * (size_t)p;
@@ -22,9 +22,6 @@ __global__ void k_geometry(const float* __restrict__ g10, float4* G0, float4* G1
     const float4 e2 = make_float4(__fdiv_rn(g[6], ds), __fdiv_rn(g[7], ds), __fdiv_rn(g[8], ds), 0.0f);
     G1[p] = e1;
     G2[p] = e2;
-    GS[3 * (size_t)p] = G0[p];
-    GS[3 * (size_t)p + 1] = e1;
-    GS[3 * (size_t)p + 2] = e2;
 }
 
 // The padded e planes (sf_internal.cuh SF_EPAD): cell (i, j) of [H + 2 EPAD][W + 2 EPAD] holds e of
@@ -353,7 +350,7 @@ __global__ void k_pack(const float* __restrict__ w, const float* __restrict__ rh
 
 cudaError_t sf_launch_geometry(sf_ctx* c, const float* g10) {
     const int n = c->fp.H * c->fp.W;
-    k_geometry<<<(n + 255) / 256, 256, 0, c->stream>>>(g10, c->G0, c->G1, c->G2, c->GS, n);
+    k_geometry<<<(n + 255) / 256, 256, 0, c->stream>>>(g10, c->G0, c->G1, c->G2, n);
     const int ne = sf_ew(c->fp.W) * sf_eh(c->fp.H);
     k_epad<<<(ne + 255) / 256, 256, 0, c->stream>>>(c->G1, c->G2, c->E, c->fp.H, c->fp.W);
     return cudaGetLastError();

@@ -45,7 +45,6 @@ struct UpdArgs {
     int rs, ys;
     const float* Y;            // [B][H][W] brightness
     const float* D;            // [B][H][W] depth (or inverse depth)
-    const float4* GS;          // [H][W][3]: (s, d2), (e1, ds), (e2, 0), or null: the separate planes
     const float4* G0;          // (s, d2)
     const float4* G1;          // (e1, ds)
     const float4* G2;          // (e2, 0)
@@ -120,6 +119,9 @@ __global__ void __launch_bounds__(UPD_NT, 1) k_upd(const __grid_constant__ UpdAr
     const size_t HW = (size_t)f.H * f.W, pl = (size_t)b * HW;
     const int lc0 = MG - h - 2, ncl = TW + 2 * h + 4;  // columns of Y used: SR +- 2 (depth: SR +- 1)
     SF_PROF_DECL(a.dbg & 8192);
+#ifdef SF_DEBUG_KNOBS
+    if (a.dbg & 32) return;  // launch-overhead experiment
+#endif
     SF_PROF();
 
     // ---------------- stage 0: Y and depth (caller inputs, prefetched into L2 by the transport
@@ -155,23 +157,12 @@ __global__ void __launch_bounds__(UPD_NT, 1) k_upd(const __grid_constant__ UpdAr
         r = min(r, srh);
         const int c = scl + 2 * pc;
         const size_t cell = (size_t)(oi + r) * f.W + (oj + c), d = c + 1 <= sch ? 1 : 0;  // ragged: the first cell again
-        if (a.GS) {
-            const float4* ga = a.GS + 3 * cell;
-            const float4* gb = ga + 3 * d;
-            q.sa = __ldg(ga);
-            q.ea = __ldg(ga + 1);
-            q.fa = __ldg(ga + 2);
-            q.sb = __ldg(gb);
-            q.eb = __ldg(gb + 1);
-            q.fb = __ldg(gb + 2);
-        } else {
-            q.sa = __ldg(a.G0 + cell);
-            q.sb = __ldg(a.G0 + cell + d);
-            q.ea = __ldg(a.G1 + cell);
-            q.eb = __ldg(a.G1 + cell + d);
-            q.fa = __ldg(a.G2 + cell);
-            q.fb = __ldg(a.G2 + cell + d);
-        }
+        q.sa = __ldg(a.G0 + cell);
+        q.sb = __ldg(a.G0 + cell + d);
+        q.ea = __ldg(a.G1 + cell);
+        q.eb = __ldg(a.G1 + cell + d);
+        q.fa = __ldg(a.G2 + cell);
+        q.fb = __ldg(a.G2 + cell + d);
     };
     auto fetch_fld = [&](int r, int pc, SolveIn& q) {
         r = min(r, srh);
@@ -476,7 +467,6 @@ cudaError_t sf_launch_update_fused(sf_ctx* c, const float* Y, const float* D, co
     a.ys = ys;
     a.Y = Y;
     a.D = D;
-    a.GS = getenv("SF_UPD_GS") ? c->GS : nullptr;  // (A/B switch: interleaved geometry)
     a.G0 = c->G0;
     a.G1 = c->G1;
     a.G2 = c->G2;

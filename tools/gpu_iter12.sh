@@ -1,0 +1,10 @@
+# k_trans prologue by TMA (fields + s): phases, kernel times, bench, parity suite.
+set -x
+SF_BUILD_DEBUG=1 python -c "import __graft_entry__ as g; g.build()" 2>&1 | tail -1
+SF_DEBUG_SKIP=8192 timeout 300 python tools/ktime.py --frames 12 --ring 8 2>&1 | grep 'SFPROF' | tail -4
+SF_NO_TMA=1 SF_DEBUG_SKIP=8192 timeout 300 python tools/ktime.py --frames 12 --ring 8 2>&1 | grep 'SFPROF trans' | tail -2
+python -c "import __graft_entry__ as g; g.build(); g.smoke()" 2>&1 | tail -1
+timeout 300 python tools/ktime2.py
+timeout 300 python bench.py --steps 2000 --warmup 20 --no-cpu-baseline 2>&1 | tail -1 > gpurun_out/bench_it12.json
+python -c "import json; d=json.load(open('gpurun_out/bench_it12.json')); print('BENCH', d['value'], d['ms_per_step']*1e3)"
+timeout 1500 python -m pytest tests -m gpu -q -x 2>&1 | tail -3
