@@ -281,6 +281,13 @@ __global__ void __launch_bounds__(UPD_NT, 1) k_upd(const __grid_constant__ UpdAr
             const float2 wp[3] = {make_float2(cu.wa.x, cu.wb.x), make_float2(cu.wa.y, cu.wb.y),
                                   make_float2(cu.wa.z, cu.wb.z)};
             float2 x[3];
+#ifdef SF_DEBUG_KNOBS
+            if (a.dbg & 1024) {  // timing experiment: no LDL^T solve (wrong results)
+                x[0] = fma2(gh[0], cY, wp[0]);
+                x[1] = fma2(m[1], cr, wp[1]);
+                x[2] = wp[2];
+            } else
+#endif
             ls_solve3x2(gh, m, cY, cr, wp, f.g1, make_float2(vc0 ? f.g2 : 0.0f, vc1 ? f.g2 : 0.0f), f.g3, x);
             *reinterpret_cast<float2*>(F0 + idx) = x[0];  // (a ragged pair's second cell: out of the grid, unused)
             *reinterpret_cast<float2*>(F0 + PF + idx) = x[1];
@@ -301,15 +308,25 @@ __global__ void __launch_bounds__(UPD_NT, 1) k_upd(const __grid_constant__ UpdAr
         advance(rm, pm);
 #pragma unroll 1
         while (rn <= srh) {
-            fetch_geo(rm, pm, ny);
-            fetch_fld(rm, pm, ny);
+#ifdef SF_DEBUG_KNOBS
+            if (!(a.dbg & 16))  // timing experiment: 16 = no global fetches in the loop (wrong results)
+#endif
+            {
+                fetch_geo(rm, pm, ny);
+                fetch_fld(rm, pm, ny);
+            }
             solve_item(rn, pn, nx);
             if (rm > srh) break;
             rn = rm;
             pn = pm;
             advance(rn, pn);
-            fetch_geo(rn, pn, nx);
-            fetch_fld(rn, pn, nx);
+#ifdef SF_DEBUG_KNOBS
+            if (!(a.dbg & 16))  // timing experiment: 16 = no global fetches in the loop (wrong results)
+#endif
+            {
+                fetch_geo(rn, pn, nx);
+                fetch_fld(rn, pn, nx);
+            }
             solve_item(rm, pm, ny);
             rm = rn;
             pm = pn;

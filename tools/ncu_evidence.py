@@ -1,0 +1,159 @@
+#!/usr/bin/env python3
+"""Per-kernel ncu evidence (north star: "each kernel is evidenced by ncu counters: achieved HBM
+GB/s against B200 peak, and bytes moved per pixel per frame against the minimal field traffic").
+
+    python tools/ncu_evidence.py REPORT.ncu-rep --kernel REGEX --pixels N --algo-bytes B --algo-ops OPS
+        --tag r02_cfg2 [--peaks MEASURED_PEAKS.json]
+
+For every captured launch of the kernels matching REGEX: duration, DRAM bytes (read + write, per
+launch and per pixel) against the algorithmic bytes per pixel, DRAM GB/s against the measured HBM
+peak, FP32 lane-operations per pixel counted from the SASS source page (executed warp-level
+instructions x 32, paired f32x2 ops FADD2 / FMUL2 / FFMA2 counted twice) against the algorithmic
+count, thread-instructions per pixel, IPC and pipe utilisation.  Writes profiles/<tag>_<kernel>.json
+and appends a row to profiles/<tag>_evidence.md.
+"""
+import argparse
+import csv
+import json
+import os
+import re
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+FP1 = {"FADD", "FMUL", "FFMA"}
+FP2 = {"FADD2", "FMUL2", "FFMA2"}
+RAW = {
+    "duration_ns": "gpu__time_duration.sum",
+    "dram_read_bytes": "dram__bytes_read.sum",
+    "dram_write_bytes": "dram__bytes_write.sum",
+    "sm_cycles_active_avg": "sm__cycles_active.avg",
+    "elapsed_cycles": "gpc__cycles_elapsed.max",
+    "inst_executed": "smsp__inst_executed.sum",
+    "ipc_active": "sm__inst_executed.avg.per_cycle_active",
+    "pipe_fma_pct": "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+    "pipe_alu_pct": "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
+    "pipe_lsu_pct": "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
+    "smem_wavefronts": "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
+    "smem_bank_conflicts": "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
+    "registers_per_thread": "launch__registers_per_thread",
+    "grid_size": "launch__grid_size",
+    "block_size": "launch__block_size",
+    "l2_hit_pct": "lts__t_sector_hit_rate.pct",
+}
+SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1, "us": 1e3, "usecond": 1e3, "nsecond": 1,
+         "ms": 1e6, "msecond": 1e6}
+
+
+def ncu(*args):
+    return subprocess.run(["ncu", *args], capture_output=True, text=True).stdout
+
+
+def raw(rep):
+    rows = list(csv.reader(ncu("-i", rep, "--page", "raw", "--csv").splitlines()))
+    return rows[0], rows[1], rows[2:]
+
+
+def fp_ops(rep, kname_regex):
+    """(fp32 lane-ops, thread instructions) per launch from the SASS source page, averaged over the
+    captured launches of the kernel."""
+    txt = ncu("-i", rep, "--page", "source", "--csv", "--print-source", "sass", "-k", f"regex:{kname_regex}")
+    lines = txt.splitlines()
+    fp, ti, nlaunch = 0, 0, 0
+    header = None
+    for ln in csv.reader(lines):
+        if not ln:
+            continue
+        if "Source" in ln and "Instructions Executed" in ln:
+            header = ln
+            nlaunch += 1
+            continue
+        if header is None or len(ln) != len(header):
+            continue
+        src = ln[header.index("Source")].strip()
+        try:
+            n = int(ln[header.index("Instructions Executed")] or 0)
+        except ValueError:
+            continue
+        toks = src.split()
+        if not toks:
+            continue
+        op = toks[1] if toks[0].startswith("@") and len(toks) > 1 else toks[0]
+        base = op.split(".")[0]
+        ti += 32 * n
+        if base in FP2:
+            fp += 64 * n
+        elif base in FP1:
+            fp += 32 * n
+    nlaunch = max(1, nlaunch)
+    return fp / nlaunch, ti / nlaunch
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("report")
+    ap.add_argument("--kernel", required=True, help="regex on the kernel name")
+    ap.add_argument("--pixels", type=float, required=True, help="pixels one launch processes (B x H x W)")
+    ap.add_argument("--algo-bytes", type=float, default=None, help="algorithmic bytes per pixel of this kernel")
+    ap.add_argument("--algo-ops", type=float, default=None, help="algorithmic FP32 ops per pixel per launch")
+    ap.add_argument("--tag", required=True)
+    ap.add_argument("--label", default=None)
+    ap.add_argument("--peaks", default=os.path.join(ROOT, "MEASURED_PEAKS.json"))
+    a = ap.parse_args()
+    pk = json.load(open(a.peaks)) if os.path.exists(a.peaks) else {}
+    hbm = pk.get("hbm_gbs", 6650.0)
+    h, units, vals = raw(a.report)
+    ki = h.index("Kernel Name")
+    caps = []
+    for v in vals:
+        if not re.search(a.kernel, v[ki]):
+            continue
+        d = {"kernel": v[ki].split("(")[0].replace("void ", "").replace("<unnamed>::", "")}
+        for k, m in RAW.items():
+            if m in h:
+                i = h.index(m)
+                try:
+                    d[k] = float(v[i].replace(",", "")) * SCALE.get(units[i], 1)
+                except ValueError:
+                    pass
+        caps.append(d)
+    if not caps:
+        print("no launches of", a.kernel, file=sys.stderr)
+        return 1
+    fp, ti = fp_ops(a.report, a.kernel)
+    avg = {k: sum(c[k] for c in caps if k in c) / len([c for c in caps if k in c])
+           for k in caps[0] if isinstance(caps[0][k], float)}
+    dram = avg.get("dram_read_bytes", 0) + avg.get("dram_write_bytes", 0)
+    t_s = avg["duration_ns"] * 1e-9
+    out = {
+        "report": os.path.basename(a.report), "kernel": caps[0]["kernel"], "label": a.label, "launches": len(caps),
+        "pixels_per_launch": a.pixels, "per_launch": avg,
+        "dram_bytes_per_launch": dram, "dram_bytes_per_px": dram / a.pixels,
+        "algo_bytes_per_px": a.algo_bytes,
+        "dram_gbs": dram / t_s / 1e9, "hbm_peak_gbs": hbm, "dram_frac_of_peak": dram / t_s / 1e9 / hbm,
+        "fp32_lane_ops_per_px": fp / a.pixels, "algo_fp32_ops_per_px": a.algo_ops,
+        "thread_inst_per_px": ti / a.pixels,
+        "note": "ncu --set full --clock-control none (replayed, cache-flushed: cold L2; durations are "
+                "serialised single launches); FP32 lane-ops from the SASS source page (FADD2/FMUL2/FFMA2 x2)",
+    }
+    name = re.sub(r"[^A-Za-z0-9_]+", "_", caps[0]["kernel"]).strip("_")
+    os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
+    json.dump(out, open(os.path.join(ROOT, "profiles", f"{a.tag}_{name}.json"), "w"), indent=1)
+    md = os.path.join(ROOT, "profiles", f"{a.tag}_evidence.md")
+    new = not os.path.exists(md)
+    with open(md, "a") as fh:
+        if new:
+            fh.write("| workload | kernel | launches | us (cold) | DRAM B/px | algo B/px | DRAM GB/s (frac) | "
+                     "FP32 ops/px | algo ops/px | thread-inst/px | IPC | FMA pipe % | ALU pipe % |\n")
+            fh.write("|---|---|---|---|---|---|---|---|---|---|---|---|---|\n")
+        fh.write(f"| {a.label or a.tag} | {caps[0]['kernel']} | {len(caps)} | {avg['duration_ns'] / 1e3:.2f} | "
+                 f"{dram / a.pixels:.1f} | {a.algo_bytes if a.algo_bytes is not None else '-'} | "
+                 f"{dram / t_s / 1e9:.0f} ({dram / t_s / 1e9 / hbm:.3f}) | {fp / a.pixels:.0f} | "
+                 f"{a.algo_ops if a.algo_ops is not None else '-'} | {ti / a.pixels:.0f} | "
+                 f"{avg.get('ipc_active', 0):.2f} | {avg.get('pipe_fma_pct', 0):.0f} | {avg.get('pipe_alu_pct', 0):.0f} |\n")
+    print(json.dumps(out, indent=1))
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())
