@@ -9,7 +9,8 @@ For every captured launch of the kernels matching REGEX: duration, DRAM bytes (r
 launch and per pixel) against the algorithmic bytes per pixel, DRAM GB/s against the measured HBM
 peak, FP32 lane-operations per pixel counted from the SASS source page (executed warp-level
 instructions x 32, paired f32x2 ops FADD2 / FMUL2 / FFMA2 counted twice) against the algorithmic
-count, thread-instructions per pixel, IPC and pipe utilisation.  Writes profiles/<tag>_<kernel>.json
+count (predicated-on thread instructions), thread-instructions per pixel, IPC and pipe
+utilisation.  Writes profiles/<tag>_<kernel>.json
 and appends a row to profiles/<tag>_evidence.md.
 """
 import argparse
@@ -55,24 +56,30 @@ def raw(rep):
 
 
 def fp_ops(rep, kname_regex):
-    """(fp32 lane-ops, thread instructions) per launch from the SASS source page, averaged over the
-    captured launches of the kernel."""
-    txt = ncu("-i", rep, "--page", "source", "--csv", "--print-source", "sass", "-k", f"regex:{kname_regex}")
-    lines = txt.splitlines()
+    """(fp32 lane-ops, thread instructions) per launch from the SASS source page (predicated-on
+    thread instructions; paired f32x2 ops count twice), averaged over the captured launches of
+    the kernels whose name matches (template casts like "(int)7" normalised to "7")."""
+    txt = ncu("-i", rep, "--page", "source", "--csv", "--print-source", "sass")
     fp, ti, nlaunch = 0, 0, 0
-    header = None
-    for ln in csv.reader(lines):
+    header, on = None, False
+    for ln in csv.reader(txt.splitlines()):
         if not ln:
             continue
-        if "Source" in ln and "Instructions Executed" in ln:
-            header = ln
-            nlaunch += 1
+        if ln[0] == "Kernel Name":
+            name = re.sub(r"\((int|bool|unsigned int|long)\)", "", ln[1])
+            on = re.search(kname_regex, name) is not None
+            nlaunch += 1 if on else 0
+            header = None
             continue
-        if header is None or len(ln) != len(header):
+        if ln[0] == "Address":
+            header = ln
+            continue
+        if not on or header is None or len(ln) != len(header):
             continue
         src = ln[header.index("Source")].strip()
+        col = "Predicated-On Thread Instructions Executed"
         try:
-            n = int(ln[header.index("Instructions Executed")] or 0)
+            n = int(ln[header.index(col)] or 0) if col in header else 32 * int(ln[header.index("Instructions Executed")] or 0)
         except ValueError:
             continue
         toks = src.split()
@@ -80,11 +87,11 @@ def fp_ops(rep, kname_regex):
             continue
         op = toks[1] if toks[0].startswith("@") and len(toks) > 1 else toks[0]
         base = op.split(".")[0]
-        ti += 32 * n
+        ti += n
         if base in FP2:
-            fp += 64 * n
+            fp += 2 * n
         elif base in FP1:
-            fp += 32 * n
+            fp += n
     nlaunch = max(1, nlaunch)
     return fp / nlaunch, ti / nlaunch
 
