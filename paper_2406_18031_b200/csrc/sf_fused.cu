@@ -74,6 +74,8 @@ struct FusedArgs {
     CUtensorMap tmY;    // [B][H][W] brightness, box 64 x 72 x 1
     CUtensorMap tmD;    // [B][H][W] depth, box 64 x 72 x 1
     int tma;            // 1: stage e / Y / depth with TMA (needs W % 4 == 0, 16-byte aligned bases)
+    int flush;          // k_trans: regions flush with the grid border where the grid is large enough
+    int onebody;        // k_trans A/B: interior CTAs on the COLFIX instantiation
     int y16;            // 1: Y and depth bases 16-byte aligned (the cp.async fallback may copy 16 bytes)
     int dbg_skip;       // timing experiments only (SF_DEBUG_SKIP): 1 = skip transport, 2 = skip update,
                         // 4 = no e TMA, 8 = no Y/depth TMA, 16 = no field / s loads, 32 = exit at entry,
@@ -123,12 +125,17 @@ struct Cfg {
 // EREG: the lane's e1 / e2 (ER[0..2] = e1.xyz, ER[3..5] = e2.xyz, cell-paired) are held in
 // registers instead of being read from the shared e planes each pass, and the run-end rows' v is
 // exchanged through the row buffer (as a fifth component) instead of being recomputed from e2.
-template <int K, int NWY, int RULE, bool CLAMP, int NF = 4, bool EDGE = true, bool IMU = true, bool EREG = false>
+// COLFIX: the region's first / last column is the grid's first / last column (fixL / fixR): the
+// replicate border is applied in the column pass itself -- lane 0's cell 0 and lane 31's cell 1 take
+// their own u and their own value as the outside neighbour's -- instead of through replica cells.
+template <int K, int NWY, int RULE, bool CLAMP, int NF = 4, bool EDGE = true, bool IMU = true, bool EREG = false,
+          bool COLFIX = false>
 __device__ __forceinline__ void transport_passes(const FrameParams& f, int M, float2 (&W)[NF][K], const float2 (&SX)[K],
                                                  const float2 (&SY)[K], const float2 (&SZ)[K], float (&mx)[K],
                                                  const float* Es, float2* XB0, int lane, int wy, int cmin, int cmax,
                                                  int rmin, int rmax, int dbg, const float* Ss = nullptr,
-                                                 const float2 (*ER)[K] = nullptr) {
+                                                 const float2 (*ER)[K] = nullptr, bool fixL = false,
+                                                 bool fixR = false) {
     using C = Cfg<K, NWY>;
     constexpr int RW = C::RW, P = C::P, RH = C::RH;
     // NF = 4: (w, rho), all dilated.  NF = 8 (pyramid bottom level): (w, dw, rho, Yhat), the last
@@ -158,6 +165,7 @@ __device__ __forceinline__ void transport_passes(const FrameParams& f, int M, fl
     };
     const float2 T2 = make_float2(-f.dt, -f.dt), SG = make_float2(f.sigma, f.sigma);
     const int srcL = lane - 1, srcR = lane + 1;
+    const bool eL = COLFIX && fixL && lane == 0, eR = COLFIX && fixR && lane == 31;
     // replica bookkeeping (block-uniform except for the lane / k tests)
     const bool repL = EDGE && cmin > 0, repR = EDGE && cmax < RW - 1, repT = EDGE && rmin > 0,
                repB = EDGE && rmax < RH - 1;
@@ -192,17 +200,23 @@ __device__ __forceinline__ void transport_passes(const FrameParams& f, int M, fl
 #pragma unroll
         for (int k = 0; k < K; ++k) {
             const float2 u = dot2(e1v(k, 0), e1v(k, 1), e1v(k, 2), W[0][k], W[1][k], W[2][k]);
-            const float uL = __shfl_up_sync(FULL, u.y, 1);    // lane-1's cell 1 = left of cell 0
-            const float uR = __shfl_down_sync(FULL, u.x, 1);  // lane+1's cell 0 = right of cell 1
+            float uL = __shfl_up_sync(FULL, u.y, 1);    // lane-1's cell 1 = left of cell 0
+            float uR = __shfl_down_sync(FULL, u.x, 1);  // lane+1's cell 0 = right of cell 1
+            if (COLFIX) {  // grid edge at the region edge: the outside neighbour is the cell itself
+                uL = eL ? u.x : uL;
+                uR = eR ? u.y : uR;
+            }
             bool p0, p1;
             const float2 A = flow(k, dominant(uL, u.y, RULE), dominant(u.x, uR, RULE), p0, p1);
             // upwind value by per-lane source: cell 0 takes lane-1's cell 1 (u_hat > 0) or its own
             // cell 1; cell 1 takes its own cell 0 (u_hat > 0) or lane+1's cell 0
             const int s0 = p0 ? srcL : lane, s1 = p1 ? lane : srcR;
+            const bool own0 = COLFIX && eL && p0, own1 = COLFIX && eR && !p1;
             const float2 q = mul2(SG, sdot(k));
 #pragma unroll
             for (int c = 0; c < NF; ++c) {
-                const float2 fu = make_float2(__shfl_sync(FULL, W[c][k].y, s0), __shfl_sync(FULL, W[c][k].x, s1));
+                float2 fu = make_float2(__shfl_sync(FULL, W[c][k].y, s0), __shfl_sync(FULL, W[c][k].x, s1));
+                if (COLFIX) fu = make_float2(own0 ? W[c][k].x : fu.x, own1 ? W[c][k].y : fu.y);
                 W[c][k] = c < ND ? tr2(W[c][k], fu, A, q, T2) : fma2(T2, mul2(A, sub2(W[c][k], fu)), W[c][k]);
             }
         }
@@ -870,7 +884,18 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_trans(const __grid_constant__ F
     const int tid = threadIdx.x, lane = tid & 31, wy = tid >> 5;
     const int c0 = 2 * lane, r0 = K * wy;
     const int b = blockIdx.z, R = a.R, TH = a.TH, TW = a.TW;
-    const int gi0 = blockIdx.y * TH - R, gj0 = blockIdx.x * TW - R;
+    // Row placement: the first and last tile rows put the region flush with the grid's top / bottom
+    // row (when the grid is at least RH rows tall), so that the grid border IS the region border:
+    // the row pass's run-end logic then replicates there by itself (the first / last warp uses its
+    // own edge row as the neighbour), no row replica is needed, and top / bottom CTAs run the
+    // interior instantiation.  The tile keeps >= R rows of halo towards the grid interior.
+    // Columns likewise (the column pass then replicates at lanes 0 / 31, COLFIX) when the grid is
+    // at least RW wide and the right-flush origin keeps the TMA box 16-byte aligned.
+    const int ti0 = blockIdx.y * TH, tj0 = blockIdx.x * TW;
+    const int gi0 = a.flush && f.H >= RH ? min(max(ti0 - R, 0), f.H - RH) : ti0 - R;
+    const bool colfit = a.flush && f.W >= RW && (f.W & 3) == 0;
+    const int gj0 = colfit ? min(max(tj0 - R, 0), f.W - RW) : tj0 - R;
+    const int Rr = ti0 - gi0, Rc = tj0 - gj0;  // tile rows / columns in the region: [Rr, Rr + TH) x [Rc, Rc + TW)
     const int cmin = max(0, -gj0), cmax = min(RW - 1, f.W - 1 - gj0);
     const int rmin = max(0, -gi0), rmax = min(RH - 1, f.H - 1 - gi0);
     const bool edge = cmin > 0 || cmax < RW - 1 || rmin > 0 || rmax < RH - 1;  // block-uniform
@@ -973,24 +998,31 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_trans(const __grid_constant__ F
 #pragma unroll
             for (int k = 0; k < K; ++k) ER[q][k] = *reinterpret_cast<const float2*>(Es + q * P + (r0 + k) * RW + c0);
     }
+    const bool fixL = gj0 == 0, fixR = gj0 + RW == f.W;  // (block-uniform)
     if (f.imu)  // (the inertial stage only where it is on: it costs registers and scheduling freedom)
-        transport_passes<K, NWY, RULE, CLAMP, 4, true, true, EREG>(f, a.M, W, SX, SY, SZ, mx, Es, XB0, lane, wy, cmin,
-                                                                   cmax, rmin, rmax, kdbg, nullptr, ER);
-    else if (edge)
-        transport_passes<K, NWY, RULE, CLAMP, 4, true, false, EREG>(f, a.M, W, SX, SY, SZ, mx, Es, XB0, lane, wy, cmin,
-                                                                    cmax, rmin, rmax, kdbg, nullptr, ER);
+        transport_passes<K, NWY, RULE, CLAMP, 4, true, true, EREG, true>(f, a.M, W, SX, SY, SZ, mx, Es, XB0, lane, wy,
+                                                                         cmin, cmax, rmin, rmax, kdbg, nullptr, ER,
+                                                                         fixL, fixR);
+    else if (edge)  // (grids narrower than the region: replica cells; a flush side by COLFIX)
+        transport_passes<K, NWY, RULE, CLAMP, 4, true, false, EREG, true>(f, a.M, W, SX, SY, SZ, mx, Es, XB0, lane, wy,
+                                                                          cmin, cmax, rmin, rmax, kdbg, nullptr, ER,
+                                                                          fixL, fixR);
+    else if (fixL || fixR || a.onebody)  // (onebody: A/B switch, interior CTAs on the same body)
+        transport_passes<K, NWY, RULE, CLAMP, 4, false, false, EREG, true>(f, a.M, W, SX, SY, SZ, mx, Es, XB0, lane, wy,
+                                                                           cmin, cmax, rmin, rmax, kdbg, nullptr, ER,
+                                                                           fixL, fixR);
     else
         transport_passes<K, NWY, RULE, CLAMP, 4, false, false, EREG>(f, a.M, W, SX, SY, SZ, mx, Es, XB0, lane, wy,
                                                                      cmin, cmax, rmin, rmax, kdbg, nullptr, ER);
     SF_PROF();  // 2: transport
     // ---- flags from tile cells (exact at every pass; |u_hat| before the clamp) and the tile store
     unsigned fl = 0;
-    const bool t0 = c0 >= R && c0 < R + TW && c0 >= cmin && c0 <= cmax;
-    const bool t1 = c0 + 1 >= R && c0 + 1 < R + TW && c0 + 1 >= cmin && c0 + 1 <= cmax;
+    const bool t0 = c0 >= Rc && c0 < Rc + TW && c0 >= cmin && c0 <= cmax;
+    const bool t1 = c0 + 1 >= Rc && c0 + 1 < Rc + TW && c0 + 1 >= cmin && c0 + 1 <= cmax;
 #pragma unroll
     for (int k = 0; k < K; ++k) {
         const int r = r0 + k;
-        if (r >= R && r < R + TH && r >= rmin && r <= rmax) {
+        if (r >= Rr && r < Rr + TH && r >= rmin && r <= rmax) {
             if (t0 && gi0 + r >= f.fr0 && gi0 + r < f.fr1) {  // (R, TW even: the pair is in or out together)
                 if (CLAMP) {
                     if (mx[k] > f.U) fl |= SF_FLAG_CLAMPED;
@@ -1049,7 +1081,12 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_low(const __grid_constant__ Low
     const int tid = threadIdx.x, lane = tid & 31, wy = tid >> 5;
     const int c0 = 2 * lane, r0 = K * wy;
     const int b = blockIdx.z, R = a.R, TH = a.TH, TW = a.TW;
-    const int gi0 = blockIdx.y * TH - R, gj0 = blockIdx.x * TW - R;
+    // region placement flush with the grid border where the grid is large enough (k_trans):
+    // replicate by the row pass's run ends and by COLFIX, no replica cells
+    const int ti0 = blockIdx.y * TH, tj0 = blockIdx.x * TW;
+    const int gi0 = f.H >= RH ? min(max(ti0 - R, 0), f.H - RH) : ti0 - R;
+    const int gj0 = (f.W >= RW && (f.W & 3) == 0) ? min(max(tj0 - R, 0), f.W - RW) : tj0 - R;
+    const int Rr = ti0 - gi0, Rc = tj0 - gj0;
     const int cmin = max(0, -gj0), cmax = min(RW - 1, f.W - 1 - gj0);
     const int rmin = max(0, -gi0), rmax = min(RH - 1, f.H - 1 - gi0);
     const size_t HW = (size_t)f.H * f.W, plane = (size_t)b * HW;
@@ -1122,14 +1159,24 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_low(const __grid_constant__ Low
     }
     // (replica e cells next to grid edges arrive with the load: padded E, reading 10)
     __syncthreads();
-    transport_passes<K, NWY, RULE, CLAMP, 8>(f, a.M, W, SX, SY, SZ, mx, Es, XB0, lane, wy, cmin, cmax, rmin, rmax, 0,
-                                             Ss);
+    const bool fixL = gj0 == 0, fixR = gj0 + RW == f.W;
+    if (cmin > 0 || cmax < RW - 1 || rmin > 0 || rmax < RH - 1)
+        transport_passes<K, NWY, RULE, CLAMP, 8, true, false, false, true>(f, a.M, W, SX, SY, SZ, mx, Es, XB0, lane, wy,
+                                                                           cmin, cmax, rmin, rmax, 0, Ss, nullptr, fixL,
+                                                                           fixR);
+    else if (fixL || fixR)
+        transport_passes<K, NWY, RULE, CLAMP, 8, false, false, false, true>(f, a.M, W, SX, SY, SZ, mx, Es, XB0, lane,
+                                                                            wy, cmin, cmax, rmin, rmax, 0, Ss, nullptr,
+                                                                            fixL, fixR);
+    else
+        transport_passes<K, NWY, RULE, CLAMP, 8, false, false>(f, a.M, W, SX, SY, SZ, mx, Es, XB0, lane, wy, cmin, cmax,
+                                                               rmin, rmax, 0, Ss);
     unsigned fl = 0;
-    const bool tcol = c0 >= R && c0 < R + TW && c0 >= cmin && c0 <= cmax;
+    const bool tcol = c0 >= Rc && c0 < Rc + TW && c0 >= cmin && c0 <= cmax;
 #pragma unroll
     for (int k = 0; k < K; ++k) {
         const int r = r0 + k;
-        if (r >= R && r < R + TH && r >= rmin && r <= rmax) {
+        if (r >= Rr && r < Rr + TH && r >= rmin && r <= rmax) {
             if (tcol) {
                 if (CLAMP) {
                     if (mx[k] > f.U) fl |= SF_FLAG_CLAMPED;
@@ -1138,11 +1185,11 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_low(const __grid_constant__ Low
                 }
             }
             const size_t g = plane + (size_t)(gi0 + r) * f.W + (gj0 + c0);
-            if (c0 >= R && c0 < R + TW && c0 >= cmin && c0 <= cmax) {
+            if (c0 >= Rc && c0 < Rc + TW && c0 >= cmin && c0 <= cmax) {
                 a.foutW[g] = make_float4(W[0][k].x, W[1][k].x, W[2][k].x, W[7][k].x);
                 a.foutA[g] = make_float4(W[3][k].x, W[4][k].x, W[5][k].x, W[6][k].x);
             }
-            if (c0 + 1 >= R && c0 + 1 < R + TW && c0 + 1 >= cmin && c0 + 1 <= cmax) {
+            if (c0 + 1 >= Rc && c0 + 1 < Rc + TW && c0 + 1 >= cmin && c0 + 1 <= cmax) {
                 a.foutW[g + 1] = make_float4(W[0][k].y, W[1][k].y, W[2][k].y, W[7][k].y);
                 a.foutA[g + 1] = make_float4(W[3][k].y, W[4][k].y, W[5][k].y, W[6][k].y);
             }
@@ -1456,6 +1503,8 @@ cudaError_t launch_trans(sf_ctx* c, const float* Y, const float* D) {
         a.TW = TC::RW - 2 * a.R;
         a.TH = TC::RH - 2 * a.R;
         a.tma = !no_tma() && encode3d(&a.tmE, c->E, sf_ew(f.W), sf_eh(f.H), 6, TC::RW, TC::RH, 3);
+        a.flush = getenv("SF_NO_FLUSH") ? 0 : 1;  // (A/B switches)
+        a.onebody = getenv("SF_ONEBODY") ? 1 : 0;
         a.fin = src;
         a.fout = (l == L - 1) ? c->pred : (((L - 1 - l) & 1) ? c->tmp : c->tmp2);
         const bool pf = l == 0 && Y && D && ((reinterpret_cast<uintptr_t>(Y) | reinterpret_cast<uintptr_t>(D)) & 15) == 0;

@@ -71,15 +71,19 @@ __device__ __forceinline__ void fill_planes(float* p, int P, int PW, int PH, int
     rb = min(rb, PH - 1);
     ca = max(ca, 0);
     cb = min(cb, PW - 1);
+    // one band: warps stride over its rows, lanes over its columns (no index division)
+    const int wid = tid >> 5, ln = tid & 31;
     auto band = [&](int r0, int r1, int c0, int c1) {
-        const int nc = c1 - c0 + 1, nr = r1 - r0 + 1;
-        if (nc <= 0 || nr <= 0) return;
+        if (c1 < c0 || r1 < r0) return;
 #pragma unroll 1
-        for (int t = tid; t < nc * nr; t += UPD_NT) {
-            const int q = t / nc, r = r0 + q, c = c0 + t - q * nc;
-            const int from = iclamp(r, rmin, rmax) * PW + iclamp(c, cmin, cmax), to = r * PW + c;
+        for (int r = r0 + wid; r <= r1; r += UPD_NT / 32) {
+            const int fr = iclamp(r, rmin, rmax) * PW;
+#pragma unroll 1
+            for (int c = c0 + ln; c <= c1; c += 32) {
+                const int from = fr + iclamp(c, cmin, cmax), to = r * PW + c;
 #pragma unroll
-            for (int q = 0; q < NP; ++q) p[q * P + to] = p[q * P + from];
+                for (int q = 0; q < NP; ++q) p[q * P + to] = p[q * P + from];
+            }
         }
     };
     band(ra, min(rb, rmin - 1), ca, cb);            // rows above the grid (with corners)

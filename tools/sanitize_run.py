@@ -1,7 +1,8 @@
 #!/usr/bin/env python3
-"""Small workloads for compute-sanitizer (tools/gpu_sanitize.sh): the fused and per-pass H = 1
-paths on ragged multi-CTA grids (interior, edge and corner CTAs; cp.async and TMA staging), the pyramid, the input
-mapping and the evaluation -- each compared with the oracle so a run is also a parity check."""
+"""Small workloads for compute-sanitizer (tools/gpu_sanitize.sh): the fused (k_trans + k_upd) and
+per-pass H = 1 paths on ragged multi-CTA grids (interior, edge and corner CTAs; regions flush with
+the grid border and replica cells; cp.async and TMA staging) and the pyramid (both bottom-level
+updates) -- each compared with the oracle so a run is also a parity check."""
 import os
 import sys
 
@@ -51,3 +52,6 @@ if __name__ == "__main__":
         h1(sf.SF_KERNEL_PASSES, 150, 130)
     if "pyramid" in which:
         pyramid()
+        os.environ["SF_UPD_LOW_FUSED"] = "1"  # the bottom-level update by k_upd
+        pyramid()
+        del os.environ["SF_UPD_LOW_FUSED"]
