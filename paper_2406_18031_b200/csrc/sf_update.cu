@@ -138,6 +138,7 @@ __global__ void __launch_bounds__(UPD_NT, 1) k_upd(const __grid_constant__ UpdAr
             tma_load_3d(Ys, &a.tmY, oj, oi, b, bar);
             tma_load_3d(RHs, &a.tmD, oj, oi, b, bar);
         }
+        __syncthreads();  // the barrier's initialisation is visible to every waiting thread
     } else {
         SF_FOR_RECT(r, c, 0, PH - 1, lc0, lc0 + ncl - 1, UPD_NT, tid) {
             const size_t g = pl + (size_t)iclamp(oi + r, 0, f.H - 1) * f.W + iclamp(oj + c, 0, f.W - 1);
