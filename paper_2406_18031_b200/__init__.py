@@ -13,7 +13,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libsf.so")
+# SF_LIB: an alternative build of the same library (A/B measurements of two builds in one run)
+LIB_PATH = os.environ.get("SF_LIB") or os.path.join(HERE, "libsf.so")
 
 SF_OK, SF_E_DATA, SF_E_STABILITY, SF_E_CONFIG, SF_E_STATE, SF_E_CUDA, SF_E_NCCL, SF_E_UNSUPPORTED = 0, 2, 3, 4, 5, 6, 7, 8
 SF_DOM_LARGEST, SF_DOM_PRINTED = 0, 1

@@ -13,9 +13,9 @@
 // in-grid cell (edge CTAs only).
 //   stage 0: Y, depth -> planes (two TMA tensor copies of the whole plane, issued before the wait
 //            on the transport kernel: they are the caller's inputs, and the transport kernel has
-//            prefetched them into L2; edge CTAs then replace the zero-filled out-of-grid cells by
-//            their clamped cell; cp.async with clamped indices without TMA); the first solve
-//            item's global inputs fetched;
+//            prefetched them into L2; edge CTAs, whose plane reaches outside the grid, and builds
+//            without TMA: cp.async with replicate-clamped indices); the first solve item's global
+//            inputs fetched;
 //   stage 1: rhohat plane (NaN = invalid) + horizontal taps HG = hz(g, Y), HH = hz(h, Y);
 //   stage 2: per SR pair of cells: vertical taps -> Yhat', beta_1, beta_2; rho one-sided
 //            differences; ghat, m; c_Y, c_rho; LDL^T solve -> w_LS planes; Yhat^{k+1} of tile cells
@@ -57,8 +57,8 @@ struct UpdArgs {
     int dbg;                           // SF_DEBUG_SKIP (debug builds only): 8192 = phase profile
 };
 
-// 14 warps, one CTA per SM (<= 146 registers); the 48 x 40 tile's 1344 solve pairs are exactly 3
-// per thread
+// 14 warps, one CTA per SM (<= 128 registers: 4 warps on the busiest scheduler x 32 x 128 = its 16K
+// registers); the 48 x 40 tile's 1344 solve pairs are exactly 3 per thread
 constexpr int UPD_NT = 448;
 
 // Replicate fill (reading 10) of the out-of-grid cells of [ra, rb] x [ca, cb] (clipped to the
@@ -130,7 +130,10 @@ __global__ void __launch_bounds__(UPD_NT, 1) k_upd(const __grid_constant__ UpdAr
 
     // ---------------- stage 0: Y and depth (caller inputs, prefetched into L2 by the transport
     // kernel): the whole plane by TMA, or the used columns by cp.async with clamped indices
-    if (a.tma) {
+    // edge CTAs (the plane reaches outside the grid) take the clamped cp.async path: no zero-filled
+    // cells to replace afterwards
+    const bool ydtma = a.tma && !(rmin > 0 || rmax < PH - 1 || cmin > 0 || cmax < PW - 1);
+    if (ydtma) {
         if (tid == 0) {
             mbar_init(bar, 1);
             asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -183,12 +186,8 @@ __global__ void __launch_bounds__(UPD_NT, 1) k_upd(const __grid_constant__ UpdAr
     griddep_launch_dependents();
     SF_PROF();  // 0: stage-0 issue + griddep
     fetch_fld(rn, pn, nx);
-    if (a.tma) {
+    if (ydtma) {
         mbar_wait(bar, 0);
-        if (rmin > 0 || rmax < PH - 1 || cmin > 0 || cmax < PW - 1) {  // out-of-grid cells arrived as zeros
-            __syncthreads();
-            fill_planes<2>(Ys, P, PW, PH, 0, PH - 1, 0, PW - 1, rmin, rmax, cmin, cmax, tid);
-        }
     } else {
         cp_async_wait<0>();
     }
