@@ -57,7 +57,7 @@ static void async_teardown(sf_ctx* c);
 static void free_ctx(sf_ctx* c) {
     if (!c) return;
     void* ptrs[] = {c->G0, c->G1, c->G2, c->E, c->state[0], c->state[1], c->pred, c->tmp, c->tmp2,
-                    c->yhat[0], c->yhat[1], c->HG, c->HH, c->flags, c->hY, c->hD, c->hw, c->hr, c->eval_part,
+                    c->yhat[0], c->yhat[1], c->HG, c->HH, c->rk, c->flags, c->hY, c->hD, c->hw, c->hr, c->eval_part,
                     c->Wf[0], c->Wf[1], c->Wpred, c->Wtmp, c->Y2, c->D2, c->mY, c->mD};
     for (void* p : ptrs)
         if (p) cudaFree(p);
@@ -191,6 +191,7 @@ extern "C" sf_status sf_create(const sf_config* cfg, const float* geometry, sf_c
               cudaMalloc(&c->yhat[1], nall * sizeof(float)) == cudaSuccess &&
               cudaMalloc(&c->HG, nall * sizeof(float)) == cudaSuccess &&
               cudaMalloc(&c->HH, nall * sizeof(float)) == cudaSuccess &&
+              cudaMalloc(&c->rk, nall * sizeof(float)) == cudaSuccess &&
               cudaMalloc(&c->flags, sizeof(unsigned)) == cudaSuccess;
     if (!ok) {
         free_ctx(c);
@@ -276,8 +277,8 @@ extern "C" sf_status sf_update(sf_ctx* c, const float* Y, const float* D) {
     }
     if (!c->pending) return SF_E_STATE;
     if (c->kernel == SF_KERNEL_FUSED)
-        SF_TRY(sf_launch_update_fused(c, Y, D, c->pred, reinterpret_cast<const float*>(c->state[c->cur]) + 3, 4,
-                                      c->yhat[c->cur], 1, c->state[1 - c->cur], c->yhat[1 - c->cur]));
+        SF_TRY(sf_launch_update_fused(c, Y, D, c->pred, c->rk, 1, c->yhat[c->cur], 1, c->state[1 - c->cur],
+                                      c->yhat[1 - c->cur]));  // (rho^k: written by sf_predict's k_trans)
     else
         SF_TRY(sf_launch_update_passes(c, Y, D, false));
     c->cur = 1 - c->cur;
@@ -353,8 +354,8 @@ extern "C" sf_status sf_step_timed(sf_ctx* c, const float* Y, const float* D, fl
         (sf_launch_spin(c, 100000) != cudaSuccess || cudaEventRecord(ev[0], c->stream) != cudaSuccess ||
          sf_launch_predict_fused(c, Y, D) != cudaSuccess ||
          cudaEventRecord(ev[1], c->stream) != cudaSuccess ||
-         sf_launch_update_fused(c, Y, D, c->pred, reinterpret_cast<const float*>(c->state[c->cur]) + 3, 4,
-                                c->yhat[c->cur], 1, c->state[1 - c->cur], c->yhat[1 - c->cur]) != cudaSuccess ||
+         sf_launch_update_fused(c, Y, D, c->pred, c->rk, 1, c->yhat[c->cur], 1, c->state[1 - c->cur],
+                                c->yhat[1 - c->cur]) != cudaSuccess ||
          cudaEventRecord(ev[2], c->stream) != cudaSuccess || cudaEventSynchronize(ev[2]) != cudaSuccess ||
          cudaEventElapsedTime(ms_predict, ev[0], ev[1]) != cudaSuccess ||
          cudaEventElapsedTime(ms_update, ev[1], ev[2]) != cudaSuccess))

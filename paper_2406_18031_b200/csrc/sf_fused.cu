@@ -94,6 +94,8 @@ struct FusedArgs {
     const float4* G2;   // e2
     const float* E;     // [6][H*W] (e1.xyz, e2.xyz planes)
     unsigned* flags;
+    float* rk;          // k_trans, first launch of a frame: rho^k of the tile cells -> [B][H][W] (k_upd's c_rho
+                        // reference, read there 4 bytes per cell); null otherwise
     FrameParams f;
     int M;    // substeps in this launch
     int upd;  // 1: run the update after the substeps
@@ -978,6 +980,19 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_trans(const __grid_constant__ F
         W[3][k] = make_float2(fa.w, fb.w);
     }
     griddep_launch_dependents();  // the update kernel's CTAs may start their geometry loads
+    const bool t0 = c0 >= Rc && c0 < Rc + TW && c0 >= cmin && c0 <= cmax;
+    const bool t1 = c0 + 1 >= Rc && c0 + 1 < Rc + TW && c0 + 1 >= cmin && c0 + 1 <= cmax;
+    if (a.rk) {  // rho^k of the tile cells for the update kernel (each grid cell written by one CTA)
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const int r = r0 + k;
+            if (r >= Rr && r < Rr + TH && r >= rmin && r <= rmax) {
+                const size_t g = plane + (size_t)(gi0 + r) * f.W + (gj0 + c0);
+                if (t0) a.rk[g] = W[3][k].x;
+                if (t1) a.rk[g + 1] = W[3][k].y;
+            }
+        }
+    }
     SF_PROF();  // 0: prologue (s, griddep, fields)
     if (a.tma) {
         mbar_wait(&bars[0], 0);
@@ -1017,8 +1032,6 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_trans(const __grid_constant__ F
     SF_PROF();  // 2: transport
     // ---- flags from tile cells (exact at every pass; |u_hat| before the clamp) and the tile store
     unsigned fl = 0;
-    const bool t0 = c0 >= Rc && c0 < Rc + TW && c0 >= cmin && c0 <= cmax;
-    const bool t1 = c0 + 1 >= Rc && c0 + 1 < Rc + TW && c0 + 1 >= cmin && c0 + 1 <= cmax;
 #pragma unroll
     for (int k = 0; k < K; ++k) {
         const int r = r0 + k;
@@ -1510,6 +1523,7 @@ cudaError_t launch_trans(sf_ctx* c, const float* Y, const float* D) {
         const bool pf = l == 0 && Y && D && ((reinterpret_cast<uintptr_t>(Y) | reinterpret_cast<uintptr_t>(D)) & 15) == 0;
         a.Y = pf ? Y : nullptr;  // L2 prefetch of the update's inputs by the first launch
         a.D = pf ? D : nullptr;
+        a.rk = l == 0 ? c->rk : nullptr;  // (state k is read by the first launch only)
         a.G0 = c->G0;
         a.E = c->E;
         a.flags = c->flags;
@@ -1582,8 +1596,8 @@ cudaError_t sf_launch_fused_step(sf_ctx* c, const float* Y, const float* D) {
     if (fused_mono()) return fused_cfg() == 1 ? launch_cfg<4, 18>(c, Y, D) : launch_cfg<6, 12>(c, Y, D);
     cudaError_t e = sf_launch_predict_fused(c, Y, D);
     if (e != cudaSuccess) return e;
-    return sf_launch_update_fused(c, Y, D, c->pred, reinterpret_cast<const float*>(c->state[c->cur]) + 3, 4,
-                                  c->yhat[c->cur], 1, c->state[1 - c->cur], c->yhat[1 - c->cur]);
+    return sf_launch_update_fused(c, Y, D, c->pred, c->rk, 1, c->yhat[c->cur], 1, c->state[1 - c->cur],
+                                  c->yhat[1 - c->cur]);
 }
 
 bool sf_low_fused_supported(const sf_ctx* c) {

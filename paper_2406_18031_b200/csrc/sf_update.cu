@@ -46,8 +46,10 @@ struct UpdArgs {
     const float* Y;            // [B][H][W] brightness
     const float* D;            // [B][H][W] depth (or inverse depth)
     const float4* G0;          // (s, d2)
-    const float4* G1;          // (e1, ds)
-    const float4* G2;          // (e2, 0)
+    const float* E;            // padded e planes [6][EH][EW] (e1.xyz, e2.xyz; cell (i, j) at (i + EPAD, j + EPAD))
+    int EW;                    // padded row length
+    size_t EP;                 // plane stride
+    int e8;                    // 1: EW even and E 8-byte aligned (a pair's e components by one 8-byte load)
     float4* out;               // (w^{k+1}, rho^{k+1})
     float* yout;               // Yhat^{k+1}
     unsigned* flags;
@@ -92,12 +94,13 @@ __device__ __forceinline__ void fill_planes(float* p, int P, int PW, int PH, int
     band(max(ra, rmin), min(rb, rmax), max(ca, cmax + 1), cb);  // right columns
 }
 
-// The global inputs of one solve item (a horizontal pair of SR cells).
+// The global inputs of one solve item (a horizontal pair of SR cells).  The directions e1, e2 come
+// from the padded planar E array (24 bytes per cell, a pair's component in one 8-byte load) rather
+// than the float4 G1 / G2 records (32 bytes per cell): the solve's loads are L2-throughput bound.
 struct SolveIn {
     float4 wa, wb;   // pred: (w^{k+}, rho^{k+})
     float4 sa, sb;   // G0: (s, d2)
-    float4 ea, eb;   // G1: e1
-    float4 fa, fb;   // G2: e2
+    float2 e[6];     // e1.x, e1.y, e1.z, e2.x, e2.y, e2.z of the pair
     float2 y, rk;    // Yhat and rho references
 };
 
@@ -167,10 +170,14 @@ __global__ void __launch_bounds__(UPD_NT, 1) k_upd(const __grid_constant__ UpdAr
         const size_t cell = (size_t)(oi + r) * f.W + (oj + c), d = c + 1 <= sch ? 1 : 0;  // ragged: the first cell again
         q.sa = __ldg(a.G0 + cell);
         q.sb = __ldg(a.G0 + cell + d);
-        q.ea = __ldg(a.G1 + cell);
-        q.eb = __ldg(a.G1 + cell + d);
-        q.fa = __ldg(a.G2 + cell);
-        q.fb = __ldg(a.G2 + cell + d);
+        const float* ep = a.E + (size_t)(oi + r + SF_EPAD) * a.EW + (oj + c + SF_EPAD);
+        if (a.e8) {  // (a ragged pair's second cell reads the padding: in bounds, unused)
+#pragma unroll
+            for (int p = 0; p < 6; ++p) q.e[p] = __ldg(reinterpret_cast<const float2*>(ep + p * a.EP));
+        } else {
+#pragma unroll
+            for (int p = 0; p < 6; ++p) q.e[p] = make_float2(__ldg(ep + p * a.EP), __ldg(ep + p * a.EP + d));
+        }
     };
     auto fetch_fld = [&](int r, int pc, SolveIn& q) {
         r = min(r, srh);
@@ -266,10 +273,8 @@ __global__ void __launch_bounds__(UPD_NT, 1) k_upd(const __grid_constant__ UpdAr
             const float2 br2 = make_float2(pick_side(rh.x, vc0, ru.x, !isnan(ru.x), rd.x, !isnan(rd.x)),
                                            pick_side(rh.y, vc1, ru.y, !isnan(ru.y), rd.y, !isnan(rd.y)));
             const float2 d2 = make_float2(cu.sa.w, cu.sb.w);
-            const float2 e1a[3] = {make_float2(cu.ea.x, cu.eb.x), make_float2(cu.ea.y, cu.eb.y),
-                                   make_float2(cu.ea.z, cu.eb.z)};
-            const float2 e2a[3] = {make_float2(cu.fa.x, cu.fb.x), make_float2(cu.fa.y, cu.fb.y),
-                                   make_float2(cu.fa.z, cu.fb.z)};
+            const float2 e1a[3] = {cu.e[0], cu.e[1], cu.e[2]};
+            const float2 e2a[3] = {cu.e[3], cu.e[4], cu.e[5]};
             const float2 sp[3] = {make_float2(cu.sa.x, cu.sb.x), make_float2(cu.sa.y, cu.sb.y),
                                   make_float2(cu.sa.z, cu.sb.z)};
             float2 gh[3], m[3];
@@ -489,8 +494,10 @@ cudaError_t sf_launch_update_fused(sf_ctx* c, const float* Y, const float* D, co
     a.Y = Y;
     a.D = D;
     a.G0 = c->G0;
-    a.G1 = c->G1;
-    a.G2 = c->G2;
+    a.E = c->E;
+    a.EW = sf_ew(f.W);
+    a.EP = (size_t)a.EW * sf_eh(f.H);
+    a.e8 = (a.EW % 2 == 0 && (reinterpret_cast<uintptr_t>(c->E) & 7) == 0) ? 1 : 0;
     a.out = out;
     a.yout = yout;
     a.flags = c->flags;
