@@ -15,7 +15,7 @@
 //            on the transport kernel: they are the caller's inputs, and the transport kernel has
 //            prefetched them into L2; edge CTAs, whose plane reaches outside the grid, and builds
 //            without TMA: cp.async with replicate-clamped indices); the first solve item's global
-//            inputs fetched;
+//            inputs fetched (the first two items);
 //   stage 1: rhohat plane (NaN = invalid) + horizontal taps HG = hz(g, Y), HH = hz(h, Y);
 //   stage 2: per SR pair of cells: vertical taps -> Yhat', beta_1, beta_2; rho one-sided
 //            differences; ghat, m; c_Y, c_rho; LDL^T solve -> w_LS planes; Yhat^{k+1} of tile cells
@@ -65,7 +65,9 @@ constexpr int UPD_NT = 448;
 
 // Replicate fill (reading 10) of the out-of-grid cells of [ra, rb] x [ca, cb] (clipped to the
 // plane) in NP planes (p, p + P, ...) of row stride PW: each takes the value of its clamped
-// in-grid cell.
+// in-grid cell.  The four out-of-grid bands (top and bottom rows with the corners, left and right
+// columns) are enumerated as one flat index range, so that every thread copies at most a cell or
+// two in one step (a few hundred cells in an edge CTA).
 template <int NP>
 __device__ __forceinline__ void fill_planes(float* p, int P, int PW, int PH, int ra, int rb, int ca, int cb, int rmin,
                                             int rmax, int cmin, int cmax, int tid) {
@@ -73,25 +75,33 @@ __device__ __forceinline__ void fill_planes(float* p, int P, int PW, int PH, int
     rb = min(rb, PH - 1);
     ca = max(ca, 0);
     cb = min(cb, PW - 1);
-    // one band: warps stride over its rows, lanes over its columns (no index division)
-    const int wid = tid >> 5, ln = tid & 31;
-    auto band = [&](int r0, int r1, int c0, int c1) {
-        if (c1 < c0 || r1 < r0) return;
+    const int mr0 = max(ra, rmin), mr1 = min(rb, rmax);  // the in-grid rows of the rectangle
+    // bands (first row, rows, first column, columns); empty bands count 0 cells
+    const int b0r = ra, b0n = max(0, min(rb, rmin - 1) - ra + 1);
+    const int b1r = max(ra, rmax + 1), b1n = max(0, rb - b1r + 1);
+    const int wc = max(0, cb - ca + 1), lc = max(0, min(cb, cmin - 1) - ca + 1);
+    const int rc0 = max(ca, cmax + 1), rcn = max(0, cb - rc0 + 1), mn = max(0, mr1 - mr0 + 1);
+    const int n0 = b0n * wc, n1 = n0 + b1n * wc, n2 = n1 + mn * lc, n3 = n2 + mn * rcn;
 #pragma unroll 1
-        for (int r = r0 + wid; r <= r1; r += UPD_NT / 32) {
-            const int fr = iclamp(r, rmin, rmax) * PW;
-#pragma unroll 1
-            for (int c = c0 + ln; c <= c1; c += 32) {
-                const int from = fr + iclamp(c, cmin, cmax), to = r * PW + c;
-#pragma unroll
-                for (int q = 0; q < NP; ++q) p[q * P + to] = p[q * P + from];
-            }
+    for (int t = tid; t < n3; t += UPD_NT) {
+        int r, c;
+        if (t < n1) {  // top / bottom rows
+            const int u = t < n0 ? t : t - n0, q = u / wc;
+            r = (t < n0 ? b0r : b1r) + q;
+            c = ca + u - q * wc;
+        } else if (t < n2) {  // left columns
+            const int u = t - n1, q = u / lc;
+            r = mr0 + q;
+            c = ca + u - q * lc;
+        } else {  // right columns
+            const int u = t - n2, q = u / rcn;
+            r = mr0 + q;
+            c = rc0 + u - q * rcn;
         }
-    };
-    band(ra, min(rb, rmin - 1), ca, cb);            // rows above the grid (with corners)
-    band(max(ra, rmax + 1), rb, ca, cb);            // rows below
-    band(max(ra, rmin), min(rb, rmax), ca, min(cb, cmin - 1));  // left columns
-    band(max(ra, rmin), min(rb, rmax), max(ca, cmax + 1), cb);  // right columns
+        const int from = iclamp(r, rmin, rmax) * PW + iclamp(c, cmin, cmax), to = r * PW + c;
+#pragma unroll
+        for (int k = 0; k < NP; ++k) p[k * P + to] = p[k * P + from];
+    }
 }
 
 // The global inputs of one solve item (a horizontal pair of SR cells).  The directions e1, e2 come
@@ -188,11 +198,22 @@ __global__ void __launch_bounds__(UPD_NT, 1) k_upd(const __grid_constant__ UpdAr
         q.y = make_float2(a.yref[ga * a.ys], a.yref[gb * a.ys]);
         q.rk = make_float2(a.rref[ga * a.rs], a.rref[gb * a.rs]);
     };
+    auto advance = [&](int& r, int& pc) {
+        r += pdr + ((pc + pdc >= np) ? 1 : 0);
+        pc = (pc + pdc >= np) ? pc + pdc - np : pc + pdc;
+    };
+    // the first two items' inputs are requested before the models run (the solve's loads are
+    // L2-throughput bound, the models are not): item 1 in nx, item 2 in ny
+    SolveIn ny;
+    int rm = rn, pm = pn;  // the item after (rn, pn)
+    advance(rm, pm);
     fetch_geo(rn, pn, nx);
+    fetch_geo(rm, pm, ny);
     griddep_wait();  // w^{k+} and the references come from the preceding kernels
     griddep_launch_dependents();
     SF_PROF();  // 0: stage-0 issue + griddep
     fetch_fld(rn, pn, nx);
+    fetch_fld(rm, pm, ny);
     if (ydtma) {
         mbar_wait(bar, 0);
     } else {
@@ -248,10 +269,6 @@ __global__ void __launch_bounds__(UPD_NT, 1) k_upd(const __grid_constant__ UpdAr
     // in-flight loads).
     {
         auto ld2 = [&](const float* p, int i) { return *reinterpret_cast<const float2*>(p + i); };
-        auto advance = [&](int& r, int& pc) {
-            r += pdr + ((pc + pdc >= np) ? 1 : 0);
-            pc = (pc + pdc >= np) ? pc + pdc - np : pc + pdc;
-        };
         auto solve_item = [&](int r, int pn_, const SolveIn& cu) {
             const int c = scl + 2 * pn_;
             const bool full = c + 1 <= sch;
@@ -312,18 +329,17 @@ __global__ void __launch_bounds__(UPD_NT, 1) k_upd(const __grid_constant__ UpdAr
                 if (bad && oi + r >= f.fr0 && oi + r < f.fr1) fl |= SF_FLAG_NONFINITE;
             }
         };
-        SolveIn ny;
-        int rm = rn, pm = pn;  // the item after (rn, pn)
-        advance(rm, pm);
+        bool first = true;  // (ny already holds item 2)
 #pragma unroll 1
         while (rn <= srh) {
 #ifdef SF_DEBUG_KNOBS
             if (!(a.dbg & 16))  // timing experiment: 16 = no global fetches in the loop (wrong results)
 #endif
-            {
+            if (!first) {
                 fetch_geo(rm, pm, ny);
                 fetch_fld(rm, pm, ny);
             }
+            first = false;
             solve_item(rn, pn, nx);
             if (rm > srh) break;
             rn = rm;
