@@ -94,6 +94,7 @@ struct FusedArgs {
     const float4* G2;   // e2
     const float* E;     // [6][H*W] (e1.xyz, e2.xyz planes)
     unsigned* flags;
+    int dslot;          // debug builds: trace slot (frame & 3)
     float* rk;          // k_trans, first launch of a frame: rho^k of the tile cells -> [B][H][W] (k_upd's c_rho
                         // reference, read there 4 bytes per cell); null otherwise
     FrameParams f;
@@ -873,6 +874,8 @@ struct TransCfg {
 };
 
 // EREG: e1 / e2 of the lane's cells held in registers for the whole frame (transport_passes).
+SF_TRACE_ARRAY(g_trace_trans);
+
 template <int K, int NWY, int RULE, bool CLAMP, bool EREG>
 __global__ void __launch_bounds__(32 * NWY, 1) k_trans(const __grid_constant__ FusedArgs a) {
     using C = TransCfg<K, NWY, EREG>;
@@ -903,6 +906,7 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_trans(const __grid_constant__ F
     const bool edge = cmin > 0 || cmax < RW - 1 || rmin > 0 || rmax < RH - 1;  // block-uniform
     const size_t HW = (size_t)f.H * f.W, plane = (size_t)b * HW;
     SF_PROF_DECL(a.dbg_skip & 8192);
+    SF_TRACE_BEGIN(a.dbg_skip & 16384);
 #ifdef SF_DEBUG_KNOBS
     if (a.dbg_skip & 32) return;  // launch-overhead experiment
 #endif
@@ -1052,6 +1056,7 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_trans(const __grid_constant__ F
     SF_PROF_PRINT("trans");
     const unsigned any = __reduce_or_sync(FULL, fl);
     if (lane == 0 && any) atomicOr(a.flags, any);
+    SF_TRACE_END(g_trace_trans, a.dslot);
 }
 
 // ================================================================== pyramid bottom level (NEXT #1)
@@ -1524,6 +1529,7 @@ cudaError_t launch_trans(sf_ctx* c, const float* Y, const float* D) {
         a.Y = pf ? Y : nullptr;  // L2 prefetch of the update's inputs by the first launch
         a.D = pf ? D : nullptr;
         a.rk = l == 0 ? c->rk : nullptr;  // (state k is read by the first launch only)
+        a.dslot = c->dbg_frame;
         a.G0 = c->G0;
         a.E = c->E;
         a.flags = c->flags;
@@ -1596,8 +1602,10 @@ cudaError_t sf_launch_fused_step(sf_ctx* c, const float* Y, const float* D) {
     if (fused_mono()) return fused_cfg() == 1 ? launch_cfg<4, 18>(c, Y, D) : launch_cfg<6, 12>(c, Y, D);
     cudaError_t e = sf_launch_predict_fused(c, Y, D);
     if (e != cudaSuccess) return e;
-    return sf_launch_update_fused(c, Y, D, c->pred, c->rk, 1, c->yhat[c->cur], 1, c->state[1 - c->cur],
-                                  c->yhat[1 - c->cur]);
+    e = sf_launch_update_fused(c, Y, D, c->pred, c->rk, 1, c->yhat[c->cur], 1, c->state[1 - c->cur],
+                               c->yhat[1 - c->cur]);
+    ++c->dbg_frame;
+    return e;
 }
 
 bool sf_low_fused_supported(const sf_ctx* c) {
@@ -1606,5 +1614,14 @@ bool sf_low_fused_supported(const sf_ctx* c) {
 }
 
 int sf_low_fused_launches(const sf_ctx* c) { return (c->fp.N + MMAX - 1) / MMAX; }
+
+#ifdef SF_DEBUG_KNOBS
+// Debug builds: the k_trans per-CTA timeline of trace slot `slot` (n CTAs x (entry ns, exit ns,
+// by << 32 | bx << 16 | smid)).
+extern "C" int sf_debug_trace_trans(int slot, unsigned long long* out, int n) {
+    return cudaMemcpyFromSymbol(out, g_trace_trans, sizeof(unsigned long long) * 3 * n,
+                                sizeof(unsigned long long) * 3 * 4096 * (slot & 3)) == cudaSuccess ? 0 : -1;
+}
+#endif
 
 cudaError_t sf_launch_predict_low_fused(sf_ctx* c) { return launch_low<LOW_K, LOW_NWY>(c); }

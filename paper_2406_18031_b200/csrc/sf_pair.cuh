@@ -41,6 +41,36 @@ namespace sfp {
 #define SF_PROF_PRINT(name) do { } while (0)
 #endif
 
+// Per-CTA timeline (debug builds, SF_DEBUG_SKIP bit 16384): thread 0 of every CTA records the
+// globaltimer at entry and exit and its SM into slot (frame & 3) of the translation unit's trace
+// array (SF_TRACE_ARRAY), read back by that unit's sf_debug_trace_* export (tools/cta_trace.py).
+#ifdef SF_DEBUG_KNOBS
+#define SF_TRACE_ARRAY(name) __device__ unsigned long long name[4][4096][3]
+#define SF_TRACE_BEGIN(on)                                                              \
+    unsigned long long trace_t0_ = 0;                                                   \
+    const bool trace_on_ = (on);                                                        \
+    if (trace_on_ && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(trace_t0_))
+#define SF_TRACE_END(arr, slot)                                                                              \
+    do {                                                                                                     \
+        if (trace_on_ && threadIdx.x == 0) {                                                                 \
+            unsigned long long t1_;                                                                          \
+            unsigned sm_;                                                                                    \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1_));                                          \
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(sm_));                                                 \
+            const unsigned cta_ = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);           \
+            if (cta_ < 4096) {                                                                               \
+                arr[(slot) & 3][cta_][0] = trace_t0_;                                                        \
+                arr[(slot) & 3][cta_][1] = t1_;                                                              \
+                arr[(slot) & 3][cta_][2] = ((unsigned long long)blockIdx.y << 32) | (blockIdx.x << 16) | sm_; \
+            }                                                                                                \
+        }                                                                                                    \
+    } while (0)
+#else
+#define SF_TRACE_ARRAY(name)
+#define SF_TRACE_BEGIN(on)
+#define SF_TRACE_END(arr, slot) do { } while (0)
+#endif
+
 // Iterate the cells of the rectangle [r0, r1] x [c0, c1] with NT threads, row-major, full lane
 // utilisation and no per-iteration integer division.
 #define SF_FOR_RECT(r, c, R0, R1, C0, C1, NT, tid)                                                  \

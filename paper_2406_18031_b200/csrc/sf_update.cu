@@ -56,7 +56,8 @@ struct UpdArgs {
     FrameParams f;
     int TH, TW, h, MR, MG, PH, PW, P;  // P: plane stride of Y, rhohat, HG, HH (a multiple of 32 floats)
     int PF;                            // plane stride of the 6 box planes (= 12 mod 32: bank-spread)
-    int dbg;                           // SF_DEBUG_SKIP (debug builds only): 8192 = phase profile
+    int dbg;                           // SF_DEBUG_SKIP (debug builds only): 8192 = phase profile, 16384 = CTA trace
+    int dslot;                         // trace slot (frame & 3)
 };
 
 // 14 warps, one CTA per SM (<= 128 registers: 4 warps on the busiest scheduler x 32 x 128 = its 16K
@@ -114,6 +115,8 @@ struct SolveIn {
     float2 y, rk;    // Yhat and rho references
 };
 
+SF_TRACE_ARRAY(g_trace_upd);
+
 __global__ void __launch_bounds__(UPD_NT, 1) k_upd(const __grid_constant__ UpdArgs a) {
     extern __shared__ __align__(1024) float sm[];  // TMA destinations: 128-byte aligned planes
     const FrameParams& f = a.f;
@@ -136,6 +139,7 @@ __global__ void __launch_bounds__(UPD_NT, 1) k_upd(const __grid_constant__ UpdAr
     const size_t HW = (size_t)f.H * f.W, pl = (size_t)b * HW;
     const int lc0 = MG - h - 2, ncl = TW + 2 * h + 4;  // columns of Y used: SR +- 2 (depth: SR +- 1)
     SF_PROF_DECL(a.dbg & 8192);
+    SF_TRACE_BEGIN(a.dbg & 16384);
 #ifdef SF_DEBUG_KNOBS
     if (a.dbg & 32) return;  // launch-overhead experiment
 #endif
@@ -439,6 +443,7 @@ __global__ void __launch_bounds__(UPD_NT, 1) k_upd(const __grid_constant__ UpdAr
     SF_PROF_PRINT("upd");
     const unsigned any = __reduce_or_sync(FULL, fl);
     if ((tid & 31) == 0 && any) atomicOr(a.flags, any);
+    SF_TRACE_END(g_trace_upd, a.dslot);
 }
 
 // Tile shapes tried by the launcher (TW a multiple of 4).
@@ -525,6 +530,7 @@ cudaError_t sf_launch_update_fused(sf_ctx* c, const float* Y, const float* D, co
         }();
         a.dbg = dbg_env;
     }
+    a.dslot = c->dbg_frame;
     cudaLaunchConfig_t lc = {};
     lc.gridDim = dim3((f.W + a.TW - 1) / a.TW, (f.H + a.TH - 1) / a.TH, f.B);
     lc.blockDim = dim3(UPD_NT);
@@ -539,3 +545,11 @@ cudaError_t sf_launch_update_fused(sf_ctx* c, const float* Y, const float* D, co
     if (e == cudaSuccess) e = cudaGetLastError();
     return e;
 }
+
+#ifdef SF_DEBUG_KNOBS
+// Debug builds: the k_upd per-CTA timeline of trace slot `slot` (as sf_debug_trace_trans).
+extern "C" int sf_debug_trace_upd(int slot, unsigned long long* out, int n) {
+    return cudaMemcpyFromSymbol(out, g_trace_upd, sizeof(unsigned long long) * 3 * n,
+                                sizeof(unsigned long long) * 3 * 4096 * (slot & 3)) == cudaSuccess ? 0 : -1;
+}
+#endif
