@@ -896,7 +896,9 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_trans(const __grid_constant__ F
     // interior instantiation.  The tile keeps >= R rows of halo towards the grid interior.
     // Columns likewise (the column pass then replicates at lanes 0 / 31, COLFIX) when the grid is
     // at least RW wide and the right-flush origin keeps the TMA box 16-byte aligned.
-    const int ti0 = blockIdx.y * TH, tj0 = blockIdx.x * TW;
+    int tx, ty;
+    edge_first_tile(false, tx, ty);  // (the left / right tile columns run the slower COLFIX body)
+    const int ti0 = ty * TH, tj0 = tx * TW;
     const int gi0 = a.flush && f.H >= RH ? min(max(ti0 - R, 0), f.H - RH) : ti0 - R;
     const bool colfit = a.flush && f.W >= RW && (f.W & 3) == 0;
     const int gj0 = colfit ? min(max(tj0 - R, 0), f.W - RW) : tj0 - R;

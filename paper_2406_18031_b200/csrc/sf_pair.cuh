@@ -71,6 +71,41 @@ namespace sfp {
 #define SF_TRACE_END(arr, slot) do { } while (0)
 #endif
 
+// Tile of this CTA in a gridDim.x x gridDim.y tile grid, edge tiles first: CTAs are dispatched in
+// linear block order as SMs free up (the first ones onto idle SMs, where they run their prologue
+// while the previous kernel drains), and the edge tiles are the slow ones -- so the first 2 ny
+// linear indices are the left / right tile columns, then (rows_too) the top / bottom tile rows,
+// then the interior in row-major order.
+#ifndef SF_EDGE_FIRST
+#define SF_EDGE_FIRST 1
+#endif
+__device__ __forceinline__ void edge_first_tile(bool rows_too, int& tx, int& ty) {
+    const int nx = gridDim.x, ny = gridDim.y;
+    tx = blockIdx.x;
+    ty = blockIdx.y;
+    if (!SF_EDGE_FIRST || nx < 3) return;
+    int I = blockIdx.x + nx * blockIdx.y;
+    if (I < 2 * ny) {
+        tx = (I & 1) ? nx - 1 : 0;
+        ty = I >> 1;
+        return;
+    }
+    I -= 2 * ny;
+    if (rows_too && ny >= 3) {
+        if (I < 2 * (nx - 2)) {
+            tx = 1 + (I >> 1);
+            ty = (I & 1) ? ny - 1 : 0;
+            return;
+        }
+        I -= 2 * (nx - 2);
+        tx = 1 + I % (nx - 2);
+        ty = 1 + I / (nx - 2);
+        return;
+    }
+    tx = 1 + I % (nx - 2);
+    ty = I / (nx - 2);
+}
+
 // Iterate the cells of the rectangle [r0, r1] x [c0, c1] with NT threads, row-major, full lane
 // utilisation and no per-iteration integer division.
 #define SF_FOR_RECT(r, c, R0, R1, C0, C1, NT, tid)                                                  \

@@ -131,7 +131,9 @@ __global__ void __launch_bounds__(UPD_NT, 1) k_upd(const __grid_constant__ UpdAr
     float* const RP = Ys;
     uint64_t* const bar = reinterpret_cast<uint64_t*>(sm + 4 * P + 6 * PF);
     const int b = blockIdx.z;
-    const int i0 = blockIdx.y * TH, j0 = blockIdx.x * TW;
+    int tx, ty;
+    edge_first_tile(true, tx, ty);  // (edge CTAs carry the replicate fills)
+    const int i0 = ty * TH, j0 = tx * TW;
     const int oi = i0 - MR, oj = j0 - MG;  // global cell of plane cell (0, 0)
     // in-grid part of the plane (also the replicate-clamp bounds), plane coordinates
     const int rmin = max(0, -oi), rmax = min(PH - 1, f.H - 1 - oi);

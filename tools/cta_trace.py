@@ -71,6 +71,14 @@ def main():
             tail = [(int(a[i, 2] >> 16 & 0xFFFF), int(a[i, 2] >> 32), int(a[i, 2] & 0xFFFF), round(rel(a[i, 0]), 2),
                      round(rel(a[i, 1]), 2)) for i in order]
             print(f"    last to finish (bx, by, sm, entry, exit): {tail}")
+        # per-SM hand-off: entry of this kernel's CTA - exit of the previous kernel's CTA on the same SM
+        for name, prev, nxt in (("k_upd(prev)->k_trans", tprev, tr), ("k_trans->k_upd", tr, up)):
+            ex = {int(r[2] & 0xFFFF): int(r[1]) for r in prev}
+            lat = [(int(r[0]) - ex[int(r[2] & 0xFFFF)]) / 1e3 for r in nxt if int(r[2] & 0xFFFF) in ex]
+            lat = [x for x in lat if x > -50]
+            if lat:
+                print(f"  hand-off {name}: SMs {len(lat)}  latency q10/50/90/max {np.percentile(lat, 10):.2f}/"
+                      f"{np.median(lat):.2f}/{np.percentile(lat, 90):.2f}/{max(lat):.2f} us")
         gap = rel(up[:, 0].min()) - rel(tr[:, 1].max())
         print(f"  k_upd first entry - k_trans last exit: {gap:.2f} us; frame span "
               f"{rel(up[:, 1].max()):.2f} us")
