@@ -68,6 +68,15 @@ def ncu_traffic(kernel="k_fused"):
     summary (profiles/*_ncu_<kernel>.json, written by tools/ncu_summary.py), or None."""
     import glob
 
+    # per-kernel evidence of the bench workload (tools/gpu_ncu_evidence.sh -> profiles/<tag>_cfg2_<kernel>.json)
+    ev = sorted(glob.glob(os.path.join(ROOT, "profiles", f"*_cfg2_{kernel}.json")))
+    for fp in reversed(ev):
+        try:
+            d = json.load(open(fp))
+            if d.get("dram_bytes_per_launch"):
+                return {"bytes_per_launch": d["dram_bytes_per_launch"], "source": os.path.relpath(fp, ROOT)}
+        except Exception:
+            continue
     files = sorted(glob.glob(os.path.join(ROOT, "profiles", f"*_ncu_{kernel}.json")), key=os.path.getmtime)
     for fp in reversed(files):
         try:

@@ -105,6 +105,7 @@ def main():
     ap.add_argument("--algo-ops", type=float, default=None, help="algorithmic FP32 ops per pixel per launch")
     ap.add_argument("--tag", required=True)
     ap.add_argument("--label", default=None)
+    ap.add_argument("--name", default=None, help="json name (default: the kernel's), e.g. cfg2_k_trans")
     ap.add_argument("--peaks", default=os.path.join(ROOT, "MEASURED_PEAKS.json"))
     a = ap.parse_args()
     pk = json.load(open(a.peaks)) if os.path.exists(a.peaks) else {}
@@ -143,7 +144,7 @@ def main():
         "note": "ncu --set full --clock-control none (replayed, cache-flushed: cold L2; durations are "
                 "serialised single launches); FP32 lane-ops from the SASS source page (FADD2/FMUL2/FFMA2 x2)",
     }
-    name = re.sub(r"[^A-Za-z0-9_]+", "_", caps[0]["kernel"]).strip("_")
+    name = a.name or re.sub(r"[^A-Za-z0-9_]+", "_", caps[0]["kernel"]).strip("_")
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
     json.dump(out, open(os.path.join(ROOT, "profiles", f"{a.tag}_{name}.json"), "w"), indent=1)
     md = os.path.join(ROOT, "profiles", f"{a.tag}_evidence.md")
