@@ -63,13 +63,13 @@ def env_rank():
     return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0)))
 
 
-def ncu_traffic(kernel="k_fused"):
+def ncu_traffic(kernel="k_fused", cid=2):
     """DRAM bytes per launch of the dominant kernel from the newest committed ncu --set full
     summary (profiles/*_ncu_<kernel>.json, written by tools/ncu_summary.py), or None."""
     import glob
 
     # per-kernel evidence of the bench workload (tools/gpu_ncu_evidence.sh -> profiles/<tag>_cfg2_<kernel>.json)
-    ev = sorted(glob.glob(os.path.join(ROOT, "profiles", f"*_cfg2_{kernel}.json")))
+    ev = sorted(glob.glob(os.path.join(ROOT, "profiles", f"*_cfg{cid}_{kernel}.json")))
     for fp in reversed(ev):
         try:
             d = json.load(open(fp))
@@ -77,6 +77,8 @@ def ncu_traffic(kernel="k_fused"):
                 return {"bytes_per_launch": d["dram_bytes_per_launch"], "source": os.path.relpath(fp, ROOT)}
         except Exception:
             continue
+    if cid != 2:
+        return None
     files = sorted(glob.glob(os.path.join(ROOT, "profiles", f"*_ncu_{kernel}.json")), key=os.path.getmtime)
     for fp in reversed(files):
         try:
@@ -447,9 +449,27 @@ def run_sf(args):
                 if i >= 5:
                     tp.append(a_ms)
                     tu.append(b_ms)
-        ktimes = {"k_trans_ms": statistics.mean(tp), "k_upd_ms": statistics.mean(tu), "frames": len(tp),
-                  "note": "sf_step_timed: CUDA events around each kernel on the context stream (no "
-                          "programmatic-launch overlap across the events), after the timed region"}
+        # average launch durations: REPS back-to-back launches of each kernel between CUDA events
+        # (consecutive launches overlap through programmatic dependent launch, as in the step)
+        REPS = 20
+        bp, bu = [], []
+        with torch.cuda.stream(s):
+            for i in range(12):
+                k = frame_of(state["i"])
+                state["i"] += 1
+                a_ms, b_ms = sf.sf_kernel_times(m.ctx, Yd[k].data_ptr(), Dd[k].data_ptr(), REPS)
+                if i >= 2:
+                    bp.append(a_ms)
+                    bu.append(b_ms)
+        ktimes = {"k_trans_ms": statistics.mean(bp), "k_upd_ms": statistics.mean(bu),
+                  "runs": len(bp), "reps": REPS,
+                  "note": f"sf_kernel_times: {REPS} back-to-back launches of each kernel between CUDA events on "
+                          "the context stream (programmatic dependent launch between consecutive launches), "
+                          "after the timed region",
+                  "single_frame": {"k_trans_ms": statistics.mean(tp), "k_upd_ms": statistics.mean(tu),
+                                   "frames": len(tp),
+                                   "note": "sf_step_timed: CUDA events around each kernel of one frame (launch "
+                                           "latency and drain included, no overlap across the events)"}}
 
     # ---- end to end through the host-buffer C-ABI call (pinned host memory), same metric
     e2e_steps = max(3, min(args.steps, 400))
@@ -511,7 +531,7 @@ def run_sf(args):
             u_ops = (109 + 27 * params.smooth_iters) * B * H * W
             t_alu = t_ops / (ktimes["k_trans_ms"] / 1e3) / 1e12
             u_alu = u_ops / (ktimes["k_upd_ms"] / 1e3) / 1e12
-            tr = ncu_traffic("k_trans")
+            tr = ncu_traffic("k_trans", cid)
             roof = {"bound": "alu", "achieved": t_alu, "peak": alu_peak, "unit": "TFLOP/s", "frac": t_alu / alu_peak,
                     "traffic": tr["bytes_per_launch"] if tr else None,
                     "traffic_source": (tr["source"] + " (ncu --set full, cache-flushed replay)") if tr else None,

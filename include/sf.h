@@ -289,6 +289,19 @@ int32_t sf_launches_per_step(const sf_ctx* ctx);
  * SF_E_CUDA. */
 sf_status sf_step_timed(sf_ctx* ctx, const float* Y_dev, const float* depth_dev, float* ms_predict, float* ms_update);
 
+/* Average launch durations of the split step's two kernels (measurement hook, DESIGN.md section
+ * 9): after a short device spin, `reps` back-to-back launches of the prediction (k_trans; each
+ * one recomputes the same w^{k+}, rho^{k+} from state k) between two CUDA events, then `reps`
+ * back-to-back launches of the update (k_upd; each one recomputes the same state k+1) between
+ * two more; consecutive launches of a kernel overlap through programmatic dependent launch as
+ * in sf_step.  *ms_predict / *ms_update receive elapsed / reps in milliseconds.  The context then
+ * holds state k+1 exactly as after one sf_step (the repeated launches are idempotent).  Y / depth
+ * as in sf_step; reps in [1, 1000].  Synchronises the stream.  Fused H = 1 contexts, initialised,
+ * no pending prediction; errors: SF_E_DATA (null pointer, reps out of range), SF_E_STATE,
+ * SF_E_UNSUPPORTED (passes kernels, pyramid), SF_E_CUDA. */
+sf_status sf_kernel_times(sf_ctx* ctx, const float* Y_dev, const float* depth_dev, int32_t reps, float* ms_predict,
+                          float* ms_update);
+
 /* Static description of a status code. */
 const char* sf_error_string(sf_status s);
 

@@ -27,7 +27,8 @@ EXPORTS = ("sf_config_default", "sf_create", "sf_destroy", "sf_predict", "sf_upd
            "sf_get_fields", "sf_set_fields", "sf_status_flags", "sf_kernel_in_use", "sf_launches_per_step",
            "sf_error_string", "sf_band_halo", "sf_band_partition", "sf_halo_exchange_peer", "sf_halo_exchange_nccl",
            "sf_nccl_unique_id", "sf_nccl_comm_init", "sf_nccl_comm_destroy", "sf_flow_px", "sf_eval", "sf_map_inputs", "sf_set_motion", "sf_step_host_async", "sf_wait",
-           "sf_step_camera", "sf_step_timed", "sf_band_halo_substep", "sf_step_banded", "sf_step_banded_nccl")
+           "sf_step_camera", "sf_step_timed", "sf_kernel_times", "sf_band_halo_substep", "sf_step_banded",
+           "sf_step_banded_nccl")
 
 
 class sf_config(C.Structure):
@@ -90,6 +91,7 @@ def _load():
     lib.sf_wait.argtypes = [P]
     lib.sf_step_camera.argtypes = [P, P, P, C.c_int32, C.c_int32, P, P]
     lib.sf_step_timed.argtypes = [P, P, P, C.POINTER(C.c_float), C.POINTER(C.c_float)]
+    lib.sf_kernel_times.argtypes = [P, P, P, C.c_int32, C.POINTER(C.c_float), C.POINTER(C.c_float)]
     lib.sf_band_halo_substep.argtypes = [C.POINTER(sf_config)]
     lib.sf_step_banded.argtypes = [P, P, P, HALO_XFER_FN, P, C.c_int32]
     lib.sf_step_banded_nccl.argtypes = [P, P, P, P, C.c_int32, C.c_int32]
@@ -97,7 +99,8 @@ def _load():
                  "sf_set_fields", "sf_status_flags", "sf_kernel_in_use", "sf_launches_per_step", "sf_band_halo",
                  "sf_band_partition", "sf_halo_exchange_peer", "sf_halo_exchange_nccl", "sf_nccl_unique_id",
                  "sf_nccl_comm_init", "sf_flow_px", "sf_eval", "sf_map_inputs", "sf_set_motion", "sf_step_host_async", "sf_wait",
-           "sf_step_camera", "sf_step_timed", "sf_band_halo_substep", "sf_step_banded", "sf_step_banded_nccl"):
+                 "sf_step_camera", "sf_step_timed", "sf_kernel_times", "sf_band_halo_substep", "sf_step_banded",
+                 "sf_step_banded_nccl"):
         getattr(lib, name).restype = C.c_int
     return lib
 
@@ -252,6 +255,15 @@ def sf_step_timed(ctx: int, Y_ptr: int, D_ptr: int):
     a, b = C.c_float(), C.c_float()
     _check(_lib.sf_step_timed(C.c_void_p(ctx), C.c_void_p(Y_ptr), C.c_void_p(D_ptr), C.byref(a), C.byref(b)),
            "sf_step_timed")
+    return a.value, b.value
+
+
+def sf_kernel_times(ctx: int, Y_ptr: int, D_ptr: int, reps: int):
+    """Average launch durations of the split step's kernels, `reps` back-to-back launches of each
+    (sf.h): returns (ms_predict, ms_update); the context advances by one frame."""
+    a, b = C.c_float(), C.c_float()
+    _check(_lib.sf_kernel_times(C.c_void_p(ctx), C.c_void_p(Y_ptr), C.c_void_p(D_ptr), int(reps), C.byref(a),
+                                C.byref(b)), "sf_kernel_times")
     return a.value, b.value
 
 

@@ -366,6 +366,37 @@ extern "C" sf_status sf_step_timed(sf_ctx* c, const float* Y, const float* D, fl
     return st;
 }
 
+extern "C" sf_status sf_kernel_times(sf_ctx* c, const float* Y, const float* D, int32_t reps, float* ms_predict,
+                                     float* ms_update) {
+    SF_NVTX("sf_kernel_times");
+    if (!c || !Y || !D || !ms_predict || !ms_update || reps < 1 || reps > 1000) return SF_E_DATA;
+    SF_DEVICE_GUARD(c);
+    if (c->levels == 2 || c->kernel != SF_KERNEL_FUSED) return SF_E_UNSUPPORTED;
+    if (!c->initialized || c->pending) return SF_E_STATE;
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    sf_status st = SF_OK;
+    for (int i = 0; i < 4 && st == SF_OK; ++i)
+        if (cudaEventCreate(&ev[i]) != cudaSuccess) st = SF_E_CUDA;
+    bool ok = st == SF_OK && sf_launch_spin(c, 100000) == cudaSuccess && cudaEventRecord(ev[0], c->stream) == cudaSuccess;
+    for (int r = 0; ok && r < reps; ++r) ok = sf_launch_predict_fused(c, Y, D) == cudaSuccess;
+    ok = ok && cudaEventRecord(ev[1], c->stream) == cudaSuccess && cudaEventRecord(ev[2], c->stream) == cudaSuccess;
+    for (int r = 0; ok && r < reps; ++r)
+        ok = sf_launch_update_fused(c, Y, D, c->pred, c->rk, 1, c->yhat[c->cur], 1, c->state[1 - c->cur],
+                                    c->yhat[1 - c->cur]) == cudaSuccess;
+    ok = ok && cudaEventRecord(ev[3], c->stream) == cudaSuccess && cudaEventSynchronize(ev[3]) == cudaSuccess &&
+         cudaEventElapsedTime(ms_predict, ev[0], ev[1]) == cudaSuccess &&
+         cudaEventElapsedTime(ms_update, ev[2], ev[3]) == cudaSuccess;
+    if (st == SF_OK && !ok) st = SF_E_CUDA;
+    if (st == SF_OK) {
+        *ms_predict /= (float)reps;
+        *ms_update /= (float)reps;
+        c->cur = 1 - c->cur;
+    }
+    for (int i = 0; i < 4; ++i)
+        if (ev[i]) cudaEventDestroy(ev[i]);
+    return st;
+}
+
 extern "C" sf_status sf_step_host(sf_ctx* c, const float* Yh, const float* Dh, float* wh, float* rh) {
     SF_NVTX("sf_step_host");
     if (!c || !Yh || !Dh) return SF_E_DATA;

@@ -183,6 +183,27 @@ def test_checkpoint_roundtrip_resumes_bitwise():
         assert np.array_equal(x, y)
 
 
+def test_kernel_times_advances_one_frame():
+    """sf_kernel_times (the bench's kernel-duration hook: back-to-back launches of each kernel)
+    leaves the context exactly one frame on, bit for bit the oracle's state."""
+    sf = _sf()
+    seq = sfgen.config_sequence(1, frames=4)
+    o = oracle.Oracle(seq.geom, seq.params, "f32")
+    m = sf.StructureFlow(seq.geom, seq.params, kernel=sf.SF_KERNEL_FUSED)
+    for k in range(4):
+        Y, D = _dev(seq.Y[k]), _dev(seq.depth[k])
+        if k == 0:
+            m.step(Y, D)
+        else:
+            tp, tu = sf.sf_kernel_times(m.ctx, Y.data_ptr(), D.data_ptr(), 3)
+            assert tp > 0 and tu > 0
+        o.step(seq.Y[k], seq.depth[k])
+    w, rho, yhat = _fields(m)
+    assert_parity(w[0], o.w, "w")
+    assert_parity(rho[0], o.rho, "rho")
+    assert_parity(yhat[0], o.yhat, "yhat")
+
+
 def test_step_host_matches_device_path():
     """The host-buffer entry point (e2e path) gives the device path's bits."""
     sf = _sf()
