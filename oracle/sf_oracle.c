@@ -29,7 +29,7 @@
  * except the full multi-frame trajectories on scenes with occlusions and an active
  * flow clamp (H = 1 and the H = 2 pyramid), which are pinned only by invariants,
  * closed-form special cases, f32-vs-f64 agreement and accuracy against the
- * rendered ground truth.
+ * rendered ground truth ("What the pins leave open").
  */
 #include <math.h>
 #include <stdint.h>
