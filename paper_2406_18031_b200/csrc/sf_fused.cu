@@ -994,6 +994,8 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_trans(const __grid_constant__ F
             const int r = r0 + k;
             if (r >= Rr && r < Rr + TH && r >= rmin && r <= rmax) {
                 const size_t g = plane + (size_t)(gi0 + r) * f.W + (gj0 + c0);
+                SF_DASSERT(!t0 || (gi0 + r >= 0 && gi0 + r < f.H && gj0 + c0 >= 0 && gj0 + c0 < f.W));
+                SF_DASSERT(!t1 || (gj0 + c0 + 1 >= 0 && gj0 + c0 + 1 < f.W));
                 if (t0) a.rk[g] = W[3][k].x;
                 if (t1) a.rk[g + 1] = W[3][k].y;
             }

@@ -41,6 +41,14 @@ namespace sfp {
 #define SF_PROF_PRINT(name) do { } while (0)
 #endif
 
+// Bounds assertions of the debug builds (SF_BUILD_DEBUG=1): a failed check traps the kernel (the
+// GPU suite run on a debug build stands in for compute-sanitizer where that is unavailable).
+#ifdef SF_DEBUG_KNOBS
+#define SF_DASSERT(cond) do { if (!(cond)) __trap(); } while (0)
+#else
+#define SF_DASSERT(cond) do { } while (0)
+#endif
+
 // Per-CTA timeline (debug builds, SF_DEBUG_SKIP bit 16384): thread 0 of every CTA records the
 // globaltimer at entry and exit and its SM into slot (frame & 3) of the translation unit's trace
 // array (SF_TRACE_ARRAY), read back by that unit's sf_debug_trace_* export (tools/cta_trace.py).

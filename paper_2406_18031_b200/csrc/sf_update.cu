@@ -100,6 +100,7 @@ __device__ __forceinline__ void fill_planes(float* p, int P, int PW, int PH, int
             c = rc0 + u - q * rcn;
         }
         const int from = iclamp(r, rmin, rmax) * PW + iclamp(c, cmin, cmax), to = r * PW + c;
+        SF_DASSERT(r >= 0 && r < PH && c >= 0 && c < PW && (r < rmin || r > rmax || c < cmin || c > cmax));
 #pragma unroll
         for (int k = 0; k < NP; ++k) p[k * P + to] = p[k * P + from];
     }
@@ -187,6 +188,7 @@ __global__ void __launch_bounds__(UPD_NT, 1) k_upd(const __grid_constant__ UpdAr
         q.sa = __ldg(a.G0 + cell);
         q.sb = __ldg(a.G0 + cell + d);
         const float* ep = a.E + (size_t)(oi + r + SF_EPAD) * a.EW + (oj + c + SF_EPAD);
+        SF_DASSERT(oi + r >= 0 && oi + r < f.H && oj + c >= 0 && oj + c < f.W && oj + c + SF_EPAD + 1 < a.EW);
         if (a.e8) {  // (a ragged pair's second cell reads the padding: in bounds, unused)
 #pragma unroll
             for (int p = 0; p < 6; ++p) q.e[p] = __ldg(reinterpret_cast<const float2*>(ep + p * a.EP));
@@ -199,6 +201,7 @@ __global__ void __launch_bounds__(UPD_NT, 1) k_upd(const __grid_constant__ UpdAr
         r = min(r, srh);
         const int c = scl + 2 * pc;
         const size_t ga = pl + (size_t)(oi + r) * f.W + (oj + c), gb = ga + (c + 1 <= sch ? 1 : 0);
+        SF_DASSERT(oi + r >= 0 && oi + r < f.H && oj + c >= 0 && oj + c + (c + 1 <= sch ? 1 : 0) < f.W);
         q.wa = a.pred[ga];
         q.wb = a.pred[gb];
         q.y = make_float2(a.yref[ga * a.ys], a.yref[gb * a.ys]);
