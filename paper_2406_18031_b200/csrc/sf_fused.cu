@@ -1104,8 +1104,11 @@ __global__ void __launch_bounds__(32 * NWY, 1) k_low(const __grid_constant__ Low
     const int c0 = 2 * lane, r0 = K * wy;
     const int b = blockIdx.z, R = a.R, TH = a.TH, TW = a.TW;
     // region placement flush with the grid border where the grid is large enough (k_trans):
-    // replicate by the row pass's run ends and by COLFIX, no replica cells
-    const int ti0 = blockIdx.y * TH, tj0 = blockIdx.x * TW;
+    // replicate by the row pass's run ends and by COLFIX, no replica cells; edge tiles first in the
+    // launch order (the COLFIX CTAs are the slow ones)
+    int tx, ty;
+    edge_first_tile(false, tx, ty);
+    const int ti0 = ty * TH, tj0 = tx * TW;
     const int gi0 = f.H >= RH ? min(max(ti0 - R, 0), f.H - RH) : ti0 - R;
     const int gj0 = (f.W >= RW && (f.W & 3) == 0) ? min(max(tj0 - R, 0), f.W - RW) : tj0 - R;
     const int Rr = ti0 - gi0, Rc = tj0 - gj0;
