@@ -306,16 +306,23 @@ static sf_status pyr_step(sf_ctx* c, const float* Y, const float* D) {
     if (st != SF_OK) return st;
     SF_TRY(cudaEventRecord(c->ev_join, ts));
     const bool init = !c->initialized;
+    // the reconstruction rides on the bottom update's last box pass where there is one (one kernel
+    // and one hand-off less on the bottom chain, the frame's critical path); else k_up2_add
+    static const bool separate = getenv("SF_PYR_UP2_SEPARATE") != nullptr;  // (A/B switch)
+    const bool fuse = !init && sf_update_low_defers(c) && !separate;
     if (init) {
         SF_TRY(sf_launch_update_low(c, Y, D, true));
     } else {
         SF_TRY(c->low_fused ? sf_launch_predict_low_fused(c) : sf_launch_predict_low(c));
-        SF_TRY(sf_launch_update_low(c, Y, D, false));
+        SF_TRY(sf_launch_update_low(c, Y, D, false, fuse));
     }
     SF_TRY(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
     const float4* w2 = c->top->state[c->top->cur];
     const int nxt = init ? c->cur : 1 - c->cur;
-    SF_TRY(sf_launch_up2_add(c, w2, c->state[nxt], c->yhat[0], c->Wf[nxt]));
+    if (fuse)
+        SF_TRY(sf_launch_box_up2(c, w2, c->Wf[nxt]));
+    else
+        SF_TRY(sf_launch_up2_add(c, w2, c->state[nxt], c->yhat[0], c->Wf[nxt]));
     c->cur = nxt;
     c->initialized = true;
     return SF_OK;

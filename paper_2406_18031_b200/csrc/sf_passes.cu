@@ -289,8 +289,11 @@ __global__ void __launch_bounds__(BX* BY) k_update(const float* __restrict__ Y, 
 // One whole box iteration (horizontal 5-sums, then vertical 5-sums / 25; the order of k_box_h +
 // k_box_v) per launch: the block stages its (BY + 4) x (BX + 4) window (replicate border) in
 // shared memory, forms the horizontal sums of its BY + 4 rows, then the vertical sums.
+// w2 (optional, pyramid bottom level): the last box pass also writes the reconstruction
+// wf = (up(w2) + dw, Yhat) of its cells (the k_up2_add of the frame, reading 25).
 __global__ void __launch_bounds__(BX* BY) k_box(const float4* __restrict__ in, float4* __restrict__ out,
-                                               FrameParams f) {
+                                               FrameParams f, const float4* __restrict__ w2 = nullptr,
+                                               const float* __restrict__ yh = nullptr, float4* wf = nullptr) {
     __shared__ float3 win[BY + 4][BX + 4];
     __shared__ float3 hs[BY + 4][BX];
     const int tx = threadIdx.x, ty = threadIdx.y, b = blockIdx.z;
@@ -325,7 +328,9 @@ __global__ void __launch_bounds__(BX* BY) k_box(const float4* __restrict__ in, f
         a.z = xadd(a.z, v.z);
     }
     const size_t p = ((size_t)b * f.H + i) * f.W + j;
-    out[p] = make_float4(div25(a.x), div25(a.y), div25(a.z), in[p].w);
+    const float4 o = make_float4(div25(a.x), div25(a.y), div25(a.z), in[p].w);
+    out[p] = o;
+    if (w2) wf[p] = up2_add_at(w2 + (size_t)b * (f.H / 2) * (f.W / 2), i, j, f.H, f.W, o, yh[p]);
 }
 
 __global__ void k_unpack(const float4* __restrict__ src, float* w, float* rho, size_t n) {
@@ -457,7 +462,20 @@ cudaError_t sf_launch_predict_low(sf_ctx* c) {
 // Update [dU] (reading 28): the H = 1 solve with prior dw^{k+}, references Yhat^{k+}
 // (Wpred.w) and rho^{k+} (pred.w), S box passes on dw, fusion -> state[1 - cur]; Yhat^{k+1} ->
 // yhat[0] (consumed by the reconstruction).  init: dw = 0, rho = rhohat, Yhat = Yhat(Y).
-cudaError_t sf_launch_update_low(sf_ctx* c, const float* Y, const float* D, bool init) {
+// The bottom-level update's last box pass can carry the reconstruction (sf_launch_box_up2) when
+// the update runs on the per-pass kernels with S >= 1.
+bool sf_update_low_defers(const sf_ctx* c) { return !c->upd_fused && c->fp.S > 0; }
+
+cudaError_t sf_launch_box_up2(sf_ctx* c, const float4* w2, float4* wf) {
+    const FrameParams& f = c->fp;
+    const int s = f.S - 1;
+    const float4* src = (s & 1) ? c->tmp2 : c->tmp;
+    k_box<<<grid_for(f), dim3(BX, BY), 0, c->stream>>>(src, c->state[1 - c->cur], f, w2, c->yhat[0], wf);
+    return cudaGetLastError();
+}
+
+// defer_last (sf_update_low_defers): the last box pass is left to sf_launch_box_up2.
+cudaError_t sf_launch_update_low(sf_ctx* c, const float* Y, const float* D, bool init, bool defer_last) {
     const FrameParams& f = c->fp;
     const dim3 g = grid_for(f), blk(BX, BY);
     if (init) {
@@ -472,7 +490,7 @@ cudaError_t sf_launch_update_low(sf_ctx* c, const float* Y, const float* D, bool
     float4* solved = f.S > 0 ? c->tmp : nxt;
     k_update<<<g, blk, 0, c->stream>>>(Y, D, c->pred, c->pred, reinterpret_cast<const float*>(c->Wpred) + 3, 4,
                                        c->yhat[0], solved, c->G0, c->G1, c->G2, f, c->flags);
-    for (int s = 0; s < f.S; ++s) {  // ping-pong tmp <-> tmp2, the last pass into nxt
+    for (int s = 0; s < f.S - (defer_last ? 1 : 0); ++s) {  // ping-pong tmp <-> tmp2, the last pass into nxt
         const float4* src = (s & 1) ? c->tmp2 : c->tmp;
         float4* dst = s == f.S - 1 ? nxt : ((s & 1) ? c->tmp : c->tmp2);
         k_box<<<g, blk, 0, c->stream>>>(src, dst, f);

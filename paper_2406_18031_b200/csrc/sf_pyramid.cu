@@ -32,22 +32,7 @@ __global__ void k_up2_add(const float4* __restrict__ w2, const float4* __restric
     const size_t n = (size_t)B * H * W;
     for (size_t p = blockIdx.x * (size_t)blockDim.x + threadIdx.x; p < n; p += (size_t)gridDim.x * blockDim.x) {
         const int j = (int)(p % W), i = (int)((p / W) % H), b = (int)(p / ((size_t)W * H));
-        const int I = i >> 1, J = j >> 1;
-        const int r0 = (i & 1) ? I : max(I - 1, 0), r1 = (i & 1) ? min(I + 1, Hc - 1) : I;
-        const int c0 = (j & 1) ? J : max(J - 1, 0), c1 = (j & 1) ? min(J + 1, Wc - 1) : J;
-        const float wr0 = (i & 1) ? 0.75f : 0.25f, wr1 = (i & 1) ? 0.25f : 0.75f;
-        const float wc0 = (j & 1) ? 0.75f : 0.25f, wc1 = (j & 1) ? 0.25f : 0.75f;
-        const float4* pl = w2 + (size_t)b * Hc * Wc;
-        const float4 x00 = pl[(size_t)r0 * Wc + c0], x01 = pl[(size_t)r0 * Wc + c1];
-        const float4 x10 = pl[(size_t)r1 * Wc + c0], x11 = pl[(size_t)r1 * Wc + c1];
-        auto up = [&](float a00, float a01, float a10, float a11) {
-            const float h0 = xfma(wc1, a01, xmul(a00, wc0));
-            const float h1 = xfma(wc1, a11, xmul(a10, wc0));
-            return xfma(wr1, h1, xmul(h0, wr0));
-        };
-        const float4 d = dwr[p];
-        out[p] = make_float4(xadd(up(x00.x, x01.x, x10.x, x11.x), d.x), xadd(up(x00.y, x01.y, x10.y, x11.y), d.y),
-                             xadd(up(x00.z, x01.z, x10.z, x11.z), d.z), yh[p]);
+        out[p] = up2_add_at(w2 + (size_t)b * (H / 2) * (W / 2), i, j, H, W, dwr[p], yh[p]);
     }
 }
 
