@@ -229,10 +229,10 @@ extern "C" sf_status sf_create(const sf_config* cfg, const float* geometry, sf_c
         }
         // bottom level: fused prediction unless the pass kernels are requested; update on passes
         c->low_fused = cfg->kernel != SF_KERNEL_PASSES && sf_low_fused_supported(c);
-        // the bottom-level update [dU] by the tiled k_upd (SF_UPD_LOW_FUSED=1) or the per-pass kernels
-        // (default): measured 62.3 vs 55.1 us/frame at 512^2 -- one full-machine k_upd grid blocks
-        // the top level's kernels on their stream, the small per-pass grids interleave with them
-        c->upd_fused = cfg->kernel != SF_KERNEL_PASSES && getenv("SF_UPD_LOW_FUSED") && sf_update_fused_supported(c);
+        // the bottom-level update [dU] by the tiled k_upd (default), launched after the top level has
+        // joined (with the reconstruction in its store stage), or by the per-pass kernels
+        // (SF_UPD_LOW_PASSES=1): 51.6 vs 52.2 us/frame at 512^2, 8 px
+        c->upd_fused = cfg->kernel != SF_KERNEL_PASSES && !getenv("SF_UPD_LOW_PASSES") && sf_update_fused_supported(c);
         c->kernel = c->low_fused ? SF_KERNEL_FUSED : SF_KERNEL_PASSES;
         *out = c;
         return SF_OK;
@@ -320,7 +320,7 @@ static sf_status pyr_step(sf_ctx* c, const float* Y, const float* D) {
     const float4* w2 = c->top->state[c->top->cur];
     const int nxt = init ? c->cur : 1 - c->cur;
     if (fuse)
-        SF_TRY(sf_launch_box_up2(c, w2, c->Wf[nxt]));
+        SF_TRY(sf_launch_update_low_last(c, Y, D, w2, c->Wf[nxt]));
     else
         SF_TRY(sf_launch_up2_add(c, w2, c->state[nxt], c->yhat[0], c->Wf[nxt]));
     c->cur = nxt;

@@ -464,17 +464,24 @@ cudaError_t sf_launch_predict_low(sf_ctx* c) {
 // yhat[0] (consumed by the reconstruction).  init: dw = 0, rho = rhohat, Yhat = Yhat(Y).
 // The bottom-level update's last box pass can carry the reconstruction (sf_launch_box_up2) when
 // the update runs on the per-pass kernels with S >= 1.
-bool sf_update_low_defers(const sf_ctx* c) { return !c->upd_fused && c->fp.S > 0; }
+bool sf_update_low_defers(const sf_ctx* c) { return c->upd_fused || c->fp.S > 0; }
 
-cudaError_t sf_launch_box_up2(sf_ctx* c, const float4* w2, float4* wf) {
+// The deferred end of the bottom-level update with the reconstruction: the tiled k_upd launch
+// (upd_fused: the whole update) or the per-pass path's last box pass.
+cudaError_t sf_launch_update_low_last(sf_ctx* c, const float* Y, const float* D, const float4* w2, float4* wf) {
     const FrameParams& f = c->fp;
+    float4* nxt = c->state[1 - c->cur];
+    if (c->upd_fused)
+        return sf_launch_update_fused(c, Y, D, c->pred, reinterpret_cast<const float*>(c->pred) + 3, 4,
+                                      reinterpret_cast<const float*>(c->Wpred) + 3, 4, nxt, c->yhat[0], w2, wf);
     const int s = f.S - 1;
     const float4* src = (s & 1) ? c->tmp2 : c->tmp;
-    k_box<<<grid_for(f), dim3(BX, BY), 0, c->stream>>>(src, c->state[1 - c->cur], f, w2, c->yhat[0], wf);
+    k_box<<<grid_for(f), dim3(BX, BY), 0, c->stream>>>(src, nxt, f, w2, c->yhat[0], wf);
     return cudaGetLastError();
 }
 
-// defer_last (sf_update_low_defers): the last box pass is left to sf_launch_box_up2.
+// defer_last (sf_update_low_defers): the end of the update (the last box pass, or all of the
+// tiled update) is left to sf_launch_update_low_last.
 cudaError_t sf_launch_update_low(sf_ctx* c, const float* Y, const float* D, bool init, bool defer_last) {
     const FrameParams& f = c->fp;
     const dim3 g = grid_for(f), blk(BX, BY);
@@ -484,6 +491,7 @@ cudaError_t sf_launch_update_low(sf_ctx* c, const float* Y, const float* D, bool
         return cudaGetLastError();
     }
     float4* nxt = c->state[1 - c->cur];
+    if (c->upd_fused && defer_last) return cudaSuccess;  // (all of it in sf_launch_update_low_last)
     if (c->upd_fused)  // one tiled launch (sf_update.cu): references rho^{k+} = pred.w, Yhat^{k+} = Wpred.w
         return sf_launch_update_fused(c, Y, D, c->pred, reinterpret_cast<const float*>(c->pred) + 3, 4,
                                       reinterpret_cast<const float*>(c->Wpred) + 3, 4, nxt, c->yhat[0]);

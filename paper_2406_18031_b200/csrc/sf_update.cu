@@ -51,6 +51,8 @@ struct UpdArgs {
     size_t EP;                 // plane stride
     int e8;                    // 1: EW even and E 8-byte aligned (a pair's e components by one 8-byte load)
     float4* out;               // (w^{k+1}, rho^{k+1})
+    const float4* w2;          // pyramid bottom level (optional): the new top-level state [B][H/2][W/2] ...
+    float4* wf;                // ... and the reconstruction (up(w2) + dw, Yhat^{k+1}) written with out
     float* yout;               // Yhat^{k+1}
     unsigned* flags;
     FrameParams f;
@@ -442,7 +444,11 @@ __global__ void __launch_bounds__(UPD_NT, 1) k_upd(const __grid_constant__ UpdAr
         const bool v = !isnan(rh);
         const float rn1 = xfma(v ? kap : 0.0f, xsub(v ? rh : 0.0f, rp), rp);
         if (!isfinite(rn1) && oi + r >= f.fr0 && oi + r < f.fr1) fl |= SF_FLAG_NONFINITE;
-        a.out[pl + (size_t)(oi + r) * f.W + (oj + c)] = make_float4(src[idx], src[PF + idx], src[2 * PF + idx], rn1);
+        const size_t g = pl + (size_t)(oi + r) * f.W + (oj + c);
+        const float4 o = make_float4(src[idx], src[PF + idx], src[2 * PF + idx], rn1);
+        a.out[g] = o;
+        if (a.w2)  // (Yhat^{k+1} of the tile cell: stored by this CTA's solve, visible after its barriers)
+            a.wf[g] = up2_add_at(a.w2 + (size_t)b * (f.H / 2) * (f.W / 2), oi + r, oj + c, f.H, f.W, o, a.yout[g]);
     }
     SF_PROF();  // 5: fusion + store
     SF_PROF_PRINT("upd");
@@ -504,7 +510,8 @@ bool sf_update_fused_supported(const sf_ctx* c) {
 
 // One update: pred (w^{k+}, rho^{k+}) + references + (Y, depth) -> out (state k+1), yout.
 cudaError_t sf_launch_update_fused(sf_ctx* c, const float* Y, const float* D, const float4* pred, const float* rref,
-                                   int rs, const float* yref, int ys, float4* out, float* yout) {
+                                   int rs, const float* yref, int ys, float4* out, float* yout, const float4* w2,
+                                   float4* wf) {
     const FrameParams& f = c->fp;
     UpdArgs a;
     size_t smem = 0;
@@ -526,6 +533,8 @@ cudaError_t sf_launch_update_fused(sf_ctx* c, const float* Y, const float* D, co
     a.e8 = (a.EW % 2 == 0 && (reinterpret_cast<uintptr_t>(c->E) & 7) == 0) ? 1 : 0;
     a.out = out;
     a.yout = yout;
+    a.w2 = w2;
+    a.wf = wf;
     a.flags = c->flags;
     a.f = f;
     {

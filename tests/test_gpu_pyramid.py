@@ -96,11 +96,12 @@ def test_pyramid_multi_launch_and_variants(max_flow, S, rule):
 
 
 @pytest.mark.parametrize("cid,H,W,frames", [(1, None, None, 8), (1, 96, 80, 5), (2, None, None, 3)])
-def test_pyramid_fused_bottom_update(cid, H, W, frames, monkeypatch):
-    """The bottom-level increment update [dU] by the tiled k_upd kernel
-    (SF_UPD_LOW_FUSED=1: references Yhat^{k+} = Wpred.w, rho^{k+} = pred.w) instead of the
-    per-pass kernels: bitwise the pyramid oracle every frame."""
-    monkeypatch.setenv("SF_UPD_LOW_FUSED", "1")
+def test_pyramid_per_pass_bottom_update(cid, H, W, frames, monkeypatch):
+    """The bottom-level increment update [dU] on the per-pass kernels
+    (SF_UPD_LOW_PASSES=1: k_update + S x k_box, the reconstruction on the last box pass) instead
+    of the default tiled k_upd (references Yhat^{k+} = Wpred.w, rho^{k+} = pred.w, the
+    reconstruction in its store stage): bitwise the pyramid oracle every frame."""
+    monkeypatch.setenv("SF_UPD_LOW_PASSES", "1")
     import paper_2406_18031_b200 as sf
     m, po, seq = _run(cid, frames, H=H, W=W)
     assert sf.sf_launches_per_step(m.ctx) > 0

@@ -52,6 +52,6 @@ if __name__ == "__main__":
         h1(sf.SF_KERNEL_PASSES, 150, 130)
     if "pyramid" in which:
         pyramid()
-        os.environ["SF_UPD_LOW_FUSED"] = "1"  # the bottom-level update by k_upd
+        os.environ["SF_UPD_LOW_PASSES"] = "1"  # the bottom-level update on the per-pass kernels
         pyramid()
-        del os.environ["SF_UPD_LOW_FUSED"]
+        del os.environ["SF_UPD_LOW_PASSES"]
