@@ -14,7 +14,7 @@ timeout 600 python bench.py --steps 500 --warmup 20 --kernel passes --no-cpu-bas
 timeout 600 python bench.py --levels 2 --steps 1000 --warmup 50 --no-cpu-baseline 2>&1 | tail -1 > gpurun_out/${TAG}_bench_h2.json
 timeout 600 python bench.py --map --steps 2000 --warmup 50 --no-cpu-baseline 2>&1 | tail -1 > gpurun_out/${TAG}_bench_map.json
 for c in 3 4 5; do
-  timeout 1200 python bench.py --config $c --steps 40 --warmup 8 --no-cpu-baseline 2>&1 | tail -1 > gpurun_out/${TAG}_bench_config$c.json
+  timeout 1200 python bench.py --config $c --steps 40 --warmup 8 2>&1 | tail -1 > gpurun_out/${TAG}_bench_config$c.json
 done
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv \
     --log-file gpurun_out/${TAG}_launches.csv python bench.py --steps 20 --warmup 5 --ring 8 --no-cpu-baseline > /dev/null 2>&1
