@@ -37,7 +37,7 @@ python tools/ncu_evidence.py gpurun_out/${TAG}_cfg4u.ncu-rep --kernel 'k_upd\(' 
 $NCU -k regex:'k_trans|k_upd' -s 9 -c 3 -o gpurun_out/${TAG}_cfg3 python bench.py --config 3 --steps 3 --warmup 3 --ring 4 --no-cpu-baseline > /dev/null 2>&1
 python tools/ncu_evidence.py gpurun_out/${TAG}_cfg3.ncu-rep --kernel k_trans --pixels 1048576 --algo-bytes 32 --algo-ops 416 --tag $TAG --name cfg3_k_trans --label "cfg3 1024^2 N=16 (8 substeps per launch)"
 python tools/ncu_evidence.py gpurun_out/${TAG}_cfg3.ncu-rep --kernel 'k_upd\(' --pixels 1048576 --algo-bytes 52 --algo-ops 163 --tag $TAG --name cfg3_k_upd --label "cfg3 1024^2"
-cp profiles/${TAG}_evidence.md profiles/${TAG}_*.json gpurun_out/ 2>/dev/null
+cp profiles/${TAG}_evidence.md profiles/${TAG}_cfg*_*.json profiles/${TAG}_h2top_*.json profiles/${TAG}_k_*.json gpurun_out/ 2>/dev/null
 rm -f gpurun_out/${TAG}_passes*.ncu-rep gpurun_out/${TAG}_h2.ncu-rep gpurun_out/${TAG}_map.ncu-rep gpurun_out/${TAG}_cfg4*.ncu-rep gpurun_out/${TAG}_cfg3.ncu-rep
 rm -f profiles/${TAG}_evidence.md.bak
 ls -la gpurun_out | tail -30
