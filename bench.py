@@ -682,6 +682,16 @@ def run_banded(args):
                             else "fused step + halo exchange",
                             "peak_source": f"{world} x 148 SMs x 128 FP32 lanes x {sm_max:.0f} MHz"},
                "gpu_launches": m.launches_per_step * args.steps, "e2e": None, "device_flags": flags, "clocks": clocks}
+        if world == 1 and not args.no_cpu_baseline:
+            # the float32 oracle on a bounded band of the frame (the first rows rows, 1 thread), scaled
+            # to whole 8192^2 frames
+            import types
+            rows = 256
+            sq = types.SimpleNamespace(geom=geom, params=params, Y=Yh.reshape(ring, Hb, W), depth=Dh.reshape(ring, Hb, W))
+            tr = oracle_frames(sq, 1, rows=rows)
+            out["cpu_baseline"] = {"value": 1.0 / (tr * H / rows), "unit": "Hz", "cores": 1, "kind": "oracle",
+                                   "sample": f"one frame of the first {rows} of {H} rows ({rows * W} px), float32 "
+                                             f"oracle, 1 thread, scaled to whole frames ({cpu_model()})"}
         print(json.dumps(out))
     if comm is not None:
         torch.cuda.synchronize(dev)

@@ -20,10 +20,14 @@ python tools/ncu_evidence.py gpurun_out/${TAG}_passes.ncu-rep --kernel 'k_pass<1
 python tools/ncu_evidence.py gpurun_out/${TAG}_passes_u.ncu-rep --kernel 'k_update' --pixels $PX2 --algo-bytes 56 --algo-ops 109 --tag $TAG --label "cfg2 passes"
 python tools/ncu_evidence.py gpurun_out/${TAG}_passes_u.ncu-rep --kernel 'k_box' --pixels $PX2 --algo-bytes 32 --algo-ops 27 --tag $TAG --label "cfg2 passes"
 # config 2 through the two-level pyramid (NEXT #1)
-$NCU -k regex:'k_low|k_down2|k_up2_add|k_trans|k_upd|k_update|k_box' -s 30 -c 12 -o gpurun_out/${TAG}_h2 $B --levels 2 > /dev/null 2>&1
+$NCU -k regex:'k_low|k_down2|k_up2_add|k_trans|k_update|k_box' -s 30 -c 12 -o gpurun_out/${TAG}_h2 $B --levels 2 > /dev/null 2>&1
 python tools/ncu_evidence.py gpurun_out/${TAG}_h2.ncu-rep --kernel k_low --pixels $PX2 --algo-bytes 64 --algo-ops 672 --tag $TAG --label "H=2 bottom 512^2 N=8"
 python tools/ncu_evidence.py gpurun_out/${TAG}_h2.ncu-rep --kernel k_trans --pixels 65536 --algo-bytes 32 --algo-ops 208 --tag $TAG --name h2top_k_trans --label "H=2 top 256^2 N=4"
-python tools/ncu_evidence.py gpurun_out/${TAG}_h2.ncu-rep --kernel 'k_upd\(' --pixels 65536 --algo-bytes 52 --algo-ops 217 --tag $TAG --name h2top_k_upd --label "H=2 top 256^2 S=4"
+# k_upd launches alternate top (256^2, S = 4) / bottom (512^2 [dU] + reconstruction) per frame: one capture each
+$NCU -k regex:'k_upd' -s 6 -c 1 -o gpurun_out/${TAG}_h2u_top $B --levels 2 > /dev/null 2>&1
+$NCU -k regex:'k_upd' -s 7 -c 1 -o gpurun_out/${TAG}_h2u_bot $B --levels 2 > /dev/null 2>&1
+python tools/ncu_evidence.py gpurun_out/${TAG}_h2u_top.ncu-rep --kernel 'k_upd\(' --pixels 65536 --algo-bytes 52 --algo-ops 217 --tag $TAG --name h2top_k_upd --label "H=2 top 256^2 S=4"
+python tools/ncu_evidence.py gpurun_out/${TAG}_h2u_bot.ncu-rep --kernel 'k_upd\(' --pixels $PX2 --algo-bytes 68 --algo-ops 163 --tag $TAG --name h2bot_k_upd --label "H=2 bottom 512^2 [dU] + reconstruction"
 python tools/ncu_evidence.py gpurun_out/${TAG}_h2.ncu-rep --kernel k_down2 --pixels $PX2 --algo-bytes 10 --tag $TAG --label "H=2"
 python tools/ncu_evidence.py gpurun_out/${TAG}_h2.ncu-rep --kernel k_up2_add --pixels $PX2 --algo-bytes 36 --tag $TAG --label "H=2"
 # input mapping (NEXT #2)
@@ -37,7 +41,7 @@ python tools/ncu_evidence.py gpurun_out/${TAG}_cfg4u.ncu-rep --kernel 'k_upd\(' 
 $NCU -k regex:'k_trans|k_upd' -s 9 -c 3 -o gpurun_out/${TAG}_cfg3 python bench.py --config 3 --steps 3 --warmup 3 --ring 4 --no-cpu-baseline > /dev/null 2>&1
 python tools/ncu_evidence.py gpurun_out/${TAG}_cfg3.ncu-rep --kernel k_trans --pixels 1048576 --algo-bytes 32 --algo-ops 416 --tag $TAG --name cfg3_k_trans --label "cfg3 1024^2 N=16 (8 substeps per launch)"
 python tools/ncu_evidence.py gpurun_out/${TAG}_cfg3.ncu-rep --kernel 'k_upd\(' --pixels 1048576 --algo-bytes 52 --algo-ops 163 --tag $TAG --name cfg3_k_upd --label "cfg3 1024^2"
-cp profiles/${TAG}_evidence.md profiles/${TAG}_cfg*_*.json profiles/${TAG}_h2top_*.json profiles/${TAG}_k_*.json gpurun_out/ 2>/dev/null
+cp profiles/${TAG}_evidence.md profiles/${TAG}_cfg*_*.json profiles/${TAG}_h2*_*.json profiles/${TAG}_k_*.json gpurun_out/ 2>/dev/null
 rm -f gpurun_out/${TAG}_passes*.ncu-rep gpurun_out/${TAG}_h2.ncu-rep gpurun_out/${TAG}_map.ncu-rep gpurun_out/${TAG}_cfg4*.ncu-rep gpurun_out/${TAG}_cfg3.ncu-rep
 rm -f profiles/${TAG}_evidence.md.bak
 ls -la gpurun_out | tail -30
