@@ -371,11 +371,14 @@ def run_sf(args):
     # CUDA graphs of CHUNK consecutive steps of the palindrome (an even count, so a chunk starts
     # and ends at the same state parity); the cycle of 2R steps is split into 2R / CHUNK graphs
     # replayed in order.  Steps beyond a multiple of CHUNK are direct sf_step calls.
-    CHUNK = 4
+    # (16: graph boundaries -- no programmatic launch across them -- cost ~6 us each; measured per
+    # frame 28.3 / 26.65 / 25.5 / 25.3 us for graphs of 2 / 4 / 16 / 32 steps and 25.9 us for direct,
+    # PDL-chained launches; SF_BENCH_CHUNK overrides, even)
+    CHUNK = int(os.environ.get("SF_BENCH_CHUNK", "16"))
     cycle = 2 * ring
     pos0 = ring  # palindrome position after the untimed pass over the ring
     chunks = []
-    for c in range(cycle // CHUNK):
+    for c in range(cycle // CHUNK if CHUNK > 0 else 0):
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, stream=s):
             for t in range(CHUNK):
@@ -389,7 +392,7 @@ def run_sf(args):
         """n steps continuing the palindrome: whole chunks as graph replays, the rest direct."""
         while n > 0:
             off = state["i"] - pos0
-            if n >= CHUNK and off % CHUNK == 0:
+            if CHUNK > 0 and n >= CHUNK and off % CHUNK == 0:
                 chunks[(off // CHUNK) % len(chunks)].replay()
                 state["i"] += CHUNK
                 n -= CHUNK
@@ -435,6 +438,27 @@ def run_sf(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms = float(t.item())
     st, flags = sf.sf_status_flags(m.ctx)
+
+    # ---- the same steps as direct sf_step calls (no graphs; consecutive kernels PDL-chained), the
+    # streaming mode of a real-time caller: an even number of steps, CUDA events around them
+    direct_ms = None
+    if world == 1:
+        nd = 2 * max(10, min(args.steps, 400) // 2)
+        with torch.cuda.stream(s):
+            dev0 = torch.cuda.Event(enable_timing=True)
+            dev1 = torch.cuda.Event(enable_timing=True)
+            for _ in range(20):  # warm-up of the direct path
+                k = frame_of(state["i"])
+                do_step(k)
+                state["i"] += 1
+            dev0.record(s)
+            for _ in range(nd):
+                k = frame_of(state["i"])
+                do_step(k)
+                state["i"] += 1
+            dev1.record(s)
+        torch.cuda.synchronize(dev)
+        direct_ms = dev0.elapsed_time(dev1) / nd
 
     # ---- per-kernel durations (fused H = 1): frames through sf_step_timed, CUDA events on the context
     # stream between the transport (k_trans) and the update (k_upd); the roofline's dominant kernel
@@ -565,7 +589,11 @@ def run_sf(args):
                                "inputs": f"ring of {ring} frames ({ring * 2 * frame_bytes / 2**20:.0f} MiB) > L2, "
                                          "replayed palindromically, cold reads each step",
                                "launch": f"CUDA graphs of {CHUNK} steps (each replayed once before the warm-up), "
-                                         "remainder steps launched directly"},
+                                         "remainder steps launched directly",
+                               "direct_launch_ms_per_step": direct_ms,
+                               "direct_launch_note": "the same steps as direct sf_step calls (no graphs, kernels "
+                                                     "chained by programmatic dependent launch), after the timed "
+                                                     "region"},
                "roofline": roof, "gpu_launches": launches * args.steps, "step_ms_median": med_ms,
                "e2e": {"value": e2e_value, "unit": "Hz", "h2d_bytes_per_step": 2 * frame_bytes,
                        "d2h_bytes_per_step": 4 * frame_bytes,
