@@ -9,7 +9,7 @@ N > 1 (torchrun, one process per GPU): each rank runs its own independent sequen
 data-path collective ("weak" scaling; value = frames of all ranks / max-over-ranks time).
 
 Inputs: a ring of R distinct frames resident in HBM (R x 2 MiB > the 126 MB L2), so each
-step reads cold brightness/depth; steps are replayed from CUDA graphs of 4 consecutive steps
+step reads cold brightness/depth; steps are replayed from CUDA graphs of 16 consecutive steps
 captured on the context stream.  Timing: CUDA events on that stream, barrier + synchronize on both
 sides, max over ranks.  --impl reference times the float32 CPU oracle (the only other
 place this file runs oracle/), see DESIGN.md section 9.
@@ -378,7 +378,7 @@ def run_sf(args):
     cycle = 2 * ring
     pos0 = ring  # palindrome position after the untimed pass over the ring
     chunks = []
-    for c in range(cycle // CHUNK if CHUNK > 0 else 0):
+    for c in range(cycle // CHUNK):
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, stream=s):
             for t in range(CHUNK):
@@ -392,7 +392,7 @@ def run_sf(args):
         """n steps continuing the palindrome: whole chunks as graph replays, the rest direct."""
         while n > 0:
             off = state["i"] - pos0
-            if CHUNK > 0 and n >= CHUNK and off % CHUNK == 0:
+            if n >= CHUNK and off % CHUNK == 0:
                 chunks[(off // CHUNK) % len(chunks)].replay()
                 state["i"] += CHUNK
                 n -= CHUNK
