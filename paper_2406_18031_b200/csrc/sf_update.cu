@@ -221,7 +221,6 @@ __global__ void __launch_bounds__(UPD_NT, 1) k_upd(const __grid_constant__ UpdAr
     fetch_geo(rn, pn, nx);
     fetch_geo(rm, pm, ny);
     griddep_wait();  // w^{k+} and the references come from the preceding kernels
-    griddep_launch_dependents();
     SF_PROF();  // 0: stage-0 issue + griddep
     fetch_fld(rn, pn, nx);
     fetch_fld(rm, pm, ny);
@@ -370,6 +369,9 @@ __global__ void __launch_bounds__(UPD_NT, 1) k_upd(const __grid_constant__ UpdAr
         }
     }
 
+    // the next kernel's CTAs may launch once the solve's L2-bound loads are done (triggering at the
+    // start instead: 25.52 vs 25.38 us/frame -- its prologue's loads then compete with the solve's)
+    griddep_launch_dependents();
     SF_PROF();  // 3: solve
     // ---------------- stage 3: S x 5x5 box (reading 13) as a register-tiled separable
     // stencil: one item = one component's 4-column quad over 6 output rows, read as a window of 10
